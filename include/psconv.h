@@ -1,0 +1,167 @@
+/*
+ * psconv.h — C ABI of the B200-native blocked direct-convolution forward path
+ * (the computation PolyScientist, arXiv 2002.02145, tunes: Fig. 5 of the paper).
+ *
+ * This is the drop-in boundary. Every entry point is plain C: integers, plain
+ * pointers and sizes, no C++ or torch types. Each one states the reference
+ * interface (under /root/reference/proj) it replaces.
+ *
+ * Tensor layouts are the reference's ArrayRef subscripts
+ * (include/nestrank/presets.hpp:93-97):
+ *   input  NCHW16c    [nImg][nIfm/16][ifh][ifw][16]          (c innermost)
+ *   filter KCRS16c16k [nOfm/16][nIfm/16][kh][kw][16c][16k]   (k innermost)
+ *   output NKPQ16k    [nImg][nOfm/16][ofh][ofw][16]          (k innermost)
+ * all fp32, dense, 16-byte aligned.
+ *
+ * Status codes follow the reference CLI's exit-code classes
+ * (include/nestrank/cli.hpp:290-321, README.md:86-87): 0 ok, 2 input/config
+ * error (ConfigRejectedError & co.), 1 runtime/analysis error. Nothing throws
+ * across this boundary; conv_last_error() returns the thread's last message.
+ */
+#ifndef PSCONV_H
+#define PSCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSCONV_OK 0
+#define PSCONV_ERR_RUNTIME 1 /* reference exit status 1 (analysis / runtime) */
+#define PSCONV_ERR_CONFIG 2  /* reference exit status 2 (input / config)     */
+
+/* Arithmetic modes of the GPU path (BASELINE.json north_star). */
+#define PSCONV_MODE_3XTF32 0 /* fp32-faithful: D += Alo*Bhi + Ahi*Blo + Ahi*Bhi */
+#define PSCONV_MODE_TF32 1   /* fast mode: one TF32 product per MAC            */
+
+/* conv_fwd flags */
+#define PSCONV_FLAG_ACCUMULATE 1u /* out += conv (the reference body is `+=`,
+                                     presets.hpp:112); default overwrites   */
+
+/*
+ * Conv-layer descriptor. Replaces nestrank::ConvPreset (presets.hpp:13-23):
+ * the first ten fields are the reference's, in the `conv:` CSV order
+ * nImg,nOfm,nIfm,ofh,ofw,kh,kw,stride_h,stride_w,gemm_block (presets.hpp:25).
+ * Extension fields (the reference has no padding, presets.hpp:88-91):
+ *   pad_h, pad_w  zero padding; 0 reproduces the reference exactly.
+ *   ifh, ifw      input extent; 0 means the reference-implied extent
+ *                 (ofh-1)*stride_h + kh - 2*pad_h (and likewise for w).
+ */
+typedef struct conv_desc {
+  int64_t nImg, nOfm, nIfm, ofh, ofw, kh, kw, stride_h, stride_w, gemm_block;
+  int64_t pad_h, pad_w, ifh, ifw;
+} conv_desc;
+
+/* Parses "conv:<10 ints>" (reference form, presets.hpp:26-50; the "conv:"
+ * prefix is optional, as in cli.hpp:54-66) or the extended forms with 12
+ * (+pad_h,pad_w) or 14 (+ifh,ifw) integers. Validates. Returns 0 or 2. */
+int conv_desc_parse(const char* text, conv_desc* out);
+
+/* Same rules as ConvPreset::validate (presets.hpp:52-58) plus the extension
+ * fields. Fills ifh/ifw when 0. Returns 0 or 2. gemm_block must be 16 for
+ * the GPU path (checked by conv_plan_create, not here). */
+int conv_desc_validate(conv_desc* d);
+
+/* Formats the descriptor back to its `conv:` string (10 ints when the
+ * extension fields are at their defaults, else 14). Returns 0, or 2 when
+ * the buffer is too small. */
+int conv_desc_format(const conv_desc* d, char* buf, size_t len);
+
+/* ---------------------------------------------------------------------------
+ * CPU microkernel with the reference's call convention. Replaces the external
+ * `gemm_microkernel(out, flt, in)` named by ConvPreset::build
+ * (presets.hpp:116-123; MicrokernelSpec loopnest.hpp:139-148): a small GEMM
+ * over the band (oi, ofm, ifm):
+ *   out[oi*16+ofm] += flt[ifm*16+ofm] * in[oi*stride_w*16+ifm]
+ * for oi < ofw. Like LIBXSMM, the shape (ofw, stride_w, block) is bound at
+ * dispatch time; the returned function takes only the three pointers.
+ */
+typedef void (*gemm_microkernel_fn)(float* out, const float* flt, const float* in);
+
+/* Returns 2 if the descriptor is invalid or gemm_block != 16, or
+ * ofw*stride_w > 4096 (no specialisation). */
+int gemm_microkernel_dispatch(const conv_desc* d, gemm_microkernel_fn* fn);
+
+/* Batch-reduce form (north_star BRGEMM): folds `count` (ifm_tile,kj,ki)
+ * blocks into one call on one output row:
+ *   for i < count: gemm_microkernel(out, flt_blocks[i], in_rows[i]). */
+int brgemm_f32(const conv_desc* d, float* out, const float* const* flt_blocks,
+               const float* const* in_rows, int64_t count);
+
+/* ---------------------------------------------------------------------------
+ * GPU layer entry (sm_100a). A plan binds a descriptor, a mode and a schedule.
+ * The schedule is chosen by the selector from the reference's recipe space
+ * (variants.hpp:16-65: "perm=...;tile=oj:T") extended with an optional GPU
+ * clause ";gpu=bn:B,box:QxPxN,st:S". recipe == NULL lets the selector choose.
+ */
+typedef struct conv_plan conv_plan;
+
+int conv_plan_create(const conv_desc* d, int mode, int device, const char* recipe_or_null,
+                     conv_plan** out);
+void conv_plan_destroy(conv_plan* p);
+
+/* The plan's recipe id in the reference's grammar plus the gpu clause. */
+const char* conv_plan_recipe(const conv_plan* p);
+
+/* Runs the forward conv on images [img_begin, img_begin+img_count) of the
+ * caller's device arrays (full-size, pointer to image 0), stream-ordered on
+ * `cuda_stream` (a cudaStream_t; NULL = legacy default). Does not allocate
+ * and does not synchronise. Reentrant. */
+int conv_fwd(const conv_plan* p, const float* in, const float* flt, float* out, int64_t img_begin,
+             int64_t img_count, void* cuda_stream, unsigned flags);
+
+/* Number of kernel launches conv_fwd issues per call (for launch accounting). */
+int conv_plan_launches(const conv_plan* p);
+
+/* Emits the plan's driver loop nest as C text in the reference emitter's
+ * format (emit.hpp:60-134; golden tests/golden/conv_identity.c). Returns the
+ * number of bytes needed (excluding NUL); writes at most len-1 bytes. */
+int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len);
+
+/* Same emission without a plan or a GPU: any reference-legal recipe
+ * (recipe NULL or "" = identity order). Returns bytes needed, or -2/-1. */
+int64_t conv_emit_driver(const conv_desc* d, const char* recipe, char* buf, size_t len);
+
+/* ---------------------------------------------------------------------------
+ * Schedule selector (the paper's reuse-model ranking, re-expressed for B200).
+ * Ranks candidate recipes for a descriptor by a closed-form SMEM/L2/HBM
+ * traffic + tensor-pipe model. Writes up to k recipe ids separated by '\n'
+ * into buf (best first) with their modelled microseconds into us_out (may be
+ * NULL). Returns the number written, or -2 / -1 on config / runtime error.
+ */
+int conv_select_topk(const conv_desc* d, int mode, int k, char* buf, size_t len, double* us_out);
+
+/* Modelled time (microseconds) of one recipe, -1 on error. */
+double conv_model_us(const conv_desc* d, int mode, const char* recipe);
+
+/* ---------------------------------------------------------------------------
+ * Device-side helpers (same stream semantics as conv_fwd).
+ * Seeded generator: value(seed, i) = (int)(splitmix64(splitmix64(seed) ^ i) >> 40) * 2^-23 - 1,
+ * i = logical NCHW (activations) or KCRS (weights) index; exactly
+ * representable in fp32 and independent of layout and sharding.
+ * c_logical < nIfm zero-fills the padded channels (ResNet-50 stem 3 -> 16). */
+int conv_fill_input(const conv_desc* d, uint64_t seed, int64_t c_logical, float* in,
+                    int64_t img_begin, int64_t img_count, void* cuda_stream);
+int conv_fill_filter(const conv_desc* d, uint64_t seed, int64_t c_logical, float* flt,
+                     void* cuda_stream);
+/* Layout packing (a9): NCHW -> NCHW16c, KCRS -> KCRS16c16k, NKPQ16k -> NKPQ. */
+int conv_pack_input(const conv_desc* d, const float* nchw, int64_t c_logical, float* nchw16c,
+                    void* cuda_stream);
+int conv_pack_filter(const conv_desc* d, const float* kcrs, int64_t c_logical, float* kcrs16c16k,
+                     void* cuda_stream);
+int conv_unpack_output(const conv_desc* d, const float* nkpq16k, float* nkpq, void* cuda_stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* conv_last_error(void);
+
+/* Library / device introspection. */
+const char* psconv_version(void);
+int psconv_device_sm_count(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSCONV_H */

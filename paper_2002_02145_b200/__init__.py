@@ -1,0 +1,265 @@
+"""B200-native blocked direct-convolution forward (the PolyScientist hot path).
+
+Python mirror of the reference's operator interface for this path, over the C
+ABI in include/psconv.h:
+
+* :class:`ConvPreset` — the conv-layer descriptor (reference
+  ``nestrank::ConvPreset``, include/nestrank/presets.hpp:13-58): same fields,
+  same ``conv:`` CSV, same validation and error class (``ConfigRejectedError``,
+  common.hpp:26 — CLI exit status 2), plus the padding / input-extent extension.
+* :class:`ConvPlan` — one layer on one GPU: a descriptor, an arithmetic mode
+  (3xTF32 fp32-faithful, or TF32) and a schedule in the reference's recipe
+  grammar (variants.hpp:16-65).
+* :func:`gemm_microkernel` — the 3-pointer CPU microkernel contract
+  (presets.hpp:116-123).
+
+The GPU path has no fallback: this package fails at import when libpsconv.so
+is missing, and ConvPlan creation fails on anything but an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, fields
+
+from . import _lib
+from ._lib import conv_desc, lib
+
+__all__ = [
+    "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
+    "MODE_TF32", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
+    "brgemm", "fill_input", "fill_filter", "version",
+]
+
+MODE_3XTF32 = 0
+MODE_TF32 = 1
+FLAG_ACCUMULATE = 1
+_MODES = {"3xtf32": MODE_3XTF32, "tf32": MODE_TF32}
+
+
+class Error(RuntimeError):
+    """Base error (reference nestrank::Error, common.hpp:11-13)."""
+
+
+class ConfigRejectedError(Error):
+    """Input / config error: status 2 (reference ConfigRejectedError & co.)."""
+
+
+class AnalysisError(Error):
+    """Runtime / analysis error: status 1."""
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (lib.conv_last_error() or b"").decode()
+    if rc == 2:
+        raise ConfigRejectedError(msg)
+    raise AnalysisError(msg or f"psconv error {rc}")
+
+
+def version() -> str:
+    return lib.psconv_version().decode()
+
+
+@dataclass
+class ConvPreset:
+    """Conv-layer descriptor; field order = the reference ``conv:`` CSV order."""
+    nImg: int = 2
+    nOfm: int = 32
+    nIfm: int = 32
+    ofh: int = 4
+    ofw: int = 4
+    kh: int = 3
+    kw: int = 3
+    stride_h: int = 1
+    stride_w: int = 1
+    gemm_block: int = 16
+    pad_h: int = 0
+    pad_w: int = 0
+    ifh: int = 0
+    ifw: int = 0
+
+    # -- reference interface -------------------------------------------------
+    @classmethod
+    def parse(cls, csv: str) -> "ConvPreset":
+        """``conv:nImg,...,gemm_block[,pad_h,pad_w[,ifh,ifw]]`` (presets.hpp:26-50)."""
+        d = conv_desc()
+        _check(lib.conv_desc_parse(csv.encode(), ctypes.byref(d)))
+        return cls._from_c(d)
+
+    def validate(self) -> "ConvPreset":
+        d = self.to_c()
+        _check(lib.conv_desc_validate(ctypes.byref(d)))
+        self.ifh, self.ifw = d.ifh, d.ifw
+        return self
+
+    # -- helpers ---------------------------------------------------------------
+    @classmethod
+    def _from_c(cls, d: conv_desc) -> "ConvPreset":
+        return cls(**{f.name: int(getattr(d, f.name)) for f in fields(cls)})
+
+    def to_c(self) -> conv_desc:
+        return conv_desc(**{f.name: int(getattr(self, f.name)) for f in fields(self)})
+
+    def __str__(self) -> str:
+        d = self.to_c()
+        buf = ctypes.create_string_buffer(512)
+        _check(lib.conv_desc_format(ctypes.byref(d), buf, len(buf)))
+        return buf.value.decode()
+
+    @property
+    def csv10(self) -> str:
+        return ",".join(str(getattr(self, n)) for n in (
+            "nImg", "nOfm", "nIfm", "ofh", "ofw", "kh", "kw", "stride_h", "stride_w", "gemm_block"))
+
+    def flops(self, c_logical: int | None = None, n_img: int | None = None) -> int:
+        """Algorithmic FLOPs 2*N*K*C*P*Q*R*S (logical C)."""
+        c = c_logical or self.nIfm
+        n = self.nImg if n_img is None else n_img
+        return 2 * n * self.nOfm * c * self.ofh * self.ofw * self.kh * self.kw
+
+    def input_elems(self, n_img: int | None = None) -> int:
+        v = self.validate()
+        return (self.nImg if n_img is None else n_img) * v.nIfm * v.ifh * v.ifw
+
+    def filter_elems(self) -> int:
+        return self.nOfm * self.nIfm * self.kh * self.kw
+
+    def output_elems(self, n_img: int | None = None) -> int:
+        return (self.nImg if n_img is None else n_img) * self.nOfm * self.ofh * self.ofw
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:  # noqa: BLE001
+            return 0
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+
+
+class ConvPlan:
+    """One conv layer bound to a device, a mode and a schedule (recipe)."""
+
+    def __init__(self, preset: ConvPreset, mode="3xtf32", device: int = 0,
+                 recipe: str | None = None):
+        if isinstance(mode, str):
+            mode = _MODES[mode.lower()]
+        self.preset = ConvPreset(**{f.name: getattr(preset, f.name) for f in fields(preset)}).validate()
+        self.mode = mode
+        self.device = device
+        self._d = self.preset.to_c()
+        h = ctypes.c_void_p()
+        _check(lib.conv_plan_create(ctypes.byref(self._d), mode, device,
+                                    recipe.encode() if recipe else None, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def recipe(self) -> str:
+        return lib.conv_plan_recipe(self._h).decode()
+
+    @property
+    def launches(self) -> int:
+        return lib.conv_plan_launches(self._h)
+
+    def emit(self) -> str:
+        n = lib.conv_plan_emit(self._h, None, 0)
+        if n < 0:
+            _check(int(-n))
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        lib.conv_plan_emit(self._h, buf, len(buf))
+        return buf.value.decode()
+
+    def forward(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
+                stream=None, accumulate: bool = False) -> None:
+        """Device pointers or CUDA tensors in NCHW16c / KCRS16c16k / NKPQ16k."""
+        if img_count is None:
+            img_count = self.preset.nImg - img_begin
+        _check(lib.conv_fwd(self._h, _ptr(inp), _ptr(flt), _ptr(out), img_begin, img_count,
+                            _stream_ptr(stream), FLAG_ACCUMULATE if accumulate else 0))
+
+    __call__ = forward
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.conv_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def emit_driver(preset: ConvPreset, recipe: str | None = None) -> str:
+    """Driver loop nest text in the reference emitter's format (emit.hpp:60-134)."""
+    d = preset.to_c()
+    rc = lib.conv_emit_driver(ctypes.byref(d), recipe.encode() if recipe else None, None, 0)
+    if rc < 0:
+        _check(int(-rc))
+    buf = ctypes.create_string_buffer(int(rc) + 1)
+    lib.conv_emit_driver(ctypes.byref(d), recipe.encode() if recipe else None, buf, len(buf))
+    return buf.value.decode()
+
+
+def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5):
+    """Model-ranked recipes, best first: [(recipe, modelled_us), ...]."""
+    if isinstance(mode, str):
+        mode = _MODES[mode.lower()]
+    d = preset.to_c()
+    buf = ctypes.create_string_buffer(1 << 16)
+    us = (ctypes.c_double * k)()
+    n = lib.conv_select_topk(ctypes.byref(d), mode, k, buf, len(buf), us)
+    if n < 0:
+        _check(-n)
+    ids = buf.value.decode().split("\n") if n else []
+    return list(zip(ids, [us[i] for i in range(n)]))
+
+
+def model_us(preset: ConvPreset, recipe: str, mode="3xtf32") -> float:
+    if isinstance(mode, str):
+        mode = _MODES[mode.lower()]
+    d = preset.to_c()
+    v = lib.conv_model_us(ctypes.byref(d), mode, recipe.encode())
+    if v < 0:
+        _check(2)
+    return v
+
+
+def gemm_microkernel(preset: ConvPreset):
+    """The dispatched 3-pointer CPU microkernel (a ctypes function)."""
+    d = preset.to_c()
+    fn = _lib.gemm_microkernel_fn()
+    _check(lib.gemm_microkernel_dispatch(ctypes.byref(d), ctypes.byref(fn)))
+    return fn
+
+
+def brgemm(preset: ConvPreset, out_ptr: int, flt_ptrs, in_ptrs) -> None:
+    d = preset.to_c()
+    n = len(flt_ptrs)
+    fa = (ctypes.c_void_p * n)(*flt_ptrs)
+    ia = (ctypes.c_void_p * n)(*in_ptrs)
+    _check(lib.brgemm_f32(ctypes.byref(d), out_ptr, fa, ia, n))
+
+
+def fill_input(preset: ConvPreset, seed: int, inp, c_logical: int = 0, img_begin: int = 0,
+               img_count: int | None = None, stream=None) -> None:
+    """Seeded uniform[-1,1) activations on the device (NCHW16c, logical-index keyed)."""
+    d = preset.to_c()
+    if img_count is None:
+        img_count = preset.nImg - img_begin
+    _check(lib.conv_fill_input(ctypes.byref(d), seed, c_logical, _ptr(inp), img_begin, img_count,
+                               _stream_ptr(stream)))
+
+
+def fill_filter(preset: ConvPreset, seed: int, flt, c_logical: int = 0, stream=None) -> None:
+    d = preset.to_c()
+    _check(lib.conv_fill_filter(ctypes.byref(d), seed, c_logical, _ptr(flt), _stream_ptr(stream)))

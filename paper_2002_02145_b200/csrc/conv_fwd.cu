@@ -1,0 +1,498 @@
+// GPU layer entry: plans, tensor maps, launches, and the device-side helpers
+// (seeded generator, layout packing, 3xTF32 weight split).
+//
+// Replaces the reference's driver loop nest (emit_source, include/nestrank/
+// emit.hpp:60-134) + the external LIBXSMM microkernel with
+// one persistent sm_100a kernel per conv_fwd call.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "conv_kernel.cuh"
+#include "internal.hpp"
+#include "seeded.hpp"
+
+struct conv_plan {
+  conv_desc d;
+  int mode;
+  int device;
+  int num_sms;
+  psconv::Schedule sched;
+  float* flt_pack = nullptr;   // prepacked K-major filter [CRS][K][16c]: hi (| lo for 3xTF32)
+  int64_t flt_elems = 0;
+};
+
+namespace psconv {
+namespace {
+
+#define CUDA_OK(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw RuntimeError(std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw RuntimeError("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+void encode(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
+            const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr) {
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base),
+                                 dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw RuntimeError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+// ---------------------------------------------------------------- helpers
+// Filter prepack: KCRS16c16k [Kb][C*R*S/16 blocks][16c][16k] -> K-major
+// [CRS][K][16c] (one 64-B row of 16 input channels per output channel), which
+// is the B-operand layout tcgen05 kind::tf32 accepts (K-major SWIZZLE_64B).
+// 3xTF32: also split x -> hi = x with the 13 low mantissa bits cleared
+// (exactly representable in tf32) and lo = x - hi (exact in fp32).
+// One 256-thread block per 16x16 [c][k] block, transposed through smem.
+__global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __restrict__ hi,
+                                      float* __restrict__ lo, int K, int CRS, int split) {
+  __shared__ float tile[16][17];
+  const int blk = blockIdx.x;  // = kb * CRS + crs
+  const int kb = blk / CRS, crs = blk % CRS;
+  const int t = threadIdx.x;
+  tile[t >> 4][t & 15] = flt[static_cast<int64_t>(blk) * 256 + t];  // [c][k]
+  __syncthreads();
+  const int k16 = t >> 4, c16 = t & 15;
+  const float x = tile[c16][k16];
+  const int64_t o = (static_cast<int64_t>(crs) * K + kb * 16 + k16) * 16 + c16;
+  if (split) {
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    hi[o] = h;
+    lo[o] = x - h;
+  } else {
+    hi[o] = x;
+  }
+}
+
+// NCHW16c element e (relative to image img_begin) <- value(seed, logical NCHW index)
+__global__ void fill_input_kernel(float* __restrict__ out, uint64_t seed, int64_t n_elems,
+                                  int64_t img_begin, int Cb, int H, int W, int c_logical) {
+  const uint64_t key = seeded::mix(seed);
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int w = int(t % W);
+    t /= W;
+    const int h = int(t % H);
+    t /= H;
+    const int cb = int(t % Cb);
+    const int64_t n = t / Cb + img_begin;
+    const int c = cb * 16 + c16;
+    float v = 0.f;
+    if (c < c_logical) v = seeded::value(key, ((n * c_logical + c) * H + h) * W + w);
+    out[e] = v;
+  }
+}
+
+// KCRS16c16k element e <- value(seed, logical KCRS index)
+__global__ void fill_filter_kernel(float* __restrict__ out, uint64_t seed, int64_t n_elems,
+                                   int Cb, int R, int S, int c_logical) {
+  const uint64_t key = seeded::mix(seed);
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int k16 = int(t & 15);
+    t >>= 4;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int s = int(t % S);
+    t /= S;
+    const int r = int(t % R);
+    t /= R;
+    const int cb = int(t % Cb);
+    const int64_t kb = t / Cb;
+    const int c = cb * 16 + c16;
+    const int64_t k = kb * 16 + k16;
+    float v = 0.f;
+    if (c < c_logical) v = seeded::value(key, ((k * c_logical + c) * R + r) * S + s);
+    out[e] = v;
+  }
+}
+
+__global__ void pack_input_kernel(const float* __restrict__ nchw, float* __restrict__ out,
+                                  int64_t n_elems, int Cb, int H, int W, int c_logical) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int w = int(t % W);
+    t /= W;
+    const int h = int(t % H);
+    t /= H;
+    const int cb = int(t % Cb);
+    const int64_t n = t / Cb;
+    const int c = cb * 16 + c16;
+    out[e] = c < c_logical ? nchw[((n * c_logical + c) * H + h) * W + w] : 0.f;
+  }
+}
+
+__global__ void pack_filter_kernel(const float* __restrict__ kcrs, float* __restrict__ out,
+                                   int64_t n_elems, int Cb, int R, int S, int c_logical) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int k16 = int(t & 15);
+    t >>= 4;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int s = int(t % S);
+    t /= S;
+    const int r = int(t % R);
+    t /= R;
+    const int cb = int(t % Cb);
+    const int64_t kb = t / Cb;
+    const int c = cb * 16 + c16;
+    const int64_t k = kb * 16 + k16;
+    out[e] = c < c_logical ? kcrs[((k * c_logical + c) * R + r) * S + s] : 0.f;
+  }
+}
+
+__global__ void unpack_output_kernel(const float* __restrict__ in16, float* __restrict__ nkpq,
+                                     int64_t n_elems, int Kb, int PQ) {
+  // element e of NKPQ: ((n*K + k)*PQ + pq)
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int pq = int(t % PQ);
+    t /= PQ;
+    const int k = int(t % (Kb * 16));
+    const int64_t n = t / (Kb * 16);
+    nkpq[e] = in16[((n * Kb + k / 16) * PQ + pq) * 16 + (k & 15)];
+  }
+}
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+// ---------------------------------------------------------------- launch
+template <int BN, bool SPLIT3>
+void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
+                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+  using Cfg = KernelCfg<BN, SPLIT3>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+  });
+  CUDA_OK(attr_err);
+  int grid = prm.num_tiles < P->num_sms ? prm.num_tiles : P->num_sms;
+  conv_fwd_sm100<BN, SPLIT3><<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(prm, a, b, blo);
+  CUDA_OK(cudaGetLastError());
+}
+
+template <bool SPLIT3>
+void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
+                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+  switch (bn) {
+    case 16: return launch_conv<16, SPLIT3>(P, prm, a, b, blo, st);
+    case 32: return launch_conv<32, SPLIT3>(P, prm, a, b, blo, st);
+    case 64: return launch_conv<64, SPLIT3>(P, prm, a, b, blo, st);
+    case 128: return launch_conv<128, SPLIT3>(P, prm, a, b, blo, st);
+    case 256: return launch_conv<256, SPLIT3>(P, prm, a, b, blo, st);
+    default: throw RuntimeError("unsupported bn");
+  }
+}
+
+}  // namespace
+}  // namespace psconv
+
+using namespace psconv;
+
+extern "C" {
+
+int psconv_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* recipe,
+                     conv_plan** out) {
+  return guarded([&] {
+    if (!d_in || !out) throw ConfigError("null argument");
+    *out = nullptr;
+    if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32)
+      throw ConfigError("unknown mode " + std::to_string(mode));
+    conv_desc d = *d_in;
+    validate_desc(d);
+    Recipe r;
+    Schedule s;
+    if (recipe && *recipe) {
+      r = Recipe::parse(recipe);
+      s = resolve_schedule(d, r, mode);
+    } else {
+      const auto cands = candidate_schedules(d, mode);
+      if (cands.empty()) throw ConfigError("no GPU schedule for this descriptor");
+      double best = 1e300;
+      for (const auto& c : cands) {
+        const double us = model_schedule(d, c, mode).us_total;
+        if (us < best) {
+          best = us;
+          s = c;
+        }
+      }
+    }
+    int ndev = 0;
+    CUDA_OK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ConfigError("invalid device " + std::to_string(device));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+      throw RuntimeError("psconv kernels are built for sm_100a; device is sm_" +
+                         std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* P = new conv_plan();
+    P->d = d;
+    P->mode = mode;
+    P->device = device;
+    P->num_sms = prop.multiProcessorCount;
+    P->sched = s;
+    P->flt_elems = d.nOfm * d.nIfm * d.kh * d.kw;
+    {
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(device);
+      const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
+      const cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
+      cudaSetDevice(prev);
+      if (e != cudaSuccess) {
+        delete P;
+        throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+      }
+    }
+    *out = P;
+  });
+}
+
+void conv_plan_destroy(conv_plan* p) {
+  if (!p) return;
+  if (p->flt_pack) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    cudaFree(p->flt_pack);
+    cudaSetDevice(prev);
+  }
+  delete p;
+}
+
+const char* conv_plan_recipe(const conv_plan* p) { return p ? p->sched.recipe_id.c_str() : ""; }
+
+int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len) {
+  int64_t need = -1;
+  const int rc = guarded([&] {
+    if (!p) throw ConfigError("null plan");
+    const std::string txt = emit_driver(p->d, p->sched);
+    need = static_cast<int64_t>(txt.size());
+    if (buf && len) {
+      const size_t n = txt.size() < len - 1 ? txt.size() : len - 1;
+      std::memcpy(buf, txt.data(), n);
+      buf[n] = 0;
+    }
+  });
+  return rc == PSCONV_OK ? need : -rc;
+}
+
+int conv_plan_launches(const conv_plan* p) {
+  return p ? 2 : 0;  // filter prepack + conv
+}
+
+int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_begin,
+             int64_t img_count, void* stream, unsigned flags) {
+  return guarded([&] {
+    if (!P) throw ConfigError("null plan");
+    if (!in || !flt || !out) throw ConfigError("null tensor pointer");
+    const conv_desc& d = P->d;
+    if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
+      throw ConfigError("image range [" + std::to_string(img_begin) + ", " +
+                        std::to_string(img_begin + img_count) + ") outside nImg=" +
+                        std::to_string(d.nImg));
+    if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(flt) |
+         reinterpret_cast<uintptr_t>(out)) & 15)
+      throw ConfigError("tensor pointers must be 16-byte aligned");
+    if (img_count == 0) return;
+    const Schedule& s = P->sched;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int Cb = int(d.nIfm / 16), Kb = int(d.nOfm / 16);
+    const int H = int(d.ifh), W = int(d.ifw), R = int(d.kh), S = int(d.kw);
+    const int Pp = int(d.ofh), Q = int(d.ofw);
+    const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+
+    // A: input viewed as [img_count][Cb][H][W][16], starting at img_begin
+    CUtensorMap ta, tb, tblo;
+    {
+      const float* base = in + img_begin * int64_t(Cb) * H * W * 16;
+      const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(Cb),
+                                  cuuint64_t(img_count)};
+      const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(H) * W * 64,
+                                     cuuint64_t(Cb) * H * W * 64};
+      const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
+                                 1, cuuint32_t(s.nb)};
+      const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
+      encode(&ta, base, 5, dims, strides, box, estr);
+    }
+    // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
+    const int CRS = Cb * R * S;
+    const int K = Kb * 16;
+    const float* b_hi = P->flt_pack;
+    const float* b_lo = split3 ? P->flt_pack + P->flt_elems : P->flt_pack;
+    prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
+                                                    split3 ? P->flt_pack + P->flt_elems : nullptr, K,
+                                                    CRS, split3 ? 1 : 0);
+    CUDA_OK(cudaGetLastError());
+    {
+      const cuuint64_t dims[3] = {16, cuuint64_t(K), cuuint64_t(CRS)};
+      const cuuint64_t strides[2] = {64, cuuint64_t(K) * 64};
+      const cuuint32_t box[3] = {16, cuuint32_t(s.bn), 1};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      encode(&tb, b_hi, 3, dims, strides, box, estr);
+      encode(&tblo, b_lo, 3, dims, strides, box, estr);
+    }
+    ConvParams prm{};
+    prm.img_count = int(img_count);
+    prm.Cb = Cb;
+    prm.H = H;
+    prm.W = W;
+    prm.Kb = Kb;
+    prm.P = Pp;
+    prm.Q = Q;
+    prm.R = R;
+    prm.S = S;
+    prm.sh = int(d.stride_h);
+    prm.sw = int(d.stride_w);
+    prm.ph = int(d.pad_h);
+    prm.pw = int(d.pad_w);
+    prm.Qb = s.qb;
+    prm.Pb = s.pb;
+    prm.Nb = s.nb;
+    prm.tiles_q = (Q + s.qb - 1) / s.qb;
+    prm.tiles_p = (Pp + s.pb - 1) / s.pb;
+    prm.tiles_n = int((img_count + s.nb - 1) / s.nb);
+    prm.tiles_k = int(d.nOfm / s.bn);
+    const int64_t nt = int64_t(prm.tiles_q) * prm.tiles_p * prm.tiles_n * prm.tiles_k;
+    if (nt >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
+    prm.num_tiles = int(nt);
+    prm.ksteps = Cb * R * S;
+    prm.chunk_ksteps = s.chunk > 0 ? s.chunk : prm.ksteps;
+    for (int i = 0; i < 3; ++i) {
+      prm.raster[i] = s.raster[i];
+      prm.kord[i] = s.kord[i];
+    }
+    prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
+    prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
+    prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
+    if (split3)
+      dispatch_bn<true>(s.bn, P, prm, ta, tb, tblo, st);
+    else
+      dispatch_bn<false>(s.bn, P, prm, ta, tb, tblo, st);
+  });
+}
+
+int conv_fill_input(const conv_desc* d_in, uint64_t seed, int64_t c_logical, float* in,
+                    int64_t img_begin, int64_t img_count, void* stream) {
+  return guarded([&] {
+    if (!d_in || !in) throw ConfigError("null argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    if (c_logical <= 0 || c_logical > d.nIfm) c_logical = d.nIfm;
+    if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
+      throw ConfigError("image range outside nImg");
+    const int64_t n = img_count * d.nIfm * d.ifh * d.ifw;
+    if (n == 0) return;
+    fill_input_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        in + img_begin * d.nIfm * d.ifh * d.ifw, seed, n, img_begin, int(d.nIfm / 16),
+        int(d.ifh), int(d.ifw), int(c_logical));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int conv_fill_filter(const conv_desc* d_in, uint64_t seed, int64_t c_logical, float* flt,
+                     void* stream) {
+  return guarded([&] {
+    if (!d_in || !flt) throw ConfigError("null argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    if (c_logical <= 0 || c_logical > d.nIfm) c_logical = d.nIfm;
+    const int64_t n = d.nOfm * d.nIfm * d.kh * d.kw;
+    fill_filter_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        flt, seed, n, int(d.nIfm / 16), int(d.kh), int(d.kw), int(c_logical));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int conv_pack_input(const conv_desc* d_in, const float* nchw, int64_t c_logical, float* out,
+                    void* stream) {
+  return guarded([&] {
+    if (!d_in || !nchw || !out) throw ConfigError("null argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    if (c_logical <= 0 || c_logical > d.nIfm) c_logical = d.nIfm;
+    const int64_t n = d.nImg * d.nIfm * d.ifh * d.ifw;
+    pack_input_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        nchw, out, n, int(d.nIfm / 16), int(d.ifh), int(d.ifw), int(c_logical));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int conv_pack_filter(const conv_desc* d_in, const float* kcrs, int64_t c_logical, float* out,
+                     void* stream) {
+  return guarded([&] {
+    if (!d_in || !kcrs || !out) throw ConfigError("null argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    if (c_logical <= 0 || c_logical > d.nIfm) c_logical = d.nIfm;
+    const int64_t n = d.nOfm * d.nIfm * d.kh * d.kw;
+    pack_filter_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        kcrs, out, n, int(d.nIfm / 16), int(d.kh), int(d.kw), int(c_logical));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int conv_unpack_output(const conv_desc* d_in, const float* nkpq16k, float* nkpq, void* stream) {
+  return guarded([&] {
+    if (!d_in || !nkpq16k || !nkpq) throw ConfigError("null argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    const int64_t n = d.nImg * d.nOfm * d.ofh * d.ofw;
+    unpack_output_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        nkpq16k, nkpq, n, int(d.nOfm / 16), int(d.ofh * d.ofw));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

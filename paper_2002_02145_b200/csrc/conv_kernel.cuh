@@ -1,0 +1,352 @@
+// Blocked direct-convolution forward on sm_100a tensor cores.
+//
+// The reference nest (ConvPreset::build, include/nestrank/presets.hpp:60-127;
+// paper Fig. 5) is
+//   for img, ofm_tile, ifm_tile, oj, kj, ki:            <- outer (driver) loops
+//     gemm_microkernel(&out[img][ofm_tile][oj][0][0],   <- band (oi, ofm, ifm)
+//                      &flt[ofm_tile][ifm_tile][kj][ki][0][0],
+//                      &in[img][ifm_tile][oj*sh+kj][ki][0])
+// Here the same contraction is one implicit GEMM per launch:
+//   M = pixels (img, oj, oi)   -> 128-row tiles = TMA box [16c][Qb][Pb][1][Nb]
+//   N = output channels        -> BN = 16 * (ofm_tile block count)
+//   K = (ifm_tile, kj, ki, ifm)-> one k-step = one (ifm_tile,kj,ki) triple =
+//                                 16 channels = two tcgen05 K=8 tf32 MMAs
+// i.e. each k-step is exactly the reference microkernel call batch-reduced
+// over 128 output pixels and BN output channels.
+//
+// Warp roles (persistent CTA, one per SM):
+//   warp 0      TMA producer: A box (NCHW16c, padding = TMA OOB zero fill,
+//               stride = TMA element strides) + B block (filter prepacked
+//               K-major as [C*R*S/16][K][16c], see conv_fwd.cu)
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer
+//   warps 2-5   epilogue: tcgen05.ld -> registers -> st.global.v4 (NKPQ16k)
+//   warps 6-9   (3xTF32 only) splitter: A -> lo = A - tf32(A) in shared memory
+//
+// Numerics (measured on B200, tools/probe2.cu): kind::tf32 reads fp32 operands
+// by truncating the 13 low mantissa bits, so A_hi is the raw fp32 tile and only
+// A_lo = x - trunc(x) is materialised. The tensor-core accumulation into TMEM
+// loses ~2^-25 of the running sum per MMA (error grows linearly with the MMA
+// chain), so in 3xTF32 mode the reduction is split into chunks of
+// `chunk_ksteps` k-steps: each chunk restarts its TMEM accumulator and the
+// epilogue adds the chunks in fp32 (round-to-nearest) into a TMEM running sum.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "sm100_ptx.cuh"
+
+namespace psconv {
+
+struct ConvParams {
+  int img_count, Cb, H, W, Kb, P, Q, R, S, sh, sw, ph, pw;
+  int Qb, Pb, Nb;                 // M-tile box in output pixels (Qb*Pb*Nb <= 128)
+  int tiles_q, tiles_p, tiles_n;  // M-tile grid
+  int tiles_k;                    // N tiles (K / BN)
+  int num_tiles, ksteps;          // ksteps = Cb*R*S
+  int chunk_ksteps;               // k-steps per TMEM accumulation chunk
+  int raster[3];                  // tile order outer->inner over {0 img, 1 ofm_tile, 2 oj}
+  int kord[3];                    // k-step order outer->inner over {0 ifm_tile, 1 kj, 2 ki}
+  int accumulate;                 // out += conv
+  float* out;                     // output at image img_begin
+  long long out_img_stride;       // Kb*P*Q*16 floats
+};
+
+template <int BN, bool SPLIT3>
+struct KernelCfg {
+  static constexpr int kABytes = 128 * 64;  // 128 pixels x 16 fp32 channels
+  static constexpr int kBBytes = BN * 64;   // BN output channels x 16 input channels (K-major)
+  // stage: [A | A_lo (3x) | B_hi | B_lo (3x)]
+  static constexpr int kStageBytes = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);
+  static constexpr int kBudget = 200 * 1024;
+  static constexpr int kStagesRaw = kBudget / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  // TMEM: kAccBufs chunk accumulators (+ one running-sum region in 3x mode)
+  static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
+  static constexpr int kSumCol = kAccBufs * BN;
+  static constexpr int kColsNeeded = kAccBufs * BN + (SPLIT3 ? BN : 0);
+  static constexpr int kTmemCols = kColsNeeded <= 32    ? 32
+                                   : kColsNeeded <= 64  ? 64
+                                   : kColsNeeded <= 128 ? 128
+                                   : kColsNeeded <= 256 ? 256
+                                                        : 512;
+  static constexpr int kThreads = SPLIT3 ? 320 : 192;
+  static constexpr int kBarBytes = 1024;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // +align slack
+  static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
+  static_assert(kStages >= 2, "stages");
+  static_assert(kColsNeeded <= 512, "TMEM");
+};
+
+struct TileCoord {
+  int tn, tp, tq, tk;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
+  TileCoord c;
+  c.tq = t % p.tiles_q;
+  int rem = t / p.tiles_q;
+  const int e2 = p.raster[2] == 0 ? p.tiles_n : (p.raster[2] == 1 ? p.tiles_k : p.tiles_p);
+  const int e1 = p.raster[1] == 0 ? p.tiles_n : (p.raster[1] == 1 ? p.tiles_k : p.tiles_p);
+  const int v2 = rem % e2;
+  rem /= e2;
+  const int v1 = rem % e1;
+  const int v0 = rem / e1;
+  c.tn = p.raster[0] == 0 ? v0 : (p.raster[1] == 0 ? v1 : v2);
+  c.tk = p.raster[0] == 1 ? v0 : (p.raster[1] == 1 ? v1 : v2);
+  c.tp = p.raster[0] == 2 ? v0 : (p.raster[1] == 2 ? v1 : v2);
+  return c;
+}
+
+__device__ __forceinline__ void decode_kstep(const ConvParams& p, int ks, int& cb, int& r, int& s) {
+  const int d2 = p.kord[2], d1 = p.kord[1], d0 = p.kord[0];
+  const int e2 = d2 == 0 ? p.Cb : (d2 == 1 ? p.R : p.S);
+  const int e1 = d1 == 0 ? p.Cb : (d1 == 1 ? p.R : p.S);
+  const int v2 = ks % e2;
+  ks /= e2;
+  const int v1 = ks % e1;
+  const int v0 = ks / e1;
+  cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
+  r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
+  s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
+}
+
+template <int BN, bool SPLIT3>
+__global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
+    conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
+                   const __grid_constant__ CUtensorMap tmap_flt,
+                   const __grid_constant__ CUtensorMap tmap_flt_lo) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using Cfg = KernelCfg<BN, SPLIT3>;
+  constexpr int kStages = Cfg::kStages;
+  constexpr int kAccBufs = Cfg::kAccBufs;
+  constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN>();
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B).
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  auto a_buf = [&](int s) { return smem + s * Cfg::kStageBytes; };
+  auto alo_buf = [&](int s) { return smem + s * Cfg::kStageBytes + Cfg::kABytes; };
+  auto b_buf = [&](int s) {
+    return smem + s * Cfg::kStageBytes + Cfg::kABytes * (SPLIT3 ? 2 : 1);
+  };
+  auto blo_buf = [&](int s) { return b_buf(s) + Cfg::kBBytes; };
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* full = bars;                     // TMA landed           (count 1 + tx)
+  uint64_t* split_full = bars + kStages;     // splitter done        (count 128)
+  uint64_t* empty = bars + 2 * kStages;      // MMA consumed stage   (tcgen05.commit)
+  uint64_t* acc_full = bars + 3 * kStages;   // chunk accumulator ready   [kAccBufs]
+  uint64_t* acc_empty = acc_full + 2;        // chunk accumulator drained [kAccBufs] (count 128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nchunks = (p.ksteps + p.chunk_ksteps - 1) / p.chunk_ksteps;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&split_full[s], 128);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < kAccBufs; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tmap_in);
+      ptx::prefetch_tmap(&tmap_flt);
+      if (SPLIT3) ptx::prefetch_tmap(&tmap_flt_lo);
+      const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
+      const uint32_t tx = (a_bytes + Cfg::kBBytes * (SPLIT3 ? 2 : 1));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const TileCoord tc = decode_tile(p, t);
+        const int wq = tc.tq * p.Qb * p.sw - p.pw;
+        const int hp = tc.tp * p.Pb * p.sh - p.ph;
+        const int n0 = tc.tn * p.Nb;
+        const int k0 = tc.tk * BN;
+        for (int ks = 0; ks < p.ksteps; ++ks) {
+          int cb, r, s;
+          decode_kstep(p, ks, cb, r, s);
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full[stage], tx);
+          ptx::tma_load_5d(a_buf(stage), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
+          const int crs = (cb * p.R + r) * p.S + s;
+          ptx::tma_load_3d(b_buf(stage), &tmap_flt, &full[stage], 0, k0, crs);
+          if (SPLIT3) ptx::tma_load_3d(blo_buf(stage), &tmap_flt_lo, &full[stage], 0, k0, crs);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int c = 0; c < nchunks; ++c, ++cit) {
+          const int buf = kAccBufs == 1 ? 0 : (cit & 1);
+          const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
+          ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+          const int ks0 = c * p.chunk_ksteps;
+          const int ks_end = min(p.ksteps, ks0 + p.chunk_ksteps);
+          for (int ks = ks0; ks < ks_end; ++ks) {
+            ptx::mbar_wait(&full[stage], phase);
+            if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t a_hi = ptx::smem_u32(a_buf(stage));
+            const uint32_t a_lo = ptx::smem_u32(alo_buf(stage));
+            const uint32_t b_hi = ptx::smem_u32(b_buf(stage));
+            const uint32_t b_lo = ptx::smem_u32(blo_buf(stage));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              // A and B: K-major SW64 (64-B rows, 8-row groups 512 B apart);
+              // K half h (channels 8h..8h+7) starts 32 B into the row.
+              const uint64_t da_hi = ptx::smem_desc_sw64(a_hi + h * 32, 16, 512);
+              const uint64_t db_hi = ptx::smem_desc_sw64(b_hi + h * 32, 16, 512);
+              const uint32_t acc_in = (ks == ks0 && h == 0) ? 0u : 1u;
+              if (SPLIT3) {
+                const uint64_t da_lo = ptx::smem_desc_sw64(a_lo + h * 32, 16, 512);
+                const uint64_t db_lo = ptx::smem_desc_sw64(b_lo + h * 32, 16, 512);
+                ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small terms first
+                ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
+                ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
+              } else {
+                ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
+              }
+            }
+            ptx::mma_commit(&empty[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          ptx::mma_commit(&acc_full[buf]);
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    const int PQ16 = p.P * p.Q * 16;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    int cit = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const TileCoord tc = decode_tile(p, t);
+      const int rq = row % p.Qb;
+      const int rp = (row / p.Qb) % p.Pb;
+      const int rn = row / (p.Qb * p.Pb);
+      const int q = tc.tq * p.Qb + rq;
+      const int pp = tc.tp * p.Pb + rp;
+      const int n = tc.tn * p.Nb + rn;
+      const bool valid = (rn < p.Nb) && (q < p.Q) && (pp < p.P) && (n < p.img_count);
+      float* orow = p.out + static_cast<long long>(n) * p.out_img_stride +
+                    (static_cast<long long>(tc.tk * (BN / 16)) * p.P + pp) * (p.Q * 16) + q * 16;
+      for (int c = 0; c < nchunks; ++c, ++cit) {
+        const int buf = kAccBufs == 1 ? 0 : (cit & 1);
+        const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
+        const bool last = c == nchunks - 1;
+        ptx::mbar_wait(&acc_full[buf], acc_phase);
+        ptx::tc_fence_after();
+        const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
+        const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
+#pragma unroll 1
+        for (int j = 0; j < BN / 16; ++j) {
+          uint32_t v[16];
+          ptx::tmem_ld16(tacc + j * 16, v);
+          if (SPLIT3 && c > 0) {
+            uint32_t sacc[16];
+            ptx::tmem_ld16(tsum + j * 16, sacc);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              v[i] = __float_as_uint(__uint_as_float(sacc[i]) + __uint_as_float(v[i]));
+          } else {
+            ptx::tmem_wait_ld();
+          }
+          if (!last) {
+            ptx::tmem_st16(tsum + j * 16, v);
+          } else if (valid) {
+            float4* dst = reinterpret_cast<float4*>(orow + static_cast<long long>(j) * PQ16);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              float4 o = make_float4(__uint_as_float(v[4 * c4 + 0]), __uint_as_float(v[4 * c4 + 1]),
+                                     __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
+              if (p.accumulate) {
+                const float4 prev = dst[c4];
+                o.x += prev.x;
+                o.y += prev.y;
+                o.z += prev.z;
+                o.w += prev.w;
+              }
+              dst[c4] = o;
+            }
+          }
+        }
+        if (!last) ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&acc_empty[buf]);
+      }
+    }
+  } else if (SPLIT3) {
+    // ------------------------------------------------------------ splitter
+    // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
+    const int tid = threadIdx.x - 192;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int ks = 0; ks < p.ksteps; ++ks) {
+        ptx::mbar_wait(&full[stage], phase);
+        const float4* a = reinterpret_cast<const float4*>(a_buf(stage));
+        float4* alo = reinterpret_cast<float4*>(alo_buf(stage));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = tid + i * 128;
+          const float4 x = a[idx];
+          float4 lo;
+          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          alo[idx] = lo;
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&split_full[stage]);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+#endif
+}
+
+}  // namespace psconv

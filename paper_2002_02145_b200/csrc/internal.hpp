@@ -1,0 +1,89 @@
+// Internal host-side declarations shared by the C-ABI translation units.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "psconv.h"
+
+namespace psconv {
+
+// Error classes mirror the reference hierarchy (include/nestrank/common.hpp:10-36):
+// ConfigError -> exit/status 2 (ConfigRejectedError, InvalidPermutationError,
+// TileSizeNonPositiveError, ParseError ...), RuntimeError -> status 1.
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+void clear_last_error();
+
+// Runs f, translating exceptions into status codes + conv_last_error().
+template <typename F>
+int guarded(F&& f) {
+  try {
+    clear_last_error();
+    f();
+    return PSCONV_OK;
+  } catch (const ConfigError& e) {
+    set_last_error(e.what());
+    return PSCONV_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PSCONV_ERR_RUNTIME;
+  }
+}
+
+void validate_desc(conv_desc& d);  // throws ConfigError; fills ifh/ifw
+
+// The reference loop names (presets.hpp:75-85) of the tunable outer loops.
+enum LoopId { L_IMG = 0, L_OFM_TILE, L_IFM_TILE, L_OJ, L_KJ, L_KI, L_COUNT };
+const char* loop_name(int id);
+int loop_id(const std::string& name);  // -1 if unknown
+
+// Reference recipe (variants.hpp:16-65) + the GPU clause.
+struct Recipe {
+  std::vector<std::string> perm;                              // listed loops, new order
+  std::vector<std::pair<std::string, int64_t>> tiles;         // loop -> tile size
+  int bn = 0;                                                 // 0 = selector decides
+  int box_q = 0, box_p = 0, box_n = 0;                        // 0 = selector decides
+  int stages = 0;                                             // informational
+  int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
+  bool has_gpu = false;
+  static Recipe parse(const std::string& text);  // throws ConfigError
+  std::string id() const;                        // reference grammar + ";gpu=..."
+};
+
+// A fully resolved GPU schedule.
+struct Schedule {
+  int order[L_COUNT];  // loop ids in execution order (outer -> inner), band excluded
+  int bn;              // output channels per tile (64/128/256)
+  int qb, pb, nb;      // pixel box (ofw x ofh x img) of one 128-row M tile
+  int oj_tile;         // reference tile=oj:T (0 = untiled)
+  int chunk;           // k-steps per TMEM accumulation chunk (0 = whole reduction)
+  int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
+  int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
+  std::string recipe_id;
+};
+
+// Resolves a recipe (possibly partial) against a descriptor; throws ConfigError
+// for illegal recipes (same checks as variants.hpp:186-228 plan_recipe).
+Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gpu = true);
+
+// Closed-form model (select.cpp).
+struct ModelBreakdown {
+  double us_total, us_tensor, us_hbm, us_l2, us_smem, us_epi;
+  double hbm_bytes, l2_bytes, flops_issued;
+  int64_t m_tiles, tiles;
+};
+ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode);
+std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode);
+
+// emit.cpp
+std::string emit_driver(const conv_desc& d, const Schedule& s);
+
+}  // namespace psconv

@@ -1,0 +1,275 @@
+// Recipe grammar and recipe -> GPU schedule resolution.
+//
+// The recipe grammar is the reference's (include/nestrank/variants.hpp:16-65):
+//   perm=ofm_tile,oj,ifm_tile,kj,ki;tile=oj:2
+// extended with one optional clause for the GPU tile axes:
+//   ;gpu=bn:128,box:8x8x2        (BN output channels; pixel box ofw x ofh x img)
+// Validation follows plan_recipe (variants.hpp:186-228) with the same error
+// classes; the conv nest has no order-constraining dependences (all 120
+// orders of the five movable loops are legal), so the
+// legality check reduces to the structural ones.
+//
+// GPU meaning of a recipe:
+//   * relative order of the parallel loops {img, ofm_tile, oj} = tile
+//     rasterisation order of the persistent scheduler (oi innermost);
+//   * relative order of the reduction loops {ifm_tile, kj, ki} = k-step order;
+//   * tile=oj:T  -> T output rows per 128-pixel tile (box P extent);
+//     tile=img:T -> T images per tile; tile=ofm_tile:T -> BN = 16*T channels.
+#include <algorithm>
+#include <cctype>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "internal.hpp"
+
+namespace psconv {
+
+namespace {
+
+std::vector<std::string> split_names(const std::string& s) {  // loopnest.hpp:317-329
+  std::vector<std::string> out;
+  std::string cur;
+  for (char c : s) {
+    if (c == ',' || std::isspace(static_cast<unsigned char>(c))) {
+      if (!cur.empty()) {
+        out.push_back(cur);
+        cur.clear();
+      }
+    } else {
+      cur += c;
+    }
+  }
+  if (!cur.empty()) out.push_back(cur);
+  return out;
+}
+
+int64_t parse_int(const std::string& s, const std::string& what) {
+  try {
+    size_t pos = 0;
+    const long long v = std::stoll(s, &pos);
+    (void)pos;
+    return v;
+  } catch (const std::logic_error&) {
+    throw ConfigError("bad " + what + " '" + s + "'");
+  }
+}
+
+bool is_band(const std::string& v) { return v == "oi" || v == "ofm" || v == "ifm"; }
+
+}  // namespace
+
+Recipe Recipe::parse(const std::string& text) {
+  Recipe r;
+  size_t pos = 0;
+  while (pos < text.size()) {
+    size_t end = text.find(';', pos);
+    if (end == std::string::npos) end = text.size();
+    const std::string part = text.substr(pos, end - pos);
+    if (part.rfind("perm=", 0) == 0) {
+      r.perm = split_names(part.substr(5));
+    } else if (part.rfind("tile=", 0) == 0) {
+      for (const std::string& item : split_names(part.substr(5))) {
+        const size_t colon = item.find(':');
+        if (colon == std::string::npos)
+          throw ConfigError("bad tile entry '" + item + "' in recipe");
+        const int64_t size = parse_int(item.substr(colon + 1), "tile size in recipe entry");
+        r.tiles.emplace_back(item.substr(0, colon), size);
+      }
+    } else if (part.rfind("gpu=", 0) == 0) {
+      r.has_gpu = true;
+      for (const std::string& item : split_names(part.substr(4))) {
+        const size_t colon = item.find(':');
+        if (colon == std::string::npos) throw ConfigError("bad gpu entry '" + item + "' in recipe");
+        const std::string key = item.substr(0, colon), val = item.substr(colon + 1);
+        if (key == "bn") {
+          r.bn = static_cast<int>(parse_int(val, "gpu bn"));
+        } else if (key == "box") {
+          int q = 0, p = 0, n = 0;
+          if (std::sscanf(val.c_str(), "%dx%dx%d", &q, &p, &n) != 3)
+            throw ConfigError("bad gpu box '" + val + "' (expected QxPxN)");
+          r.box_q = q;
+          r.box_p = p;
+          r.box_n = n;
+        } else if (key == "st") {
+          r.stages = static_cast<int>(parse_int(val, "gpu stages"));
+        } else if (key == "ch") {
+          r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
+          if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
+        } else {
+          throw ConfigError("unknown gpu recipe key '" + key + "'");
+        }
+      }
+    } else if (!part.empty()) {
+      throw ConfigError("unknown recipe clause '" + part + "'");
+    }
+    pos = end + 1;
+  }
+  return r;
+}
+
+std::string Recipe::id() const {
+  std::string s = "perm=";
+  for (size_t i = 0; i < perm.size(); ++i) s += (i ? "," : "") + perm[i];
+  if (!tiles.empty()) {
+    s += ";tile=";
+    for (size_t i = 0; i < tiles.size(); ++i)
+      s += (i ? "," : "") + tiles[i].first + ":" + std::to_string(tiles[i].second);
+  }
+  if (has_gpu) {
+    s += ";gpu=bn:" + std::to_string(bn) + ",box:" + std::to_string(box_q) + "x" +
+         std::to_string(box_p) + "x" + std::to_string(box_n);
+    if (chunk) s += ",ch:" + std::to_string(chunk);
+  }
+  return s;
+}
+
+// Best 128-row pixel box for a (Q, P, N) output grid: maximal useful-row
+// fraction, then longest contiguous input run (qb), then taller boxes.
+static void choose_box(int64_t Q, int64_t P, int64_t N, int64_t sh, int64_t sw, int fix_p,
+                       int fix_n, int& qb, int& pb, int& nb) {
+  double best_eff = -1;
+  int bq = 1, bp = 1, bn = 1;
+  const int64_t useful = Q * P * N;
+  for (int p = 1; p <= 128 && p <= P; ++p) {
+    if (fix_p && p != fix_p) continue;
+    if (p * sh > 256) break;
+    for (int q = 1; q * p <= 128 && q <= Q; ++q) {
+      if (q * sw > 256) break;
+      const int nmax = static_cast<int>(std::min<int64_t>(N, 128 / (q * p)));
+      for (int n = nmax; n >= 1; --n) {
+        if (fix_n && n != fix_n) continue;
+        if (n > 256) continue;
+        const int64_t tiles = ((Q + q - 1) / q) * ((P + p - 1) / p) * ((N + n - 1) / n);
+        const double eff = double(useful) / double(tiles * 128);
+        const bool better = eff > best_eff + 1e-12 ||
+                            (eff > best_eff - 1e-12 && (q > bq || (q == bq && p > bp)));
+        if (better) {
+          best_eff = eff;
+          bq = q;
+          bp = p;
+          bn = n;
+        }
+        break;  // largest n for this (q,p) that fits is best for efficiency
+      }
+    }
+  }
+  if (best_eff < 0) {  // fixed p/n infeasible: fall back to unconstrained
+    if (fix_p || fix_n) return choose_box(Q, P, N, sh, sw, 0, 0, qb, pb, nb);
+  }
+  qb = bq;
+  pb = bp;
+  nb = bn;
+}
+
+Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gpu) {
+  (void)mode;
+  if (gpu && d.gemm_block != 16) throw ConfigError("GPU path requires gemm_block == 16 (NCHW16c layout)");
+  // --- plan_recipe (variants.hpp:186-228) structural checks
+  std::map<std::string, int> pos;
+  for (int i = 0; i < L_COUNT; ++i) pos[loop_name(i)] = i;
+  std::set<std::string> seen;
+  std::vector<int> listed;
+  for (const std::string& v : r.perm) {
+    auto it = pos.find(v);
+    if (it == pos.end()) {
+      if (is_band(v)) throw ConfigError("recipe permutes microkernel band loop '" + v + "'");
+      throw ConfigError("recipe names unknown loop '" + v + "'");
+    }
+    if (!seen.insert(v).second) throw ConfigError("recipe lists loop '" + v + "' twice");
+    listed.push_back(it->second);
+  }
+  std::vector<int> order(L_COUNT);
+  for (int i = 0; i < L_COUNT; ++i) order[i] = i;
+  std::vector<int> slots = listed;
+  std::sort(slots.begin(), slots.end());
+  for (size_t k = 0; k < slots.size(); ++k) order[slots[k]] = listed[k];
+
+  std::map<std::string, int64_t> tile_of;
+  for (const auto& [var, size] : r.tiles) {
+    if (size <= 0)
+      throw ConfigError("tile size for loop '" + var + "' must be positive");
+    auto it = pos.find(var);
+    if (it == pos.end()) {
+      if (is_band(var)) throw ConfigError("recipe tiles microkernel band loop '" + var + "'");
+      throw ConfigError("recipe tiles unknown loop '" + var + "'");
+    }
+    if (tile_of.count(var)) throw ConfigError("recipe tiles loop '" + var + "' twice");
+    tile_of[var] = size;
+  }
+
+  Schedule s{};
+  for (int i = 0; i < L_COUNT; ++i) s.order[i] = order[i];
+  // raster: relative order of {img, ofm_tile, oj}; kord: of {ifm_tile, kj, ki}
+  int nr = 0, nk = 0;
+  for (int i = 0; i < L_COUNT; ++i) {
+    const int l = order[i];
+    if (l == L_IMG) s.raster[nr++] = 0;
+    if (l == L_OFM_TILE) s.raster[nr++] = 1;
+    if (l == L_OJ) s.raster[nr++] = 2;
+    if (l == L_IFM_TILE) s.kord[nk++] = 0;
+    if (l == L_KJ) s.kord[nk++] = 1;
+    if (l == L_KI) s.kord[nk++] = 2;
+  }
+
+  s.oj_tile = tile_of.count("oj") ? static_cast<int>(tile_of["oj"]) : 0;
+  if (!gpu) {
+    Recipe canon;
+    for (int i = 0; i < L_COUNT; ++i)
+      if (order[i] != L_IMG || i != 0) canon.perm.push_back(loop_name(order[i]));
+    for (const auto& t : r.tiles) canon.tiles.push_back(t);
+    s.recipe_id = canon.id();
+    return s;
+  }
+  // --- tile axes
+  const int64_t K = d.nOfm;
+  int bn = r.bn;
+  if (tile_of.count("ofm_tile") && !bn) bn = static_cast<int>(16 * tile_of["ofm_tile"]);
+  if (!bn) {
+    for (int c : {256, 128, 64, 32, 16})
+      if (K % c == 0) {
+        bn = c;
+        break;
+      }
+  }
+  if (bn != 16 && bn != 32 && bn != 64 && bn != 128 && bn != 256)
+    throw ConfigError("GPU tile: bn must be 16, 32, 64, 128 or 256 (got " + std::to_string(bn) + ")");
+  if (K % bn != 0)
+    throw ConfigError("GPU tile: nOfm=" + std::to_string(K) + " is not a multiple of bn=" +
+                      std::to_string(bn));
+  s.bn = bn;
+
+  int fix_p = tile_of.count("oj") ? static_cast<int>(std::min<int64_t>(tile_of["oj"], d.ofh)) : 0;
+  int fix_n = tile_of.count("img") ? static_cast<int>(std::min<int64_t>(tile_of["img"], d.nImg)) : 0;
+  if (r.box_q || r.box_p || r.box_n) {
+    s.qb = r.box_q;
+    s.pb = r.box_p;
+    s.nb = r.box_n;
+    if (s.qb < 1 || s.pb < 1 || s.nb < 1 || s.qb * s.pb * s.nb > 128)
+      throw ConfigError("GPU tile: box QxPxN must be positive with Q*P*N <= 128");
+    if (s.qb * d.stride_w > 256 || s.pb * d.stride_h > 256 || s.nb > 256)
+      throw ConfigError("GPU tile: box exceeds the TMA box limit (256 per dimension)");
+  } else {
+    if (fix_p > 128) fix_p = 128;
+    choose_box(d.ofw, d.ofh, d.nImg, d.stride_h, d.stride_w, fix_p, fix_n, s.qb, s.pb, s.nb);
+  }
+
+  Recipe canon;
+  for (int i = 0; i < L_COUNT; ++i)
+    if (order[i] != L_IMG || i != 0) canon.perm.push_back(loop_name(order[i]));
+  for (const auto& t : r.tiles) canon.tiles.push_back(t);
+  canon.has_gpu = true;
+  canon.bn = s.bn;
+  canon.box_q = s.qb;
+  canon.box_p = s.pb;
+  canon.box_n = s.nb;
+  // TMEM accumulation chunk (3xTF32 numerics, see conv_kernel.cuh); tf32: whole reduction
+  const int ksteps = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
+  s.chunk = r.chunk ? r.chunk : (mode == PSCONV_MODE_3XTF32 ? 16 : ksteps);
+  if (s.chunk > ksteps) s.chunk = ksteps;
+  canon.chunk = (mode == PSCONV_MODE_3XTF32 || r.chunk) ? s.chunk : 0;
+  s.recipe_id = canon.id();
+  return s;
+}
+
+}  // namespace psconv

@@ -1,0 +1,188 @@
+// Schedule selector: the PolyScientist ranking step (paper §4, reference
+// pipeline.hpp:61-92 rank_variants -> costrank.hpp:19-40 cost/rank_by_cost)
+// re-expressed for B200.
+//
+// The reference costs a variant by exact per-dependence working sets placed
+// greedily in a cache hierarchy (reuse.hpp:29-82, cachefit.hpp:157-183). That
+// engine materialises every iteration point (intset.hpp:295-307) and cannot
+// run at BASELINE sizes (~2,000 s / ~700 GB per variant for
+// cfg1), so here each candidate is costed in closed form:
+//   t = max(tensor-pipe time, L2->SMEM operand time, HBM time) + fixed costs
+// where the working set that decides HBM re-reads is the L2 footprint of the
+// tiles co-resident on the 148 SMs (the GPU analogue of Alg. 1's WS at the
+// level the persistent scheduler's rasterisation order controls).
+// Candidates are the reference's recipe space (the four loop orders of
+// samples/variants/conv_orders.cfg, the oj row tile) crossed with the GPU tile
+// axes (BN, pixel box); ranking is ascending cost with ties broken by id, as
+// in rank_by_cost (costrank.hpp:31-40).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+#include <tuple>
+
+#include "internal.hpp"
+
+namespace psconv {
+
+namespace {
+
+// B200 machine model. Peaks: MEASURED_PEAKS.json (HBM copy 6538.9 GB/s,
+// bf16 1622.7 TFLOP/s -> tf32 811.4 derived); the rest are modelling
+// constants to be refined from measurements.
+struct Machine {
+  double sms = 148;
+  double hbm_gbs = 6538.9;
+  double l2_gbs = 9000.0;        // aggregate L2 -> SMEM operand bandwidth (TMA)
+  double tf32_tflops = 811.4;    // dense tf32 tensor peak (derived)
+  double l2_bytes = 100e6;       // usable share of the 126 MB L2
+  double launch_us = 4.0;        // launch + prologue (TMEM alloc, barrier init)
+  double tile_fill_us = 0.6;     // pipeline fill of the first k-steps of a tile
+};
+const Machine kB200{};
+
+struct Geo {
+  int64_t N, C, K, H, W, P, Q, R, S, Cb, Kb;
+};
+Geo geo(const conv_desc& d) {
+  return Geo{d.nImg, d.nIfm, d.nOfm, d.ifh, d.ifw, d.ofh, d.ofw, d.kh, d.kw, d.nIfm / 16, d.nOfm / 16};
+}
+
+// Paper's four §2 orders (reference samples/variants/conv_orders.cfg:3-6).
+const char* kPerms[] = {"ofm_tile,ifm_tile,oj,kj,ki", "ifm_tile,ofm_tile,oj,kj,ki",
+                        "oj,ofm_tile,ifm_tile,kj,ki", "kj,ki,oj,ofm_tile,ifm_tile"};
+
+std::vector<std::tuple<int, int, int>> box_candidates(const conv_desc& d) {
+  // enumerate boxes, keep the best few by useful-row fraction
+  struct B {
+    double eff;
+    int q, p, n;
+  };
+  std::vector<B> all;
+  const int64_t Q = d.ofw, P = d.ofh, N = d.nImg;
+  for (int p = 1; p <= 128 && p <= P && p * d.stride_h <= 256; ++p)
+    for (int q = 1; q * p <= 128 && q <= Q && q * d.stride_w <= 256; ++q) {
+      const int n = static_cast<int>(std::min<int64_t>({N, 128 / (q * p), 256}));
+      const int64_t tiles = ((Q + q - 1) / q) * ((P + p - 1) / p) * ((N + n - 1) / n);
+      all.push_back({double(Q * P * N) / double(tiles * 128), q, p, n});
+    }
+  std::sort(all.begin(), all.end(), [](const B& a, const B& b) {
+    if (std::fabs(a.eff - b.eff) > 1e-12) return a.eff > b.eff;
+    if (a.q != b.q) return a.q > b.q;
+    return a.p > b.p;
+  });
+  std::vector<std::tuple<int, int, int>> out;
+  for (const B& b : all) {
+    if (out.size() >= 4 || b.eff < all.front().eff - 0.15) break;
+    out.emplace_back(b.q, b.p, b.n);
+  }
+  return out;
+}
+
+}  // namespace
+
+ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
+  const Machine& m = kB200;
+  const Geo g = geo(d);
+  const double mult = mode == PSCONV_MODE_3XTF32 ? 3.0 : 1.0;
+  const int64_t tq = (g.Q + s.qb - 1) / s.qb, tp = (g.P + s.pb - 1) / s.pb,
+                tn = (g.N + s.nb - 1) / s.nb, tk = g.K / s.bn;
+  const int64_t mt = tq * tp * tn, tiles = mt * tk;
+  const int64_t ksteps = g.Cb * g.R * g.S;
+  const double per_sm = std::ceil(double(tiles) / m.sms);  // static round-robin waves
+
+  ModelBreakdown b{};
+  b.m_tiles = mt;
+  b.tiles = tiles;
+  const double tile_flops = 2.0 * 128 * s.bn * 16.0 * ksteps * mult;
+  b.flops_issued = tile_flops * tiles;
+  b.us_tensor = per_sm * tile_flops / (m.tf32_tflops * 1e12 / m.sms) * 1e6;
+
+  const double a_box = double(s.qb) * s.pb * s.nb * 64.0;
+  const double tile_l2 = ksteps * (a_box + s.bn * 64.0 * (mult > 1 ? 2 : 1));
+  b.l2_bytes = tile_l2 * tiles;
+  b.us_l2 = per_sm * m.sms * tile_l2 / (m.l2_gbs * 1e9) * 1e6;
+
+  // HBM: compulsory bytes + input re-reads when the rasterisation sweeps all
+  // pixels once per output-channel tile and the input does not stay in L2.
+  const double in_b = 4.0 * g.N * g.C * g.H * g.W;
+  const double flt_b = 4.0 * g.K * g.C * g.R * g.S * (mult > 1 ? 3 : 1);  // + hi/lo copies
+  const double out_b = 4.0 * g.N * g.K * g.P * g.Q;
+  const bool ofm_outer = s.raster[0] == 1 || (s.raster[1] == 1 && s.raster[2] != 1 && s.raster[0] == 0 &&
+                                              tn == 1);
+  double in_reads = 1.0;
+  if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
+  b.hbm_bytes = in_b * in_reads + flt_b + out_b;
+  b.us_hbm = b.hbm_bytes / (m.hbm_gbs * 1e9) * 1e6;
+  b.us_smem = 0;
+  b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain
+  b.us_total = std::max({b.us_tensor, b.us_l2, b.us_hbm}) + m.launch_us + m.tile_fill_us + b.us_epi +
+               (mult > 1 ? 2.0 + 3.0 * flt_b / 3 / (m.hbm_gbs * 1e9) * 1e6 : 0.0);
+  return b;
+}
+
+std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
+  std::vector<Schedule> out;
+  std::set<std::string> seen;
+  std::vector<int> bns;
+  for (int c : {256, 128, 64, 32, 16})
+    if (d.nOfm % c == 0) bns.push_back(c);
+  const auto boxes = box_candidates(d);
+  for (const char* perm : kPerms)
+    for (int bn : bns)
+      for (const auto& [q, p, n] : boxes) {
+        Recipe r = Recipe::parse(std::string("perm=") + perm);
+        r.has_gpu = true;
+        r.bn = bn;
+        r.box_q = q;
+        r.box_p = p;
+        r.box_n = n;
+        Schedule s = resolve_schedule(d, r, mode);
+        if (seen.insert(s.recipe_id).second) out.push_back(s);
+      }
+  return out;
+}
+
+}  // namespace psconv
+
+using namespace psconv;
+
+extern "C" {
+
+int conv_select_topk(const conv_desc* d_in, int mode, int k, char* buf, size_t len, double* us) {
+  int written = 0;
+  const int rc = guarded([&] {
+    if (!d_in || !buf || k < 1) throw ConfigError("bad argument");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    auto cands = candidate_schedules(d, mode);
+    if (cands.empty()) throw ConfigError("no GPU schedule for this descriptor");
+    std::vector<std::pair<double, std::string>> scored;
+    for (const auto& s : cands) scored.emplace_back(model_schedule(d, s, mode).us_total, s.recipe_id);
+    std::sort(scored.begin(), scored.end());
+    std::string txt;
+    for (int i = 0; i < k && i < static_cast<int>(scored.size()); ++i) {
+      txt += (i ? "\n" : "") + scored[i].second;
+      if (us) us[i] = scored[i].first;
+      ++written;
+    }
+    if (txt.size() + 1 > len) throw ConfigError("buffer too small");
+    std::memcpy(buf, txt.c_str(), txt.size() + 1);
+  });
+  return rc == PSCONV_OK ? written : -rc;
+}
+
+double conv_model_us(const conv_desc* d_in, int mode, const char* recipe) {
+  double us = -1;
+  guarded([&] {
+    if (!d_in) throw ConfigError("null descriptor");
+    conv_desc d = *d_in;
+    validate_desc(d);
+    const Schedule s = resolve_schedule(d, Recipe::parse(recipe ? recipe : ""), mode);
+    us = model_schedule(d, s, mode).us_total;
+  });
+  return us;
+}
+
+}  // extern "C"

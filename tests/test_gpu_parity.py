@@ -1,0 +1,106 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+Tolerances are BASELINE.json north_star's: relative L2 <= 1e-5 (3xTF32), <= 5e-3 (TF32);
+max-abs is reported. Full-size BASELINE shapes are checked on image subsets (every image
+is an independent unit: SURVEY.md §8e), with seeds keyed by global image index.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.cases import ALL, BASELINE, R50, seeds, with_images
+
+torch = pytest.importorskip("torch")
+ps = pytest.importorskip("paper_2002_02145_b200")
+
+TOL = {"3xtf32": 1e-5, "tf32": 5e-3}
+
+
+def _run_gpu(p, c_logical, sx, sw, mode, recipe=None, img_begin=0, img_count=None,
+             accumulate=False, out_init=None):
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), dtype=torch.float32, device=dev)
+    w = torch.empty(p.filter_elems(), dtype=torch.float32, device=dev)
+    y = torch.full((p.output_elems(),), float("nan"), dtype=torch.float32, device=dev)
+    if out_init is not None:
+        y.copy_(torch.from_numpy(out_init.ravel()).to(dev))
+    ps.fill_input(p, sx, x, c_logical=c_logical)
+    ps.fill_filter(p, sw, w, c_logical=c_logical)
+    plan = ps.ConvPlan(p, mode=mode, device=0, recipe=recipe)
+    plan.forward(x, w, y, img_begin=img_begin, img_count=img_count, accumulate=accumulate)
+    torch.cuda.synchronize()
+    return x.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), plan.recipe
+
+
+def _check(name, conv, c_logical, cfg_id, mode, n_img, recipe=None):
+    p = ps.ConvPreset.parse(with_images(conv, n_img))
+    sx, sw = seeds(cfg_id)
+    xg, wg, yg, rec = _run_gpu(p, c_logical, sx, sw, mode, recipe)
+    x = oracle.fill_input(p, sx, c_logical)
+    w = oracle.fill_filter(p, sw, c_logical)
+    assert np.array_equal(xg, x.ravel()), "device generator != host generator (input)"
+    assert np.array_equal(wg, w.ravel()), "device generator != host generator (filter)"
+    ref = oracle.conv(p, x, w).ravel()
+    assert np.isfinite(yg).all(), f"{name}: non-finite / unwritten outputs ({rec})"
+    err = oracle.rel_l2(yg, ref)
+    mx = oracle.max_abs(yg, ref)
+    print(f"{name} {mode} N={n_img} recipe={rec} relL2={err:.3e} maxabs={mx:.3e}")
+    assert err <= TOL[mode], f"{name} {mode}: relL2 {err:.3e} > {TOL[mode]} (maxabs {mx:.3e}, {rec})"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_default_preset(mode):
+    # the reference's default preset conv:2,32,32,4,4,3,3,1,1,16 (presets.hpp:14-23)
+    _check("default", "conv:2,32,32,4,4,3,3,1,1,16", 32, 0, mode, 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("name", list(BASELINE))
+def test_baseline_shapes(name, mode):
+    conv, c_log, cid = BASELINE[name]
+    n = {"cfg1": 4, "cfg2": 4, "cfg3": 4, "cfg5": 40}[name]
+    _check(name, conv, c_log, cid, mode, n)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(R50))
+def test_resnet50_layers(name):
+    conv, c_log, cid = R50[name]
+    p = ps.ConvPreset.parse(conv)
+    n = max(1, min(16, 200000 // (p.ofh * p.ofw)))
+    _check(name, conv, c_log, cid, "3xtf32", n)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("recipe", [
+    "perm=ofm_tile,ifm_tile,oj,kj,ki",
+    "perm=oj,ofm_tile,ifm_tile,kj,ki",
+    "perm=kj,ki,oj,ofm_tile,ifm_tile",
+    "perm=ifm_tile,ofm_tile,oj,kj,ki;tile=oj:2",
+    "perm=oj,ofm_tile,ifm_tile,kj,ki;gpu=bn:32,box:56x2x1",
+    "perm=ofm_tile,ifm_tile,oj,kj,ki;gpu=bn:64,box:8x8x2",
+    "perm=ofm_tile,ifm_tile,oj,kj,ki;gpu=bn:16,box:7x3x5",
+])
+def test_recipes(recipe):
+    _check("cfg1-recipe", BASELINE["cfg1"][0], 64, 1, "3xtf32", 3, recipe)
+
+
+@pytest.mark.gpu
+def test_image_range_and_accumulate():
+    """conv_fwd on [img_begin, img_begin+count) touches only those images; FLAG_ACCUMULATE
+    reproduces the reference body's `+=` (presets.hpp:112)."""
+    p = ps.ConvPreset.parse(with_images(BASELINE["cfg3"][0], 6))
+    sx, sw = seeds(3)
+    base = np.random.default_rng(0).standard_normal(p.output_elems()).astype(np.float32)
+    xg, wg, yg, _ = _run_gpu(p, 128, sx, sw, "3xtf32", img_begin=2, img_count=3,
+                             accumulate=True, out_init=base)
+    x = oracle.fill_input(p, sx, 128)
+    w = oracle.fill_filter(p, sw, 128)
+    ref = base.reshape(6, -1).copy()
+    conv = oracle.conv(p, x, w).reshape(6, -1)
+    ref[2:5] += conv[2:5]
+    yg = yg.reshape(6, -1)
+    assert np.array_equal(yg[:2], ref[:2]) and np.array_equal(yg[5:], ref[5:])
+    assert oracle.rel_l2(yg[2:5], ref[2:5]) <= 1e-5
