@@ -1,0 +1,467 @@
+#!/usr/bin/env python3
+"""Bench: blocked fp32 direct-conv forward (the PolyScientist hot path) on B200.
+
+Metric (BASELINE.json): "conv fwd GFLOP/s per layer & fraction of roofline at 1/2/4/8 B200
+vs host-CPU ref". Default workload = BASELINE configs[4] ("cfg5", N=2048 3x3 256->256 14x14,
+the config the metric is quoted on at 1/2/4/8 GPUs), fp32-faithful 3xTF32 mode; the TF32 fast
+mode is reported beside it. One step = one conv_fwd pass (filter repack + conv kernel) over
+this rank's images [rank*N/W, (rank+1)*N/W) — strong scaling, no collective on the hot path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5] [--mode 3xtf32]
+  python bench.py --impl reference ...   # the reference's own emitted CPU driver (oracle/_ref)
+
+Prints ONE JSON line on rank 0. Timing: CUDA events on the launching stream, L2 flushed
+(256 MiB write) before every timed step, barrier + synchronize around the timed loop, max
+over ranks. GFLOP/s = 2*N*K*C*P*Q*R*S / time with logical C.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("conv fwd GFLOP/s per layer & fraction of roofline at 1/2/4/8 B200 vs host-CPU ref")
+HBM_FALLBACK_GBS, BF16_FALLBACK_TFLOPS = 6650.0, 1590.0
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "MEASURED_PEAKS.json (measured)"
+    except Exception:  # noqa: BLE001
+        return HBM_FALLBACK_GBS, BF16_FALLBACK_TFLOPS, "B200_PROFILING.md fallback"
+
+
+def compulsory_bytes(p, c_logical):
+    """4*(distinct input elements touched + K*C_L*R*S + N*K*P*Q)."""
+    rows = {min(oj * p.stride_h + kj - p.pad_h, 10**9) for oj in range(p.ofh) for kj in range(p.kh)}
+    cols = {oi * p.stride_w + ki - p.pad_w for oi in range(p.ofw) for ki in range(p.kw)}
+    rows = [r for r in rows if 0 <= r < p.ifh]
+    cols = [c for c in cols if 0 <= c < p.ifw]
+    touched_in = p.nImg * c_logical * len(rows) * len(cols)
+    return 4 * (touched_in + p.nOfm * p.nIfm * p.kh * p.kw + p.nImg * p.nOfm * p.ofh * p.ofw)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the measurement window."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.2)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    rows.append((float(f[0]), float(f[1]), float(f[2]), f[3], f[4], f[5], f[6], f[7]))
+                except ValueError:
+                    continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        mx = max(r[1] for r in rows)
+        load = [r for r in rows if r[2] > 250.0] or rows  # under load: board power above idle
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in load:
+            for n, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def _ref_driver_lib():
+    """oracle/_ref/libref_driver_{v4,v3}.so (the reference's emitted driver) or None."""
+    man = os.path.join(ROOT, "oracle", "_ref", "refdrv.json")
+    if not os.path.exists(man):
+        return None, None
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        flags = ""
+    tag = "v4" if " avx512f" in flags else "v3"
+    so = os.path.join(ROOT, "oracle", "_ref", f"libref_driver_{tag}.so")
+    if not os.path.exists(so):
+        return None, None
+    with open(man) as fh:
+        return ctypes.CDLL(so), json.load(fh)
+
+
+def cpu_leg(workload, conv, c_logical, sx, sw, reps, warmup):
+    """Times the CPU path on a bounded sample; returns dict (value GFLOP/s etc.)."""
+    import numpy as np  # noqa: F401
+    import oracle
+    import paper_2002_02145_b200 as ps
+    from paper_2002_02145_b200.workloads import with_images
+    lib, man = _ref_driver_lib()
+    if lib is not None and workload in man:
+        kind = "reference"
+        n = man[workload]["sample_img"]
+        fn = getattr(lib, man[workload]["symbol"])
+        fn.restype = None
+        fn.argtypes = [ctypes.c_void_p] * 3
+    else:
+        kind = "port"
+        n = None
+    p_full = ps.ConvPreset.parse(conv)
+    if n is None:  # oracle port: size the sample to ~10 s from a 1-image probe
+        p1 = ps.ConvPreset.parse(with_images(conv, 1))
+        x1 = oracle.pad_input(p1, oracle.fill_input(p1, sx, c_logical))
+        w1 = oracle.fill_filter(p1, sw, c_logical)
+        t = time.perf_counter()
+        oracle.conv_fig5(p1, x1, w1)
+        dt = max(time.perf_counter() - t, 1e-4)
+        n = max(1, min(p_full.nImg, int(10.0 / max(reps + warmup, 1) / dt * oracle.threads())))
+    p = ps.ConvPreset.parse(with_images(conv, n))
+    xpad = oracle.pad_input(p, oracle.fill_input(p, sx, c_logical))
+    w = oracle.fill_filter(p, sw, c_logical)
+    out = np.zeros((n, p.nOfm // 16, p.ofh, p.ofw, 16), np.float32)
+    times = []
+    for i in range(warmup + reps):
+        out[...] = 0
+        t = time.perf_counter()
+        if kind == "reference":
+            fn(out.ctypes.data, w.ctypes.data, xpad.ctypes.data)
+        else:
+            oracle.conv_fig5(p, xpad, w, out)
+        dt = time.perf_counter() - t
+        if i >= warmup:
+            times.append(dt)
+    flops = p.flops(c_logical)
+    best, mean = min(times), statistics.mean(times)
+    what = ("reference emitted Fig.5 driver (oracle/_ref, emit.hpp:60-134) + plain-C band microkernel"
+            if kind == "reference" else "oracle port (oracle/oracle.c Fig.5 restatement)")
+    return {"value": round(flops / mean / 1e9, 3), "unit": "GFLOP/s", "cores": oracle.threads(),
+            "kind": kind, "best_value": round(flops / best / 1e9, 3),
+            "sample": f"{n} of {p_full.nImg} images of {workload} ({flops / 1e9:.2f} GFLOP), "
+                      f"{reps} reps after {warmup} warm-up, gcc -O3 OpenMP over img; {what}",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2002_02145_b200 as ps
+    from paper_2002_02145_b200.workloads import ALL, seeds
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    conv, c_logical, cfg_id = ALL[args.workload]
+    p = ps.ConvPreset.parse(conv)
+    N = p.nImg
+    b0, b1 = rank * N // world, (rank + 1) * N // world
+    n_local = b1 - b0
+    sx, sw = seeds(cfg_id)
+    stream = torch.cuda.current_stream()
+
+    x = torch.empty(p.input_elems(), dtype=torch.float32, device=dev)
+    w = torch.empty(p.filter_elems(), dtype=torch.float32, device=dev)
+    y = torch.zeros(p.output_elems(), dtype=torch.float32, device=dev)
+    ps.fill_input(p, sx, x, c_logical=c_logical, img_begin=b0, img_count=n_local)
+    ps.fill_filter(p, sw, w, c_logical=c_logical)
+    plan = ps.ConvPlan(p, mode=args.mode, device=local_rank, recipe=args.recipe)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return [e0.elapsed_time(e1) for e0, e1 in ev]
+
+    total_flops = p.flops(c_logical)  # all ranks together
+    local_flops = p.flops(c_logical, n_img=n_local)
+    hbm_gbs, bf16_tflops, peak_src = peaks()
+    p_tf32 = bf16_tflops / 2.0
+    p_mode = p_tf32 / 3.0 if args.mode == "3xtf32" else p_tf32
+
+    with ClockSampler(local_rank) as clk:
+        # (1) the step: conv_fwd (filter repack + conv kernel), L2 flushed before each step
+        step_ms = timed(lambda: plan.forward(x, w, y, b0, n_local, stream), args.steps, args.warmup)
+        ms = statistics.mean(step_ms)
+        ms_max = max_over_ranks(ms)
+        # (2) dominant kernel alone (filter prepacked once): roofline
+        plan.prepack(w, stream)
+        kern_ms = timed(lambda: plan.forward(x, None, y, b0, n_local, stream, prepacked=True),
+                        args.steps, args.warmup)
+        kms = max_over_ranks(statistics.mean(kern_ms))
+        # (3) TF32 fast mode, same protocol
+        other = "tf32" if args.mode == "3xtf32" else "3xtf32"
+        plan2 = ps.ConvPlan(p, mode=other, device=local_rank)
+        ms2 = max_over_ranks(statistics.mean(
+            timed(lambda: plan2.forward(x, w, y, b0, n_local, stream), args.steps, args.warmup)))
+        plan2.prepack(w, stream)
+        kms2 = max_over_ranks(statistics.mean(
+            timed(lambda: plan2.forward(x, None, y, b0, n_local, stream, prepacked=True),
+                  args.steps, args.warmup)))
+        # restore this mode's output for verification
+        plan.forward(x, w, y, b0, n_local, stream)
+        # (4) end to end through the public API with host buffers
+        in_elems_img = p.input_elems(n_img=1)
+        out_elems_img = p.output_elems(n_img=1)
+        hx = torch.empty(n_local * in_elems_img, dtype=torch.float32).pin_memory()
+        hw = torch.empty(p.filter_elems(), dtype=torch.float32).pin_memory()
+        hy = torch.empty(n_local * out_elems_img, dtype=torch.float32).pin_memory()
+        hx.copy_(x[b0 * in_elems_img:b1 * in_elems_img])
+        hw.copy_(w)
+        xs = x[b0 * in_elems_img:b1 * in_elems_img]
+        ys = y[b0 * out_elems_img:b1 * out_elems_img]
+
+        def e2e_step():
+            xs.copy_(hx, non_blocking=True)
+            w.copy_(hw, non_blocking=True)
+            plan.forward(x, w, y, b0, n_local, stream)
+            hy.copy_(ys, non_blocking=True)
+
+        e2e_ms = max_over_ranks(statistics.mean(timed(e2e_step, args.steps, max(1, args.warmup))))
+    clocks = clk.summary()
+
+    # ---- verification (untimed): gather output shards to rank 0 over NCCL, check sampled images
+    verified = None
+    ys_dev = y[b0 * out_elems_img:b1 * out_elems_img].contiguous()
+    if world > 1:
+        gathered = torch.empty(world * ys_dev.numel(), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(gathered, ys_dev)
+        full_out = gathered
+    else:
+        full_out = ys_dev
+    if rank == 0 and not args.no_verify:
+        verified = verify(p, conv, c_logical, sx, sw, full_out.cpu().numpy(), N, world)
+
+    result = None
+    if rank == 0:
+        value = total_flops / (ms_max * 1e-3) / 1e9
+        f_alg = local_flops  # per launch on one GPU
+        achieved_tflops = f_alg / (kms * 1e-3) / 1e12
+        t_tensor = total_flops / world / (p_mode * 1e12)
+        b_comp = compulsory_bytes(p, c_logical) / world
+        t_hbm = b_comp / (hbm_gbs * 1e9)
+        bound = "tensor" if t_tensor >= t_hbm else "hbm"
+        if bound == "tensor":
+            roof = {"bound": "tensor", "achieved": round(achieved_tflops, 2), "peak": round(p_mode, 2),
+                    "unit": "TFLOP/s", "frac": round(achieved_tflops / p_mode, 4)}
+        else:
+            gbs = b_comp / (kms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": round(gbs / hbm_gbs, 4)}
+        roof.update({
+            "traffic": ncu_traffic(args.workload, args.mode),
+            "kernel_ms": round(kms, 4),
+            "roofline_ms": round(max(t_tensor, t_hbm) * 1e3, 4),
+            "step_frac": round(max(t_tensor, t_hbm) * 1e3 / ms_max, 4),
+            "peak_source": f"{peak_src}: bf16 {bf16_tflops} TFLOP/s /2 (tf32 rate)"
+                           + (" /3 (3xTF32: three tf32 MMAs per MAC)" if args.mode == "3xtf32" else "")
+                           + f"; HBM {hbm_gbs} GB/s",
+            "algorithmic": f"{f_alg / 1e9:.3f} GFLOP and {b_comp / 1e6:.1f} MB compulsory per launch "
+                           f"({n_local} images x 2*K*C*P*Q*R*S)"})
+        bi = 4 * (n_local * in_elems_img + p.filter_elems())
+        bo = 4 * n_local * out_elems_img
+        e2e_value = total_flops / (e2e_ms * 1e-3) / 1e9
+        tf32 = {"mode": other, "value": round(total_flops / (ms2 * 1e-3) / 1e9, 1),
+                "ms_per_step": round(ms2, 4), "kernel_ms": round(kms2, 4),
+                "kernel_tflops": round(f_alg / (kms2 * 1e-3) / 1e12, 2),
+                "frac_of_peak": round(f_alg / (kms2 * 1e-3) / 1e12 /
+                                      (p_tf32 if other == "tf32" else p_tf32 / 3), 4)}
+        result = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (3xtf32 tensor-core split, fp32 in/out)" if args.mode == "3xtf32" else "f32 in/out, tf32 tensor-core",
+            "data": "synthetic: seeded uniform[-1,1) by logical NCHW/KCRS index (BASELINE configs)",
+            "config": {"workload": f"{args.workload} {conv}", "mode": args.mode,
+                       "recipe": plan.recipe, "images_per_gpu": n_local, "parallelism": f"dp{world} (img split)",
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "c_logical": c_logical},
+            "roofline": roof,
+            "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": bi,
+                    "d2h_bytes_per_step": bo, "ms_per_step": round(e2e_ms, 3),
+                    "path": "pinned host -> device copy, ConvPlan.forward (C ABI conv_fwd), device -> pinned host"},
+            "gpu_launches": args.steps * plan.launches,
+            "clocks": clocks,
+            args.mode if args.mode != "3xtf32" else "tf32_mode": tf32,
+            "verified": verified,
+        }
+    return result
+
+
+def verify(p, conv, c_logical, sx, sw, out_flat, N, world):
+    """Untimed: sampled images (first of every shard) vs the CPU oracle."""
+    import numpy as np
+    import oracle
+    import paper_2002_02145_b200 as ps
+    from paper_2002_02145_b200.workloads import with_images
+    per = p.output_elems(n_img=1)
+    imgs = sorted({r * N // world for r in range(world)} | {N - 1})[:8]
+    p1 = ps.ConvPreset.parse(with_images(conv, N))
+    w = oracle.fill_filter(p1, sw, c_logical)
+    worst = 0.0
+    for img in imgs:
+        pi = ps.ConvPreset.parse(with_images(conv, img + 1))
+        x = oracle.fill_input(pi, sx, c_logical, img_begin=img, img_count=1)
+        ref = oracle.conv(ps.ConvPreset.parse(with_images(conv, 1)), x, w)
+        got = out_flat[img * per:(img + 1) * per]
+        worst = max(worst, oracle.rel_l2(got, ref))
+    return {"images": imgs, "max_rel_l2_vs_oracle": worst,
+            "gather": "NCCL all_gather of output shards" if world > 1 else "single GPU"}
+
+
+def ncu_traffic(workload, mode):
+    """dram bytes per launch of the conv kernel from the committed ncu capture, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        return j.get(f"{workload}/{mode}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from paper_2002_02145_b200.workloads import ALL, seeds
+    conv, c_logical, cfg_id = ALL[args.workload]
+    sx, sw = seeds(cfg_id)
+    leg = cpu_leg(args.workload, conv, c_logical, sx, sw, args.steps, args.warmup)
+    v = leg["value"]
+    return {
+        "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "impl": "reference",
+        "data": "synthetic: seeded uniform[-1,1) by logical NCHW/KCRS index (BASELINE configs)",
+        "config": {"workload": f"{args.workload} {conv}", "mode": "fp32 CPU"},
+        "cpu_baseline": {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_model": leg["cpu_model"],
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5")
+    ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--recipe", default=None)
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import torch.distributed as dist
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu:
+            from paper_2002_02145_b200.workloads import ALL, seeds
+            conv, c_logical, cfg_id = ALL[args.workload]
+            sx, sw = seeds(cfg_id)
+            leg = cpu_leg(args.workload, conv, c_logical, sx, sw, reps=3, warmup=1)
+            res["cpu_baseline"] = {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            res["cpu_baseline"]["cpu_model"] = leg["cpu_model"]
+        else:
+            res["cpu_baseline"] = None
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

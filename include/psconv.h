@@ -39,6 +39,8 @@ extern "C" {
 /* conv_fwd flags */
 #define PSCONV_FLAG_ACCUMULATE 1u /* out += conv (the reference body is `+=`,
                                      presets.hpp:112); default overwrites   */
+#define PSCONV_FLAG_PREPACKED 2u  /* use the filter already prepacked into the
+                                     plan by conv_plan_prepack (flt ignored) */
 
 /*
  * Conv-layer descriptor. Replaces nestrank::ConvPreset (presets.hpp:13-23):
@@ -108,9 +110,16 @@ const char* conv_plan_recipe(const conv_plan* p);
 /* Runs the forward conv on images [img_begin, img_begin+img_count) of the
  * caller's device arrays (full-size, pointer to image 0), stream-ordered on
  * `cuda_stream` (a cudaStream_t; NULL = legacy default). Does not allocate
- * and does not synchronise. Reentrant. */
+ * and does not synchronise. Each call first repacks `flt` into the plan's
+ * K-major operand buffer (the tcgen05 tf32 B-operand layout; plus the
+ * hi/lo split in 3xTF32 mode), so calls on ONE plan must be stream-ordered;
+ * use one plan per concurrent stream. */
 int conv_fwd(const conv_plan* p, const float* in, const float* flt, float* out, int64_t img_begin,
              int64_t img_count, void* cuda_stream, unsigned flags);
+
+/* Repacks a filter into the plan once (weights held constant, e.g. inference);
+ * later conv_fwd calls with PSCONV_FLAG_PREPACKED skip the repack launch. */
+int conv_plan_prepack(conv_plan* p, const float* flt, void* cuda_stream);
 
 /* Number of kernel launches conv_fwd issues per call (for launch accounting). */
 int conv_plan_launches(const conv_plan* p);

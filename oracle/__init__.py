@@ -76,10 +76,13 @@ def value(seed: int, idx: int) -> float:
 def fill_input(p, seed: int, c_logical: int = 0, img_begin: int = 0, img_count=None) -> np.ndarray:
     d = desc(p)
     n = p.nImg - img_begin if img_count is None else img_count
-    # the C routine indexes arrays from image 0; allocate the full prefix
-    out = np.zeros((img_begin + n, p.nIfm // 16, d.ifh, d.ifw, 16), np.float32)
-    lib.oracle_fill_input(ctypes.byref(d), seed, c_logical, _p(out), img_begin, n)
-    return out[img_begin:]
+    # the C routine indexes arrays from image 0: hand it a base shifted back by
+    # img_begin images (only images [img_begin, img_begin+n) are written)
+    out = np.zeros((n, p.nIfm // 16, d.ifh, d.ifw, 16), np.float32)
+    img_bytes = 4 * (p.nIfm // 16) * d.ifh * d.ifw * 16
+    lib.oracle_fill_input(ctypes.byref(d), seed, c_logical, _p(out) - img_begin * img_bytes,
+                          img_begin, n)
+    return out
 
 
 def fill_filter(p, seed: int, c_logical: int = 0) -> np.ndarray:

@@ -78,13 +78,31 @@ void oracle_pad_input(const oc_desc* d, const float* in, float* inp, int64_t img
  * runs over ifm = 0..15 in order, so results are those of the band order. */
 static inline void band(float* restrict o, const float* restrict f, const float* restrict x,
                         int64_t ofw, int64_t sw) {
-  for (int64_t oi = 0; oi < ofw; ++oi) {
-    float* oo = o + oi * 16;
-    const float* xx = x + oi * sw * 16;
+  /* Register-blocked over 4 output pixels (independent elements) for ILP;
+   * each element's accumulation order over ifm is unchanged. */
+  int64_t oi = 0;
+  for (; oi + 4 <= ofw; oi += 4) {
+    float acc[4][16];
+    for (int j = 0; j < 4; ++j)
+      for (int k = 0; k < 16; ++k) acc[j][k] = o[(oi + j) * 16 + k];
     for (int ifm = 0; ifm < 16; ++ifm) {
-      const float xv = xx[ifm];
-      for (int ofm = 0; ofm < 16; ++ofm) oo[ofm] = oo[ofm] + f[ifm * 16 + ofm] * xv;
+      const float* fr = f + ifm * 16;
+      for (int j = 0; j < 4; ++j) {
+        const float xv = x[(oi + j) * sw * 16 + ifm];
+        for (int k = 0; k < 16; ++k) acc[j][k] = acc[j][k] + fr[k] * xv;
+      }
     }
+    for (int j = 0; j < 4; ++j)
+      for (int k = 0; k < 16; ++k) o[(oi + j) * 16 + k] = acc[j][k];
+  }
+  for (; oi < ofw; ++oi) {
+    float acc[16];
+    for (int k = 0; k < 16; ++k) acc[k] = o[oi * 16 + k];
+    for (int ifm = 0; ifm < 16; ++ifm) {
+      const float xv = x[oi * sw * 16 + ifm];
+      for (int k = 0; k < 16; ++k) acc[k] = acc[k] + f[ifm * 16 + k] * xv;
+    }
+    for (int k = 0; k < 16; ++k) o[oi * 16 + k] = acc[k];
   }
 }
 

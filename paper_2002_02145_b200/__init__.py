@@ -33,6 +33,7 @@ __all__ = [
 MODE_3XTF32 = 0
 MODE_TF32 = 1
 FLAG_ACCUMULATE = 1
+FLAG_PREPACKED = 2
 _MODES = {"3xtf32": MODE_3XTF32, "tf32": MODE_TF32}
 
 
@@ -177,13 +178,18 @@ class ConvPlan:
         lib.conv_plan_emit(self._h, buf, len(buf))
         return buf.value.decode()
 
+    def prepack(self, flt, stream=None) -> None:
+        """Repack a constant filter once; then forward(..., prepacked=True) skips that launch."""
+        _check(lib.conv_plan_prepack(self._h, _ptr(flt), _stream_ptr(stream)))
+
     def forward(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
-                stream=None, accumulate: bool = False) -> None:
+                stream=None, accumulate: bool = False, prepacked: bool = False) -> None:
         """Device pointers or CUDA tensors in NCHW16c / KCRS16c16k / NKPQ16k."""
         if img_count is None:
             img_count = self.preset.nImg - img_begin
-        _check(lib.conv_fwd(self._h, _ptr(inp), _ptr(flt), _ptr(out), img_begin, img_count,
-                            _stream_ptr(stream), FLAG_ACCUMULATE if accumulate else 0))
+        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_PREPACKED if prepacked else 0)
+        _check(lib.conv_fwd(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
+                            img_begin, img_count, _stream_ptr(stream), flags))
 
     __call__ = forward
 

@@ -46,6 +46,7 @@ _sigs = {
     "conv_plan_recipe": (ctypes.c_char_p, [c_vp]),
     "conv_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
     "conv_plan_launches": (ctypes.c_int, [c_vp]),
+    "conv_plan_prepack": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "conv_plan_emit": (c_i64, [c_vp, ctypes.c_char_p, ctypes.c_size_t]),
     "conv_emit_driver": (c_i64, [_P(conv_desc), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
     "conv_select_topk": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,

@@ -23,6 +23,7 @@ struct conv_plan {
   int num_sms;
   psconv::Schedule sched;
   float* flt_pack = nullptr;   // prepacked K-major filter [CRS][K][16c]: hi (| lo for 3xTF32)
+  mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
 };
 
@@ -192,6 +193,15 @@ __global__ void unpack_output_kernel(const float* __restrict__ in16, float* __re
   }
 }
 
+void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
+  const int Kb = int(P->d.nOfm / 16), CRS = int(P->d.nIfm / 16 * P->d.kh * P->d.kw);
+  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+  prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
+                                                  split3 ? P->flt_pack + P->flt_elems : nullptr,
+                                                  int(P->d.nOfm), CRS, split3 ? 1 : 0);
+  CUDA_OK(cudaGetLastError());
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -336,7 +346,10 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
              int64_t img_count, void* stream, unsigned flags) {
   return guarded([&] {
     if (!P) throw ConfigError("null plan");
-    if (!in || !flt || !out) throw ConfigError("null tensor pointer");
+    const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
+    if (!in || !out || (!flt && !prepacked)) throw ConfigError("null tensor pointer");
+    if (prepacked && !P->prepacked) throw ConfigError("PSCONV_FLAG_PREPACKED without conv_plan_prepack");
+    if (prepacked) flt = in;  // unused; keeps the alignment check below simple
     const conv_desc& d = P->d;
     if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
       throw ConfigError("image range [" + std::to_string(img_begin) + ", " +
@@ -371,10 +384,10 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     const int K = Kb * 16;
     const float* b_hi = P->flt_pack;
     const float* b_lo = split3 ? P->flt_pack + P->flt_elems : P->flt_pack;
-    prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
-                                                    split3 ? P->flt_pack + P->flt_elems : nullptr, K,
-                                                    CRS, split3 ? 1 : 0);
-    CUDA_OK(cudaGetLastError());
+    if (!prepacked) {
+      launch_prepack(P, flt, st);
+      P->prepacked = false;  // buffer now holds this call's filter
+    }
     {
       const cuuint64_t dims[3] = {16, cuuint64_t(K), cuuint64_t(CRS)};
       const cuuint64_t strides[2] = {64, cuuint64_t(K) * 64};
@@ -420,6 +433,15 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       dispatch_bn<true>(s.bn, P, prm, ta, tb, tblo, st);
     else
       dispatch_bn<false>(s.bn, P, prm, ta, tb, tblo, st);
+  });
+}
+
+int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
+  return guarded([&] {
+    if (!P || !flt) throw ConfigError("null argument");
+    if (reinterpret_cast<uintptr_t>(flt) & 15) throw ConfigError("filter must be 16-byte aligned");
+    launch_prepack(P, flt, static_cast<cudaStream_t>(stream));
+    P->prepacked = true;
   });
 }
 

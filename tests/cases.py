@@ -1,51 +1,2 @@
-"""Named conv shapes: BASELINE.json configs and the ResNet-50 layer sweep (SURVEY.md §8 table,
-§8(d) roofline table), as `conv:` strings in the reference's field order plus the pad
-extension (pad_h, pad_w, ifh, ifw)."""
-
-# name -> (conv string with 14 fields, logical input channels, seed offset id)
-BASELINE = {
-    "cfg1": ("conv:28,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, 1),
-    "cfg2": ("conv:28,64,256,56,56,1,1,1,1,16,0,0,56,56", 256, 2),
-    "cfg3": ("conv:56,128,128,28,28,3,3,2,2,16,1,1,56,56", 128, 3),
-    "cfg5": ("conv:2048,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, 5),
-}
-
-# ResNet-50 distinct conv shapes at N=256 (BASELINE.json configs[3]); stem C=3 padded to 16.
-R50 = {
-    "r50_stem": ("conv:256,64,16,112,112,7,7,2,2,16,3,3,224,224", 3, 100),
-    "r50_l1_1x1_64_64": ("conv:256,64,64,56,56,1,1,1,1,16,0,0,56,56", 64, 101),
-    "r50_l1_3x3_64_64": ("conv:256,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, 102),
-    "r50_l1_1x1_64_256": ("conv:256,256,64,56,56,1,1,1,1,16,0,0,56,56", 64, 103),
-    "r50_l1_1x1_256_64": ("conv:256,64,256,56,56,1,1,1,1,16,0,0,56,56", 256, 104),
-    "r50_l2_1x1_256_128": ("conv:256,128,256,56,56,1,1,1,1,16,0,0,56,56", 256, 105),
-    "r50_l2_3x3s2_128_128": ("conv:256,128,128,28,28,3,3,2,2,16,1,1,56,56", 128, 106),
-    "r50_l2_1x1_128_512": ("conv:256,512,128,28,28,1,1,1,1,16,0,0,28,28", 128, 107),
-    "r50_l2_ds_1x1s2_256_512": ("conv:256,512,256,28,28,1,1,2,2,16,0,0,56,56", 256, 108),
-    "r50_l2_1x1_512_128": ("conv:256,128,512,28,28,1,1,1,1,16,0,0,28,28", 512, 109),
-    "r50_l2_3x3_128_128": ("conv:256,128,128,28,28,3,3,1,1,16,1,1,28,28", 128, 110),
-    "r50_l3_1x1_512_256": ("conv:256,256,512,28,28,1,1,1,1,16,0,0,28,28", 512, 111),
-    "r50_l3_3x3s2_256_256": ("conv:256,256,256,14,14,3,3,2,2,16,1,1,28,28", 256, 112),
-    "r50_l3_1x1_256_1024": ("conv:256,1024,256,14,14,1,1,1,1,16,0,0,14,14", 256, 113),
-    "r50_l3_ds_1x1s2_512_1024": ("conv:256,1024,512,14,14,1,1,2,2,16,0,0,28,28", 512, 114),
-    "r50_l3_1x1_1024_256": ("conv:256,256,1024,14,14,1,1,1,1,16,0,0,14,14", 1024, 115),
-    "r50_l3_3x3_256_256": ("conv:256,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, 116),
-    "r50_l4_1x1_1024_512": ("conv:256,512,1024,14,14,1,1,1,1,16,0,0,14,14", 1024, 117),
-    "r50_l4_3x3s2_512_512": ("conv:256,512,512,7,7,3,3,2,2,16,1,1,14,14", 512, 118),
-    "r50_l4_1x1_512_2048": ("conv:256,2048,512,7,7,1,1,1,1,16,0,0,7,7", 512, 119),
-    "r50_l4_ds_1x1s2_1024_2048": ("conv:256,2048,1024,7,7,1,1,2,2,16,0,0,14,14", 1024, 120),
-    "r50_l4_1x1_2048_512": ("conv:256,512,2048,7,7,1,1,1,1,16,0,0,7,7", 2048, 121),
-    "r50_l4_3x3_512_512": ("conv:256,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, 122),
-}
-
-ALL = {**BASELINE, **R50}
-
-
-def seeds(cfg_id: int):
-    """Activation / weight seeds: 1000+id, 2000+id."""
-    return 1000 + cfg_id, 2000 + cfg_id
-
-
-def with_images(conv: str, n: int) -> str:
-    f = conv.split(":", 1)[1].split(",")
-    f[0] = str(n)
-    return "conv:" + ",".join(f)
+"""Test-side view of the named workloads (defined with the package: paper_2002_02145_b200/workloads.py)."""
+from paper_2002_02145_b200.workloads import ALL, BASELINE, R50, seeds, with_images  # noqa: F401
