@@ -49,7 +49,7 @@ def compulsory_bytes(p, c_logical):
     cols = {oi * p.stride_w + ki - p.pad_w for oi in range(p.ofw) for ki in range(p.kw)}
     rows = [r for r in rows if 0 <= r < p.ifh]
     cols = [c for c in cols if 0 <= c < p.ifw]
-    touched_in = p.nImg * c_logical * len(rows) * len(cols)
+    touched_in = p.nImg * p.nIfm * len(rows) * len(cols)  # C_L = layout channels (stem 16)
     return 4 * (touched_in + p.nOfm * p.nIfm * p.kh * p.kw + p.nImg * p.nOfm * p.ofh * p.ofw)
 
 

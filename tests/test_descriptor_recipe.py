@@ -1,0 +1,104 @@
+"""Host logic (CPU): conv-layer descriptor and recipe grammar, mirroring the reference's
+ConvPreset (presets.hpp:26-58), the `conv:` loader (cli.hpp:54-66) and VariantRecipe /
+plan_recipe (variants.hpp:16-65, 186-228), with the reference's error classes (status 2)."""
+import os
+
+import pytest
+
+import paper_2002_02145_b200 as ps
+from paper_2002_02145_b200 import ConfigRejectedError, ConvPreset
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_default_preset_fields():
+    p = ConvPreset.parse("conv:2,32,32,4,4,3,3,1,1,16")
+    assert (p.nImg, p.nOfm, p.nIfm, p.ofh, p.ofw, p.kh, p.kw, p.stride_h, p.stride_w,
+            p.gemm_block) == (2, 32, 32, 4, 4, 3, 3, 1, 1, 16)
+    assert (p.pad_h, p.pad_w, p.ifh, p.ifw) == (0, 0, 6, 6)  # implied extent (presets.hpp:88-91)
+    assert str(p) == "conv:2,32,32,4,4,3,3,1,1,16"
+
+
+@pytest.mark.parametrize("bad", [
+    "conv:1,2,3",                               # tests/test_cli.cpp:295 (not 10 ints)
+    "conv:2,33,32,4,4,3,3,1,1,16",              # tests/test_cli.cpp:296 (33 % 16)
+    "conv:2,32,32,4,4,3,3,1,0,16",              # non-positive
+    "conv:2,32,32,4,4,3,3,1,1,16,1",            # 11 values
+    "conv:2,32,32,4,4,x,3,1,1,16",              # bad value
+    "gemm:2,32,32,4,4,3,3,1,1,16",              # unknown preset kind
+    "conv:2,32,32,4,4,3,3,1,1,16,3,0,4,4",      # pad >= kh
+    "conv:2,32,32,4,4,3,3,1,1,16,1,1,2,2",      # input too small for ofh
+])
+def test_rejected_descriptors(bad):
+    with pytest.raises(ConfigRejectedError):
+        ConvPreset.parse(bad)
+
+
+def test_whitespace_and_empty_fields_like_reference():
+    # presets.hpp:29-42: whitespace dropped, empty fields skipped
+    p = ConvPreset.parse("conv: 2, 32,,32 ,4,4,3,3,1,1,16")
+    assert (p.nImg, p.nOfm, p.nIfm) == (2, 32, 32)
+    q = ConvPreset.parse("2,32,32,4,4,3,3,1,1,16")  # ConvPreset::parse form (no prefix)
+    assert q == p
+
+
+def test_extension_round_trip():
+    s = "conv:56,128,128,28,28,3,3,2,2,16,1,1,56,56"
+    p = ConvPreset.parse(s)
+    assert str(p) == s and ConvPreset.parse(str(p)) == p
+    assert p.flops() == 2 * 56 * 128 * 128 * 28 * 28 * 9
+
+
+@pytest.mark.parametrize("i", range(7))
+def test_emission_matches_reference_emitter(i):
+    import json
+    idx = json.load(open(os.path.join(GOLDEN, "index.json")))["emit"][i]
+    want = open(os.path.join(GOLDEN, idx["file"])).read()
+    got = ps.emit_driver(ConvPreset.parse(idx["conv"]), idx["recipe"])
+    assert got == want
+
+
+@pytest.mark.parametrize("recipe", [
+    "perm=oi,ofm_tile",          # band loop permuted (InvalidPermutationError)
+    "perm=ofm_tile,ofm_tile",    # listed twice
+    "perm=foo",                  # unknown loop
+    "tile=oj:0",                 # TileSizeNonPositiveError
+    "tile=ifm:2",                # tiles band loop
+    "tile=oj",                   # bad entry
+    "order=ofm_tile",            # unknown clause
+    "tile=oj:2,oj:4",            # tiled twice
+])
+def test_rejected_recipes(recipe):
+    with pytest.raises(ConfigRejectedError):
+        ps.emit_driver(ConvPreset(), recipe)
+
+
+def test_select_topk_deterministic_and_resolvable():
+    p = ConvPreset.parse("conv:2048,256,256,14,14,3,3,1,1,16,1,1,14,14")
+    a = ps.select_topk(p, "3xtf32", 5)
+    b = ps.select_topk(p, "3xtf32", 5)
+    assert a == b and len(a) == 5
+    us = [u for _, u in a]
+    assert us == sorted(us)
+    for rid, u in a:
+        assert rid.startswith("perm=") and ";gpu=bn:" in rid
+        assert abs(ps.model_us(p, rid, "3xtf32") - u) < 1e-6 * max(1.0, u)
+
+
+def test_model_scales_with_work():
+    small = ConvPreset.parse("conv:256,256,256,14,14,3,3,1,1,16,1,1,14,14")
+    big = ConvPreset.parse("conv:2048,256,256,14,14,3,3,1,1,16,1,1,14,14")
+    r = "perm=ofm_tile,ifm_tile,oj,kj,ki;gpu=bn:256,box:2x2x32"
+    assert ps.model_us(big, r) > 4 * ps.model_us(small, r)
+    assert ps.model_us(big, r, "tf32") < ps.model_us(big, r, "3xtf32")
+
+
+def test_gpu_clause_validation():
+    p = ConvPreset.parse("conv:8,64,64,8,8,3,3,1,1,16,1,1,8,8")
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(p, "gpu=bn:48")             # not a supported tile width
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(p, "gpu=bn:128")            # 64 % 128
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(p, "gpu=box:16x16x1")       # > 128 rows
+    assert ps.model_us(p, "gpu=bn:32,box:8x8x2,ch:4") > 0
