@@ -218,7 +218,20 @@ def run_ours(args, rank, world, local_rank):
     y = torch.zeros(p.output_elems(), dtype=torch.float32, device=dev)
     ps.fill_input(p, sx, x, c_logical=c_logical, img_begin=b0, img_count=n_local)
     ps.fill_filter(p, sw, w, c_logical=c_logical)
-    plan = ps.ConvPlan(p, mode=args.mode, device=local_rank, recipe=args.recipe)
+    # schedule: the selector's model top-k timed on the device (untimed plan creation,
+    # PAPER.md:224-226), rank 0's choice broadcast so every rank runs the same recipe
+    recipes = {args.mode: args.recipe, "tf32" if args.mode == "3xtf32" else "3xtf32": None}
+    if args.tune > 0:
+        from paper_2002_02145_b200.tune import autotune
+        for m in list(recipes):
+            if recipes[m] is None and rank == 0:
+                recipes[m] = autotune(p, m, k=args.tune, device=local_rank, c_logical=c_logical,
+                                      seeds=(sx, sw))[0]
+        if world > 1:
+            obj = [recipes]
+            dist.broadcast_object_list(obj, src=0)
+            recipes = obj[0]
+    plan = ps.ConvPlan(p, mode=args.mode, device=local_rank, recipe=recipes[args.mode])
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
     def barrier():
@@ -267,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
         kms = max_over_ranks(statistics.mean(kern_ms))
         # (3) TF32 fast mode, same protocol
         other = "tf32" if args.mode == "3xtf32" else "3xtf32"
-        plan2 = ps.ConvPlan(p, mode=other, device=local_rank)
+        plan2 = ps.ConvPlan(p, mode=other, device=local_rank, recipe=recipes[other])
         ms2 = max_over_ranks(statistics.mean(
             timed(lambda: plan2.forward(x, w, y, b0, n_local, stream), args.steps, args.warmup)))
         plan2.prepack(w, stream)
@@ -426,6 +439,8 @@ def main():
     ap.add_argument("--workload", default="cfg5")
     ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--recipe", default=None)
+    ap.add_argument("--tune", type=int, default=4,
+                    help="time the selector's top-k recipes before the run (0: model top-1)")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()

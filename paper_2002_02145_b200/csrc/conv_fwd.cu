@@ -210,32 +210,59 @@ int grid_for(int64_t n) {
 }
 
 // ---------------------------------------------------------------- launch
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, int CS>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
-  using Cfg = KernelCfg<BN, SPLIT3>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-  });
-  CUDA_OK(attr_err);
-  int grid = prm.num_tiles < P->num_sms ? prm.num_tiles : P->num_sms;
-  conv_fwd_sm100<BN, SPLIT3><<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(prm, a, b, blo);
-  CUDA_OK(cudaGetLastError());
+  if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2)) {
+    throw RuntimeError("unsupported (bn, cluster, mode) combination");
+  } else {
+    constexpr bool PAIR = CS == 2;
+    using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    });
+    CUDA_OK(attr_err);
+    const int max_clusters = P->num_sms / CS;
+    const int clusters = prm.groups < max_clusters ? prm.groups : max_clusters;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * CS);
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo));
+  }
 }
 
-template <bool SPLIT3>
+template <bool SPLIT3, int CS>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_conv<16, SPLIT3>(P, prm, a, b, blo, st);
-    case 32: return launch_conv<32, SPLIT3>(P, prm, a, b, blo, st);
-    case 64: return launch_conv<64, SPLIT3>(P, prm, a, b, blo, st);
-    case 128: return launch_conv<128, SPLIT3>(P, prm, a, b, blo, st);
-    case 256: return launch_conv<256, SPLIT3>(P, prm, a, b, blo, st);
+    case 16: return launch_conv<16, SPLIT3, CS>(P, prm, a, b, blo, st);
+    case 32: return launch_conv<32, SPLIT3, CS>(P, prm, a, b, blo, st);
+    case 64: return launch_conv<64, SPLIT3, CS>(P, prm, a, b, blo, st);
+    case 128: return launch_conv<128, SPLIT3, CS>(P, prm, a, b, blo, st);
+    case 256: return launch_conv<256, SPLIT3, CS>(P, prm, a, b, blo, st);
     default: throw RuntimeError("unsupported bn");
+  }
+}
+
+template <bool SPLIT3>
+void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
+                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+  switch (cs) {
+    case 1: return dispatch_bn<SPLIT3, 1>(bn, P, prm, a, b, blo, st);
+    case 2: return dispatch_bn<SPLIT3, 2>(bn, P, prm, a, b, blo, st);
+    default: throw RuntimeError("unsupported cluster size");
   }
 }
 
@@ -391,7 +418,7 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     {
       const cuuint64_t dims[3] = {16, cuuint64_t(K), cuuint64_t(CRS)};
       const cuuint64_t strides[2] = {64, cuuint64_t(K) * 64};
-      const cuuint32_t box[3] = {16, cuuint32_t(s.bn), 1};
+      const cuuint32_t box[3] = {16, cuuint32_t(s.bn / s.cs), 1};  // one cluster CTA's piece
       const cuuint32_t estr[3] = {1, 1, 1};
       encode(&tb, b_hi, 3, dims, strides, box, estr);
       encode(&tblo, b_lo, 3, dims, strides, box, estr);
@@ -417,22 +444,27 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.tiles_p = (Pp + s.pb - 1) / s.pb;
     prm.tiles_n = int((img_count + s.nb - 1) / s.nb);
     prm.tiles_k = int(d.nOfm / s.bn);
-    const int64_t nt = int64_t(prm.tiles_q) * prm.tiles_p * prm.tiles_n * prm.tiles_k;
-    if (nt >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
-    prm.num_tiles = int(nt);
+    const int64_t mt = int64_t(prm.tiles_q) * prm.tiles_p * prm.tiles_n;
+    const int64_t mg = (mt + s.cs - 1) / s.cs;
+    if (mg * prm.tiles_k >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
+    prm.mtiles = int(mt);
+    prm.mgroups = int(mg);
+    prm.groups = int(mg * prm.tiles_k);
+    // recipe loop order -> rasterisation: pixel-loop order and ofm_tile position
+    int pos[3];
+    for (int i = 0; i < 3; ++i) pos[s.raster[i]] = i;
+    prm.m_order = pos[0] < pos[2] ? 0 : 1;
+    prm.k_outer = pos[1] == 0 ? 1 : 0;
     prm.ksteps = Cb * R * S;
     prm.chunk_ksteps = s.chunk > 0 ? s.chunk : prm.ksteps;
-    for (int i = 0; i < 3; ++i) {
-      prm.raster[i] = s.raster[i];
-      prm.kord[i] = s.kord[i];
-    }
+    for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
     prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
     prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
     prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
     if (split3)
-      dispatch_bn<true>(s.bn, P, prm, ta, tb, tblo, st);
+      dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, st);
     else
-      dispatch_bn<false>(s.bn, P, prm, ta, tb, tblo, st);
+      dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, st);
   });
 }
 

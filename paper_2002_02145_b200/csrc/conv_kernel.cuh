@@ -12,15 +12,24 @@
 //   K = (ifm_tile, kj, ki, ifm)-> one k-step = one (ifm_tile,kj,ki) triple =
 //                                 16 channels = two tcgen05 K=8 tf32 MMAs
 // i.e. each k-step is exactly the reference microkernel call batch-reduced
-// over 128 output pixels and BN output channels.
+// over 128 (or, for a CTA pair, 256) output pixels and BN output channels.
 //
 // Warp roles (persistent CTA, one per SM):
 //   warp 0      TMA producer: A box (NCHW16c, padding = TMA OOB zero fill,
-//               stride = TMA element strides) + B block (filter prepacked
-//               K-major as [C*R*S/16][K][16c], see conv_fwd.cu)
-//   warp 1      TMEM owner + single-thread tcgen05.mma issuer
+//               stride = TMA element strides) + this CTA's rows of the B block
+//               (filter prepacked K-major [C*R*S/16][K][16c])
+//   warp 1      TMEM owner; MMA issuer (single CTA, or the pair's leader);
+//               in the pair's second CTA: forwards "stage ready" to the leader
 //   warps 2-5   epilogue: tcgen05.ld -> registers -> st.global.v4 (NKPQ16k)
 //   warps 6-9   (3xTF32 only) splitter: A -> lo = A - tf32(A) in shared memory
+//
+// PAIR (cluster of 2, tcgen05.mma.cta_group::2, M = 256): the two SMs of a
+// pair work on two 128-pixel tiles with the same BN output channels; each CTA
+// stages its own A tile and HALF of the B block, and the leader issues one
+// M=256 MMA that reads A from both SMs and B halves from both. Measured on B200
+// (r01 model fit) the single-CTA kernel is bound by ~128 B/cycle/SM of shared
+// memory traffic (tensor-core operand reads + TMA writes + splitter); the pair
+// halves the B share of both, so the loop becomes MMA-bound.
 //
 // Numerics (measured on B200, tools/probe2.cu): kind::tf32 reads fp32 operands
 // by truncating the 13 low mantissa bits, so A_hi is the raw fp32 tile and only
@@ -42,25 +51,29 @@ struct ConvParams {
   int Qb, Pb, Nb;                 // M-tile box in output pixels (Qb*Pb*Nb <= 128)
   int tiles_q, tiles_p, tiles_n;  // M-tile grid
   int tiles_k;                    // N tiles (K / BN)
-  int num_tiles, ksteps;          // ksteps = Cb*R*S
+  int mtiles, mgroups, groups;    // M tiles; groups of CS M tiles; groups * tiles_k
+  int m_order;                    // 0: img outer of oj, 1: oj outer of img (oi innermost)
+  int k_outer;                    // 1: ofm_tile outer of the pixel loops (recipe order)
+  int ksteps;                     // Cb*R*S
   int chunk_ksteps;               // k-steps per TMEM accumulation chunk
-  int raster[3];                  // tile order outer->inner over {0 img, 1 ofm_tile, 2 oj}
   int kord[3];                    // k-step order outer->inner over {0 ifm_tile, 1 kj, 2 ki}
   int accumulate;                 // out += conv
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
 };
 
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, bool PAIR>
 struct KernelCfg {
-  static constexpr int kABytes = 128 * 64;  // 128 pixels x 16 fp32 channels
-  static constexpr int kBBytes = BN * 64;   // BN output channels x 16 input channels (K-major)
+  static constexpr int kCS = PAIR ? 2 : 1;
+  static constexpr int kBRows = BN / kCS;     // B rows staged per CTA
+  static constexpr int kABytes = 128 * 64;    // 128 pixels x 16 fp32 channels
+  static constexpr int kBBytes = kBRows * 64; // kBRows output channels x 16 input channels
   // stage: [A | A_lo (3x) | B_hi | B_lo (3x)]
   static constexpr int kStageBytes = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);
   static constexpr int kBudget = 200 * 1024;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  // TMEM: kAccBufs chunk accumulators (+ one running-sum region in 3x mode)
+  // TMEM (per CTA: 128 lanes x BN columns per accumulator)
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
   static constexpr int kSumCol = kAccBufs * BN;
   static constexpr int kColsNeeded = kAccBufs * BN + (SPLIT3 ? BN : 0);
@@ -72,57 +85,60 @@ struct KernelCfg {
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // +align slack
+  static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
+  static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
   static_assert(kStages >= 2, "stages");
   static_assert(kColsNeeded <= 512, "TMEM");
+  // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
+  // a cluster-scope release per k-step (MEMBAR.GPU, measured ~3x slower).
+  static_assert(!(PAIR && SPLIT3), "CTA pair is used for TF32 only");
 };
 
 struct TileCoord {
   int tn, tp, tq, tk;
+  bool live;  // false: padding tile of the last pair group (no stores)
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
+__device__ __forceinline__ TileCoord decode_group(const ConvParams& p, int g, int rank, int CS) {
   TileCoord c;
-  c.tq = t % p.tiles_q;
-  int rem = t / p.tiles_q;
-  const int e2 = p.raster[2] == 0 ? p.tiles_n : (p.raster[2] == 1 ? p.tiles_k : p.tiles_p);
-  const int e1 = p.raster[1] == 0 ? p.tiles_n : (p.raster[1] == 1 ? p.tiles_k : p.tiles_p);
-  const int v2 = rem % e2;
-  rem /= e2;
-  const int v1 = rem % e1;
-  const int v0 = rem / e1;
-  c.tn = p.raster[0] == 0 ? v0 : (p.raster[1] == 0 ? v1 : v2);
-  c.tk = p.raster[0] == 1 ? v0 : (p.raster[1] == 1 ? v1 : v2);
-  c.tp = p.raster[0] == 2 ? v0 : (p.raster[1] == 2 ? v1 : v2);
+  int mg;
+  if (p.k_outer) {
+    c.tk = g / p.mgroups;
+    mg = g - c.tk * p.mgroups;
+  } else {
+    mg = g / p.tiles_k;
+    c.tk = g - mg * p.tiles_k;
+  }
+  const int m = mg * CS + rank;
+  c.live = m < p.mtiles;
+  c.tq = m % p.tiles_q;
+  const int rest = m / p.tiles_q;
+  if (p.m_order == 0) {
+    c.tp = rest % p.tiles_p;
+    c.tn = rest / p.tiles_p;  // may exceed tiles_n for padding tiles -> TMA OOB zeros
+  } else {
+    c.tn = rest % p.tiles_n;
+    c.tp = rest / p.tiles_n;
+  }
   return c;
 }
 
-__device__ __forceinline__ void decode_kstep(const ConvParams& p, int ks, int& cb, int& r, int& s) {
-  const int d2 = p.kord[2], d1 = p.kord[1], d0 = p.kord[0];
-  const int e2 = d2 == 0 ? p.Cb : (d2 == 1 ? p.R : p.S);
-  const int e1 = d1 == 0 ? p.Cb : (d1 == 1 ? p.R : p.S);
-  const int v2 = ks % e2;
-  ks /= e2;
-  const int v1 = ks % e1;
-  const int v0 = ks / e1;
-  cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
-  r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
-  s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
-}
-
-template <int BN, bool SPLIT3>
-__global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
+template <int BN, bool SPLIT3, bool PAIR>
+__global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
                    const __grid_constant__ CUtensorMap tmap_flt_lo) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using Cfg = KernelCfg<BN, SPLIT3>;
+  using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+  constexpr int CS = Cfg::kCS;
   constexpr int kStages = Cfg::kStages;
   constexpr int kAccBufs = Cfg::kAccBufs;
-  constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN>();
+  constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B).
+  // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B). The offset is the
+  // same in both CTAs of a pair, which the pair MMA relies on.
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   auto a_buf = [&](int s) { return smem + s * Cfg::kStageBytes; };
@@ -133,15 +149,19 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
   auto blo_buf = [&](int s) { return b_buf(s) + Cfg::kBBytes; };
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
-  uint64_t* full = bars;                     // TMA landed           (count 1 + tx)
-  uint64_t* split_full = bars + kStages;     // splitter done        (count 128)
-  uint64_t* empty = bars + 2 * kStages;      // MMA consumed stage   (tcgen05.commit)
-  uint64_t* acc_full = bars + 3 * kStages;   // chunk accumulator ready   [kAccBufs]
-  uint64_t* acc_empty = acc_full + 2;        // chunk accumulator drained [kAccBufs] (count 128)
+  uint64_t* full = bars;                     // own TMA landed (1 arrive + tx)
+  uint64_t* split_full = bars + kStages;     // own splitter done (count 128)
+  uint64_t* empty = bars + 2 * kStages;      // MMA consumed the stage (commit, pair: both CTAs)
+  uint64_t* peer_full = bars + 3 * kStages;  // leader: the peer's stage is ready (count 1, remote)
+  uint64_t* acc_full = bars + 4 * kStages;   // chunk accumulator ready   [kAccBufs]
+  uint64_t* acc_empty = acc_full + 2;        // chunk accumulator drained [kAccBufs] (4 warps x CS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+  const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / CS;
+  const int nclusters = gridDim.x / CS;
   const int nchunks = (p.ksteps + p.chunk_ksteps - 1) / p.chunk_ksteps;
 
   if (threadIdx.x == 0) {
@@ -149,163 +169,246 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&split_full[s], 128);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&peer_full[s], 1);
     }
     for (int a = 0; a < kAccBufs; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
-      ptx::mbar_init(&acc_empty[a], 128);
+      ptx::mbar_init(&acc_empty[a], 4 * CS);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 1) {
+    if (PAIR)
+      ptx::tmem_alloc_pair(tmem_slot, Cfg::kTmemCols);
+    else
+      ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    // Warp-uniform loop (all lanes iterate, one elected lane issues): keeps the
+    // coordinates in uniform registers; k-step coordinates advance
+    // incrementally in the recipe's reduction order (no divisions).
+    if (ptx::elect_one()) {
       ptx::prefetch_tmap(&tmap_in);
       ptx::prefetch_tmap(&tmap_flt);
       if (SPLIT3) ptx::prefetch_tmap(&tmap_flt_lo);
-      const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
-      const uint32_t tx = (a_bytes + Cfg::kBBytes * (SPLIT3 ? 2 : 1));
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const TileCoord tc = decode_tile(p, t);
-        const int wq = tc.tq * p.Qb * p.sw - p.pw;
-        const int hp = tc.tp * p.Pb * p.sh - p.ph;
-        const int n0 = tc.tn * p.Nb;
-        const int k0 = tc.tk * BN;
-        for (int ks = 0; ks < p.ksteps; ++ks) {
-          int cb, r, s;
-          decode_kstep(p, ks, cb, r, s);
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full[stage], tx);
-          ptx::tma_load_5d(a_buf(stage), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
-          const int crs = (cb * p.R + r) * p.S + s;
-          ptx::tma_load_3d(b_buf(stage), &tmap_flt, &full[stage], 0, k0, crs);
-          if (SPLIT3) ptx::tma_load_3d(blo_buf(stage), &tmap_flt_lo, &full[stage], 0, k0, crs);
+    }
+    __syncwarp();
+    const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
+    // PAIR: both CTAs' loads complete on the LEADER's full barrier (the leader
+    // expects both shares); the second CTA never arrives on its own.
+    const uint32_t tx = (a_bytes + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;
+    const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
+    const int d0 = p.kord[0], d1 = p.kord[1], d2 = p.kord[2];
+    const int e1 = d1 == 0 ? p.Cb : (d1 == 1 ? p.R : p.S);
+    const int e2 = d2 == 0 ? p.Cb : (d2 == 1 ? p.R : p.S);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int g = cluster; g < p.groups; g += nclusters) {
+      const TileCoord tc = decode_group(p, g, rank, CS);
+      const int wq = tc.tq * p.Qb * p.sw - p.pw;
+      const int hp = tc.tp * p.Pb * p.sh - p.ph;
+      const int n0 = tc.tn * p.Nb;
+      const int k0 = tc.tk * BN + rank * Cfg::kBRows;
+      int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
+      for (int ks = 0; ks < p.ksteps; ++ks) {
+        const int cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
+        const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
+        const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
+        const int crs = (cb * p.R + r) * p.S + s;
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (ptx::elect_one()) {
+          if (!PAIR) {
+            ptx::mbar_expect_tx(&full[stage], tx);
+            ptx::tma_load_5d(a_buf(stage), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
+            ptx::tma_load_3d(b_buf(stage), &tmap_flt, &full[stage], 0, k0, crs);
+            if (SPLIT3) ptx::tma_load_3d(blo_buf(stage), &tmap_flt_lo, &full[stage], 0, k0, crs);
+          } else {
+            if (leader) ptx::mbar_expect_tx(&full[stage], tx);
+            const uint32_t fb = full_leader + 8u * stage;
+            ptx::tma_load_5d_cb(a_buf(stage), &tmap_in, fb, 0, wq + s, hp + r, cb, n0);
+            ptx::tma_load_3d_cb(b_buf(stage), &tmap_flt, fb, 0, k0, crs);
+          }
+        }
+        __syncwarp();
+        if (++v2 == e2) {
+          v2 = 0;
+          if (++v1 == e1) {
+            v1 = 0;
+            ++v0;
+          }
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && leader) {
+    // ------------------------------------------------------------ MMA issuer
+    // Warp-uniform loop; one elected lane issues tcgen05.mma / commit.
+    // Descriptors: A and B are K-major SW64 (64-B rows, 8-row groups 512 B
+    // apart); K half h (channels 8h..8h+7) starts 32 B (2 x 16 B) into the row.
+    const uint64_t desc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
+    constexpr uint32_t kStageDesc = Cfg::kStageBytes >> 4;
+    constexpr uint32_t kAloDesc = Cfg::kABytes >> 4;
+    constexpr uint32_t kBDesc = (Cfg::kABytes * (SPLIT3 ? 2 : 1)) >> 4;
+    constexpr uint32_t kBloDesc = kBDesc + (Cfg::kBBytes >> 4);
+    int stage = 0;
+    uint32_t phase = 0;
+    int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
+    for (int g = cluster; g < p.groups; g += nclusters) {
+      for (int c = 0; c < nchunks; ++c, ++cit) {
+        const int buf = kAccBufs == 1 ? 0 : (cit & 1);
+        const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
+        if (PAIR)
+          ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
+        else
+          ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+        const int ks0 = c * p.chunk_ksteps;
+        const int ks_end = min(p.ksteps, ks0 + p.chunk_ksteps);
+        for (int ks = ks0; ks < ks_end; ++ks) {
+          ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
+          if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t ds = desc0 + static_cast<uint64_t>(stage) * kStageDesc;
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint64_t da_hi = ds + h * 2;
+              const uint64_t db_hi = ds + kBDesc + h * 2;
+              const uint32_t acc_in = (ks == ks0 && h == 0) ? 0u : 1u;
+              if (SPLIT3) {
+                const uint64_t da_lo = ds + kAloDesc + h * 2;
+                const uint64_t db_lo = ds + kBloDesc + h * 2;
+                if (PAIR) {
+                  ptx::mma_tf32_pair(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small terms first
+                  ptx::mma_tf32_pair(d_tmem, da_hi, db_lo, kIdesc, 1u);
+                  ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, 1u);
+                } else {
+                  ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);
+                  ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
+                  ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
+                }
+              } else {
+                if (PAIR)
+                  ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, acc_in);
+                else
+                  ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
+              }
+            }
+            if (PAIR)
+              ptx::mma_commit_pair(&empty[stage]);
+            else
+              ptx::mma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
+        if (ptx::elect_one()) {
+          if (PAIR)
+            ptx::mma_commit_pair(&acc_full[buf]);
+          else
+            ptx::mma_commit(&acc_full[buf]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        for (int c = 0; c < nchunks; ++c, ++cit) {
-          const int buf = kAccBufs == 1 ? 0 : (cit & 1);
-          const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
-          ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
-          const int ks0 = c * p.chunk_ksteps;
-          const int ks_end = min(p.ksteps, ks0 + p.chunk_ksteps);
-          for (int ks = ks0; ks < ks_end; ++ks) {
-            ptx::mbar_wait(&full[stage], phase);
-            if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
-            ptx::tc_fence_after();
-            const uint32_t a_hi = ptx::smem_u32(a_buf(stage));
-            const uint32_t a_lo = ptx::smem_u32(alo_buf(stage));
-            const uint32_t b_hi = ptx::smem_u32(b_buf(stage));
-            const uint32_t b_lo = ptx::smem_u32(blo_buf(stage));
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              // A and B: K-major SW64 (64-B rows, 8-row groups 512 B apart);
-              // K half h (channels 8h..8h+7) starts 32 B into the row.
-              const uint64_t da_hi = ptx::smem_desc_sw64(a_hi + h * 32, 16, 512);
-              const uint64_t db_hi = ptx::smem_desc_sw64(b_hi + h * 32, 16, 512);
-              const uint32_t acc_in = (ks == ks0 && h == 0) ? 0u : 1u;
-              if (SPLIT3) {
-                const uint64_t da_lo = ptx::smem_desc_sw64(a_lo + h * 32, 16, 512);
-                const uint64_t db_lo = ptx::smem_desc_sw64(b_lo + h * 32, 16, 512);
-                ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small terms first
-                ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
-                ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
-              } else {
-                ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
-              }
-            }
-            ptx::mma_commit(&empty[stage]);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          ptx::mma_commit(&acc_full[buf]);
-        }
-      }
-    }
+    // second CTA of a pair: its loads complete on the leader's barrier and the
+    // leader issues the pair MMAs; nothing to do here.
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
+    constexpr int DW = Cfg::kDrainW;
+    const int lane = threadIdx.x & 31;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
     const int PQ16 = p.P * p.Q * 16;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
+    const int rq = row % p.Qb;
+    const int rp = (row / p.Qb) % p.Pb;
+    const int rn = row / (p.Qb * p.Pb);
     int cit = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const TileCoord tc = decode_tile(p, t);
-      const int rq = row % p.Qb;
-      const int rp = (row / p.Qb) % p.Pb;
-      const int rn = row / (p.Qb * p.Pb);
+    for (int g = cluster; g < p.groups; g += nclusters) {
+      const TileCoord tc = decode_group(p, g, rank, CS);
       const int q = tc.tq * p.Qb + rq;
       const int pp = tc.tp * p.Pb + rp;
       const int n = tc.tn * p.Nb + rn;
-      const bool valid = (rn < p.Nb) && (q < p.Q) && (pp < p.P) && (n < p.img_count);
+      const bool valid =
+          tc.live && (rn < p.Nb) && (q < p.Q) && (pp < p.P) && (n < p.img_count);
       float* orow = p.out + static_cast<long long>(n) * p.out_img_stride +
                     (static_cast<long long>(tc.tk * (BN / 16)) * p.P + pp) * (p.Q * 16) + q * 16;
       for (int c = 0; c < nchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
         const bool last = c == nchunks - 1;
-        ptx::mbar_wait(&acc_full[buf], acc_phase);
+        ptx::mbar_wait_sleep(&acc_full[buf], acc_phase);
         ptx::tc_fence_after();
         const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
 #pragma unroll 1
-        for (int j = 0; j < BN / 16; ++j) {
-          uint32_t v[16];
-          ptx::tmem_ld16(tacc + j * 16, v);
+        for (int j = 0; j < BN / DW; ++j) {
+          uint32_t v[DW];
+          if constexpr (DW == 32) ptx::tmem_ld32(tacc + j * 32, v);
+          else ptx::tmem_ld16(tacc + j * 16, v);
           if (SPLIT3 && c > 0) {
-            uint32_t sacc[16];
-            ptx::tmem_ld16(tsum + j * 16, sacc);
+            uint32_t sacc[DW];
+            if constexpr (DW == 32) ptx::tmem_ld32(tsum + j * 32, sacc);
+            else ptx::tmem_ld16(tsum + j * 16, sacc);
             ptx::tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
+            for (int i = 0; i < DW; ++i)
               v[i] = __float_as_uint(__uint_as_float(sacc[i]) + __uint_as_float(v[i]));
           } else {
             ptx::tmem_wait_ld();
           }
           if (!last) {
-            ptx::tmem_st16(tsum + j * 16, v);
+            if constexpr (DW == 32) ptx::tmem_st32(tsum + j * 32, v);
+            else ptx::tmem_st16(tsum + j * 16, v);
           } else if (valid) {
-            float4* dst = reinterpret_cast<float4*>(orow + static_cast<long long>(j) * PQ16);
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              float4 o = make_float4(__uint_as_float(v[4 * c4 + 0]), __uint_as_float(v[4 * c4 + 1]),
-                                     __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
-              if (p.accumulate) {
-                const float4 prev = dst[c4];
-                o.x += prev.x;
-                o.y += prev.y;
-                o.z += prev.z;
-                o.w += prev.w;
+            for (int blk = 0; blk < DW / 16; ++blk) {
+              float4* dst = reinterpret_cast<float4*>(
+                  orow + static_cast<long long>(j * (DW / 16) + blk) * PQ16);
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const int b = blk * 16 + 4 * c4;
+                float4 o = make_float4(__uint_as_float(v[b + 0]), __uint_as_float(v[b + 1]),
+                                       __uint_as_float(v[b + 2]), __uint_as_float(v[b + 3]));
+                if (p.accumulate) {
+                  const float4 prev = dst[c4];
+                  o.x += prev.x;
+                  o.y += prev.y;
+                  o.z += prev.z;
+                  o.w += prev.w;
+                }
+                dst[c4] = o;
               }
-              dst[c4] = o;
             }
           }
         }
         if (!last) ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&acc_empty[buf]);
+        __syncwarp();
+        if (ptx::elect_one()) {
+          if (PAIR && !leader)
+            ptx::mbar_arrive_remote(acc_empty_leader + 8u * buf);
+          else
+            ptx::mbar_arrive(&acc_empty[buf]);
+        }
+        __syncwarp();
       }
     }
   } else if (SPLIT3) {
@@ -314,7 +417,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
     const int tid = threadIdx.x - 192;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int g = cluster; g < p.groups; g += nclusters) {
       for (int ks = 0; ks < p.ksteps; ++ks) {
         ptx::mbar_wait(&full[stage], phase);
         const float4* a = reinterpret_cast<const float4*>(a_buf(stage));
@@ -342,9 +445,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3>::kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync_all();  // no CTA leaves while the pair still uses it
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    if (PAIR)
+      ptx::tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+    else
+      ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 #endif
 }

@@ -53,6 +53,7 @@ struct Recipe {
   int box_q = 0, box_p = 0, box_n = 0;                        // 0 = selector decides
   int stages = 0;                                             // informational
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
+  int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
   static Recipe parse(const std::string& text);  // throws ConfigError
   std::string id() const;                        // reference grammar + ";gpu=..."
@@ -65,6 +66,7 @@ struct Schedule {
   int qb, pb, nb;      // pixel box (ofw x ofh x img) of one 128-row M tile
   int oj_tile;         // reference tile=oj:T (0 = untiled)
   int chunk;           // k-steps per TMEM accumulation chunk (0 = whole reduction)
+  int cs;              // CTAs per cluster sharing (multicasting) the filter block
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;

@@ -93,6 +93,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.box_n = n;
         } else if (key == "st") {
           r.stages = static_cast<int>(parse_int(val, "gpu stages"));
+        } else if (key == "cl") {
+          r.cs = static_cast<int>(parse_int(val, "gpu cluster size"));
+          if (r.cs != 1 && r.cs != 2) throw ConfigError("gpu cl must be 1 (single CTA) or 2 (CTA pair)");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -119,6 +122,7 @@ std::string Recipe::id() const {
   if (has_gpu) {
     s += ";gpu=bn:" + std::to_string(bn) + ",box:" + std::to_string(box_q) + "x" +
          std::to_string(box_p) + "x" + std::to_string(box_n);
+    if (cs) s += ",cl:" + std::to_string(cs);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
   return s;
@@ -263,9 +267,19 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.box_q = s.qb;
   canon.box_p = s.pb;
   canon.box_n = s.nb;
+  // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
+  // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
+  // TF32 only (see conv_kernel.cuh)
+  s.cs = r.cs ? r.cs : (mode == PSCONV_MODE_TF32 ? 2 : 1);
+  if (s.cs == 2 && mode == PSCONV_MODE_3XTF32)
+    throw ConfigError("GPU tile: the CTA pair (cl:2) is TF32-only; use cl:1 for 3xTF32");
+  if (s.bn / s.cs < 8) throw ConfigError("GPU tile: bn / cluster size must be >= 8");
+  canon.cs = s.cs;
   // TMEM accumulation chunk (3xTF32 numerics, see conv_kernel.cuh); tf32: whole reduction
   const int ksteps = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
-  s.chunk = r.chunk ? r.chunk : (mode == PSCONV_MODE_3XTF32 ? 16 : ksteps);
+  // bn 256 has a single TMEM chunk buffer (drain not overlapped): longer chunks
+  // (error ~1.2e-7 per k-step of chunk, tools/chunk_sweep.py: ch 32 -> 3.5e-6)
+  s.chunk = r.chunk ? r.chunk : (mode == PSCONV_MODE_3XTF32 ? (s.bn == 256 ? 32 : 16) : ksteps);
   if (s.chunk > ksteps) s.chunk = ksteps;
   canon.chunk = (mode == PSCONV_MODE_3XTF32 || r.chunk) ? s.chunk : 0;
   s.recipe_id = canon.id();

@@ -34,11 +34,15 @@ namespace {
 struct Machine {
   double sms = 148;
   double hbm_gbs = 6538.9;
-  double l2_gbs = 9000.0;        // aggregate L2 -> SMEM operand bandwidth (TMA)
+  double l2_gbs = 20000.0;       // aggregate L2 slice read bandwidth (not binding in r01 data)
   double tf32_tflops = 811.4;    // dense tf32 tensor peak (derived)
   double l2_bytes = 100e6;       // usable share of the 126 MB L2
   double launch_us = 4.0;        // launch + prologue (TMEM alloc, barrier init)
   double tile_fill_us = 0.6;     // pipeline fill of the first k-steps of a tile
+  double clock_ghz = 1.6;        // SM clock under sustained tensor load (power-capped)
+  double port_bytes_per_cycle = 110.0;  // ~0.85 x 128 B/cycle L2->SMEM per SM
+  double kstep_sync_cyc = 30.0;  // mbarrier round trips per k-step
+  double drain_round_trip_cyc = 100.0;  // one 32-column TMEM drain step
 };
 const Machine kB200{};
 
@@ -97,12 +101,45 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.tiles = tiles;
   const double tile_flops = 2.0 * 128 * s.bn * 16.0 * ksteps * mult;
   b.flops_issued = tile_flops * tiles;
-  b.us_tensor = per_sm * tile_flops / (m.tf32_tflops * 1e12 / m.sms) * 1e6;
 
+  // Per-SM k-step pipeline (cycles), fitted to r01 measurements (cfg5 tf32 /
+  // 3xtf32, per-layer sweep): the MMA needs BN cycles per k-step (two
+  // M=128,N=BN,K=8 tf32 MMAs at BN/2 cycles each; x3 for 3xTF32); the operand
+  // delivery (A box + filter block, multicast or not, every CTA ingests all of
+  // it) streams through the ~128 B/cycle L2->SMEM port at ~85%; the two
+  // overlap imperfectly.
+  // Shared memory (~128 B/cycle/SM, measured r01: the single-CTA loop runs at
+  // exactly this rate) carries the tensor-core operand reads (each M=128,K=8
+  // MMA reads 4 KB of A and BN*32 B of B; a CTA pair reads only its half of B),
+  // the TMA writes and, in 3xTF32, the splitter's A -> A_lo pass.
+  const int cs = std::max(1, s.cs);
   const double a_box = double(s.qb) * s.pb * s.nb * 64.0;
-  const double tile_l2 = ksteps * (a_box + s.bn * 64.0 * (mult > 1 ? 2 : 1));
-  b.l2_bytes = tile_l2 * tiles;
-  b.us_l2 = per_sm * m.sms * tile_l2 / (m.l2_gbs * 1e9) * 1e6;
+  const double b_rows = double(s.bn) / cs;
+  const double deliver_b = a_box + b_rows * 64.0 * (mult > 1 ? 2 : 1);
+  const double mma_cyc = s.bn * mult;
+  const double del_cyc = deliver_b / m.port_bytes_per_cycle;
+  const double tc_reads = 2.0 * mult * (4096.0 + b_rows * 32.0);
+  // (the splitter's LSU traffic only partly competes with the async-proxy traffic)
+  const double smem_cyc = 0.94 * (tc_reads + deliver_b + (mult > 1 ? 4096.0 : 0.0)) / 128.0;
+  const double busy = std::max(mma_cyc, smem_cyc);
+  const double other = std::min(mma_cyc, smem_cyc);
+  double kstep_cyc = busy * std::pow(1.0 + std::pow(other / busy, 4.0), 0.25);
+  // + TMA descriptor traversal: one request per contiguous pixel run of the box
+  kstep_cyc = std::max(kstep_cyc, del_cyc) + m.kstep_sync_cyc + 0.5 * s.pb * s.nb;
+  const int chunk = s.chunk > 0 ? s.chunk : static_cast<int>(ksteps);
+  const double nchunks = std::ceil(double(ksteps) / chunk);
+  // 3xTF32 chunk drain: tcgen05.ld acc + sum, fadd, tcgen05.st, 32 columns per
+  // round trip; hidden behind the next chunk unless TMEM holds a single
+  // accumulator (bn 256)
+  const double drain_cyc = (s.bn / 32.0) * m.drain_round_trip_cyc;
+  const bool drain_exposed = mult > 1 && s.bn == 256;
+  const double tile_cyc = ksteps * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
+  // a CTA pair works on 2 pixel tiles at once: tiles per SM are still tiles/148
+  const double groups_per_cluster = std::ceil(double(tiles) / m.sms);
+  b.us_tensor = groups_per_cluster * tile_cyc / (m.clock_ghz * 1e3);
+  b.l2_bytes = ksteps * (a_box + s.bn * 64.0 * (mult > 1 ? 2 : 1) / std::max(1, s.cs)) * tiles;
+  b.us_l2 = b.l2_bytes / (m.l2_gbs * 1e9) * 1e6;
+  (void)per_sm;
 
   // HBM: compulsory bytes + input re-reads when the rasterisation sweeps all
   // pixels once per output-channel tile and the input does not stay in L2.
@@ -114,10 +151,13 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   double in_reads = 1.0;
   if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
-  b.us_hbm = b.hbm_bytes / (m.hbm_gbs * 1e9) * 1e6;
+  b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain
-  b.us_total = std::max({b.us_tensor, b.us_l2, b.us_hbm}) + m.launch_us + m.tile_fill_us + b.us_epi +
+  // SM-side and HBM-side times overlap imperfectly (soft max, p = 4)
+  const double hi = std::max({b.us_tensor, b.us_l2, b.us_hbm});
+  const double lo = std::max(std::min(b.us_tensor, b.us_hbm), 1e-9);
+  b.us_total = hi * std::pow(1.0 + std::pow(lo / hi, 4.0), 0.25) + m.launch_us + m.tile_fill_us + b.us_epi +
                (mult > 1 ? 2.0 + 3.0 * flt_b / 3 / (m.hbm_gbs * 1e9) * 1e6 : 0.0);
   return b;
 }

@@ -1,0 +1,107 @@
+"""Empirical top-k schedule selection (PolyScientist's last step: "run the
+top-k variants and pick the best").
+
+The closed-form model (csrc/select.cpp, conv_select_topk) ranks the recipe space; the top-k
+plus the structural alternatives the model is least sure about (CTA pair on/off, BN one step
+down) are timed on the device with the bench protocol (prepacked filter, L2 flushed, median of
+repeats). Results go to a plan cache keyed by the descriptor and mode, and to a report in the
+reference's tab-separated `rows` style (pipeline.hpp:232-278: one `ranked` row per variant).
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+
+from . import ConfigRejectedError, ConvPlan, ConvPreset, fill_filter, fill_input, select_topk
+
+CACHE_ENV = "PSCONV_PLAN_CACHE"
+
+
+def _variants(preset: ConvPreset, mode: str, k: int) -> list[str]:
+    ranked = [r for r, _ in select_topk(preset, mode, k)]
+    out = list(ranked)
+    base = ranked[0]
+    head, gpu = base.split(";gpu=")
+    kv = dict(item.split(":") for item in gpu.split(","))
+    alts = []
+    if mode == "tf32":
+        alts.append({**kv, "cl": "1" if kv.get("cl") == "2" else "2"})
+    bn = int(kv["bn"])
+    for nb in (bn * 2, bn // 2):
+        if 16 <= nb <= 256 and preset.nOfm % nb == 0:
+            alt = {**kv, "bn": str(nb)}
+            if mode == "3xtf32":
+                alt["ch"] = "32" if nb == 256 else "16"
+            alts.append(alt)
+    for a in alts:
+        rid = head + ";gpu=" + ",".join(f"{key}:{val}" for key, val in a.items())
+        if rid not in out:
+            out.append(rid)
+    return out
+
+
+def time_recipe(preset, mode, recipe, x, w, y, flush, stream, reps=5, warm=2) -> float:
+    import torch
+    plan = ConvPlan(preset, mode=mode, device=x.device.index or 0, recipe=recipe)
+    plan.prepack(w, stream)
+    f = lambda: plan.forward(x, None, y, stream=stream, prepacked=True)  # noqa: E731
+    for _ in range(warm):
+        f()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    plan.close()
+    return statistics.median(ts)
+
+
+def autotune(preset: ConvPreset, mode: str = "3xtf32", k: int = 4, device: int = 0,
+             c_logical: int = 0, seeds=(1, 2), cache_path: str | None = None,
+             report_path: str | None = None) -> tuple[str, list[tuple[str, float, float]]]:
+    """Returns (best recipe id, [(recipe, model_us, measured_us), ...] best first)."""
+    import torch
+    from . import model_us
+    cache_path = cache_path or os.environ.get(CACHE_ENV)
+    key = f"{preset}|{mode}"
+    if cache_path and os.path.exists(cache_path):
+        with open(cache_path) as fh:
+            cache = json.load(fh)
+        if key in cache:
+            return cache[key]["recipe"], [tuple(r) for r in cache[key]["ranked"]]
+    dev = torch.device("cuda", device)
+    stream = torch.cuda.current_stream(dev)
+    x = torch.empty(preset.input_elems(), dtype=torch.float32, device=dev)
+    w = torch.empty(preset.filter_elems(), dtype=torch.float32, device=dev)
+    y = torch.empty(preset.output_elems(), dtype=torch.float32, device=dev)
+    fill_input(preset, seeds[0], x, c_logical=c_logical)
+    fill_filter(preset, seeds[1], w, c_logical=c_logical)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    rows = []
+    for rid in _variants(preset, mode, k):
+        try:
+            ms = time_recipe(preset, mode, rid, x, w, y, flush, stream)
+        except ConfigRejectedError:
+            continue
+        rows.append((rid, model_us(preset, rid, mode), ms * 1e3))
+    rows.sort(key=lambda r: (r[2], r[0]))
+    best = rows[0][0]
+    if cache_path:
+        cache = {}
+        if os.path.exists(cache_path):
+            with open(cache_path) as fh:
+                cache = json.load(fh)
+        cache[key] = {"recipe": best, "ranked": rows}
+        with open(cache_path, "w") as fh:
+            json.dump(cache, fh, indent=1, sort_keys=True)
+    if report_path:
+        with open(report_path, "a") as fh:
+            for i, (rid, mu, us) in enumerate(rows):
+                fh.write(f"ranked\t{key}\t{i + 1}\t{rid}\tmodel_us={mu:.1f}\tmeasured_us={us:.1f}\n")
+    return best, rows

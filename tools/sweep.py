@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--only", default=None, help="comma list of workload names")
     ap.add_argument("--modes", default="3xtf32,tf32")
     ap.add_argument("--recipe", default=None)
+    ap.add_argument("--tune", type=int, default=0, help="time the model's top-k per layer")
+    ap.add_argument("--rows", default=None, help="append tuner `ranked` rows here")
     args = ap.parse_args()
     hbm, bf16, src = bench.peaks()
     dev = torch.device("cuda:0")
@@ -62,7 +64,12 @@ def main():
         flops = p.flops(c_log)
         bytes_c = bench.compulsory_bytes(p, c_log)
         for mode in args.modes.split(","):
-            plan = ps.ConvPlan(p, mode=mode, recipe=args.recipe)
+            recipe = args.recipe
+            if args.tune and recipe is None:
+                from paper_2002_02145_b200.tune import autotune
+                recipe, _ = autotune(p, mode, k=args.tune, c_logical=c_log, seeds=(sx, sw),
+                                     report_path=args.rows)
+            plan = ps.ConvPlan(p, mode=mode, recipe=recipe)
             step = time_it(lambda: plan.forward(x, w, y, stream=stream), flush, args.steps, args.warmup, stream)
             plan.prepack(w, stream)
             kern = time_it(lambda: plan.forward(x, None, y, stream=stream, prepacked=True), flush,
