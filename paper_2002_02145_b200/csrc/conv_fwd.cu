@@ -212,7 +212,7 @@ int grid_for(int64_t n) {
 // ---------------------------------------------------------------- launch
 template <int BN, bool SPLIT3, int CS>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
-                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+                 const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2)) {
     throw RuntimeError("unsupported (bn, cluster, mode) combination");
   } else {
@@ -239,29 +239,29 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
   }
 }
 
 template <bool SPLIT3, int CS>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
-                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+                 const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_conv<16, SPLIT3, CS>(P, prm, a, b, blo, st);
-    case 32: return launch_conv<32, SPLIT3, CS>(P, prm, a, b, blo, st);
-    case 64: return launch_conv<64, SPLIT3, CS>(P, prm, a, b, blo, st);
-    case 128: return launch_conv<128, SPLIT3, CS>(P, prm, a, b, blo, st);
-    case 256: return launch_conv<256, SPLIT3, CS>(P, prm, a, b, blo, st);
+    case 16: return launch_conv<16, SPLIT3, CS>(P, prm, a, b, blo, o, st);
+    case 32: return launch_conv<32, SPLIT3, CS>(P, prm, a, b, blo, o, st);
+    case 64: return launch_conv<64, SPLIT3, CS>(P, prm, a, b, blo, o, st);
+    case 128: return launch_conv<128, SPLIT3, CS>(P, prm, a, b, blo, o, st);
+    case 256: return launch_conv<256, SPLIT3, CS>(P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported bn");
   }
 }
 
 template <bool SPLIT3>
 void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
-                 const CUtensorMap& b, const CUtensorMap& blo, cudaStream_t st) {
+                 const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (cs) {
-    case 1: return dispatch_bn<SPLIT3, 1>(bn, P, prm, a, b, blo, st);
-    case 2: return dispatch_bn<SPLIT3, 2>(bn, P, prm, a, b, blo, st);
+    case 1: return dispatch_bn<SPLIT3, 1>(bn, P, prm, a, b, blo, o, st);
+    case 2: return dispatch_bn<SPLIT3, 2>(bn, P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported cluster size");
   }
 }
@@ -394,7 +394,19 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     const bool split3 = P->mode == PSCONV_MODE_3XTF32;
 
     // A: input viewed as [img_count][Cb][H][W][16], starting at img_begin
-    CUtensorMap ta, tb, tblo;
+    CUtensorMap ta, tb, tblo, tout;
+    // output viewed as [img_count][Kb][P][Q][16] starting at img_begin; the box is
+    // the pixel tile (no stride factor); stores outside the layer are clipped
+    {
+      const float* base = out + img_begin * int64_t(Kb) * Pp * Q * 16;
+      const cuuint64_t dims[5] = {16, cuuint64_t(Q), cuuint64_t(Pp), cuuint64_t(Kb),
+                                  cuuint64_t(img_count)};
+      const cuuint64_t strides[4] = {64, cuuint64_t(Q) * 64, cuuint64_t(Pp) * Q * 64,
+                                     cuuint64_t(Kb) * Pp * Q * 64};
+      const cuuint32_t box[5] = {16, cuuint32_t(s.qb), cuuint32_t(s.pb), 1, cuuint32_t(s.nb)};
+      const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+      encode(&tout, base, 5, dims, strides, box, estr);
+    }
     {
       const float* base = in + img_begin * int64_t(Cb) * H * W * 16;
       const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(Cb),
@@ -462,9 +474,9 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
     prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
     if (split3)
-      dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, st);
+      dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
     else
-      dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, st);
+      dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
   });
 }
 

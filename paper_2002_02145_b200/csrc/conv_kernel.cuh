@@ -70,7 +70,9 @@ struct KernelCfg {
   static constexpr int kBBytes = kBRows * 64; // kBRows output channels x 16 input channels
   // stage: [A | A_lo (3x) | B_hi | B_lo (3x)]
   static constexpr int kStageBytes = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);
-  static constexpr int kBudget = 200 * 1024;
+  static constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
+  // 227 KB per CTA = stages + 2 output staging blocks + barriers + alignment slack
+  static constexpr int kBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   // TMEM (per CTA: 128 lanes x BN columns per accumulator)
@@ -84,11 +86,13 @@ struct KernelCfg {
                                                         : 512;
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kBarBytes = 1024;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // +align slack
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + 2 * kOutStageBytes + kBarBytes + 1024;  // +align slack
   static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
   static_assert(kStages >= 2, "stages");
+  static_assert(kStages * kStageBytes + 2 * kOutStageBytes + 1024 + 1024 <= 227 * 1024, "smem");
   static_assert(kColsNeeded <= 512, "TMEM");
   // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
   // a cluster-scope release per k-step (MEMBAR.GPU, measured ~3x slower).
@@ -128,7 +132,8 @@ template <int BN, bool SPLIT3, bool PAIR>
 __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
-                   const __grid_constant__ CUtensorMap tmap_flt_lo) {
+                   const __grid_constant__ CUtensorMap tmap_flt_lo,
+                   const __grid_constant__ CUtensorMap tmap_out) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
   constexpr int CS = Cfg::kCS;
@@ -148,7 +153,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   };
   auto blo_buf = [&](int s) { return b_buf(s) + Cfg::kBBytes; };
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint8_t* out_stage = smem + kStages * Cfg::kStageBytes;  // 2 x 8 KB (1024-B aligned)
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes + 2 * Cfg::kOutStageBytes);
   uint64_t* full = bars;                     // own TMA landed (1 arrive + tx)
   uint64_t* split_full = bars + kStages;     // own splitter done (count 128)
   uint64_t* empty = bars + 2 * kStages;      // MMA consumed the stage (commit, pair: both CTAs)
@@ -331,25 +338,25 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
     constexpr int DW = Cfg::kDrainW;
+    // Output path: each 16-channel block of the 128-pixel tile is staged in
+    // shared memory (SWIZZLE_64B image of the TMA box, conflict-free 16-B
+    // writes) and written by one TMA tensor store (full lines; pixels outside
+    // the layer are clipped by TMA; `+=` semantics via TMA reduce-add).
     const int lane = threadIdx.x & 31;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const int PQ16 = p.P * p.Q * 16;
+    const bool store_thread = threadIdx.x == 64;  // first epilogue thread issues TMA stores
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
-    const int rq = row % p.Qb;
-    const int rp = (row / p.Qb) % p.Pb;
-    const int rn = row / (p.Qb * p.Pb);
+    const uint32_t row_off = static_cast<uint32_t>(row) * 64u;
+    const uint32_t row_swz = (static_cast<uint32_t>(row) >> 1) & 3u;  // SW64: chunk ^= bits[7:8]
+    int ostage = 0;                                                  // staging buffer toggle
+    if (store_thread) ptx::prefetch_tmap(&tmap_out);
     int cit = 0;
     for (int g = cluster; g < p.groups; g += nclusters) {
       const TileCoord tc = decode_group(p, g, rank, CS);
-      const int q = tc.tq * p.Qb + rq;
-      const int pp = tc.tp * p.Pb + rp;
-      const int n = tc.tn * p.Nb + rn;
-      const bool valid =
-          tc.live && (rn < p.Nb) && (q < p.Q) && (pp < p.P) && (n < p.img_count);
-      float* orow = p.out + static_cast<long long>(n) * p.out_img_stride +
-                    (static_cast<long long>(tc.tk * (BN / 16)) * p.P + pp) * (p.Q * 16) + q * 16;
+      const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
+      const int kb0 = tc.tk * (BN / 16);
       for (int c = 0; c < nchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -377,25 +384,30 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           if (!last) {
             if constexpr (DW == 32) ptx::tmem_st32(tsum + j * 32, v);
             else ptx::tmem_st16(tsum + j * 16, v);
-          } else if (valid) {
+          } else if (tc.live) {
 #pragma unroll
             for (int blk = 0; blk < DW / 16; ++blk) {
-              float4* dst = reinterpret_cast<float4*>(
-                  orow + static_cast<long long>(j * (DW / 16) + blk) * PQ16);
+              uint8_t* st = out_stage + ostage * Cfg::kOutStageBytes;
+              // staging buffer free? (the store issued two blocks ago has read it)
+              if (store_thread) ptx::bulk_wait_read<1>();
+              ptx::named_bar(1, 128);
 #pragma unroll
               for (int c4 = 0; c4 < 4; ++c4) {
                 const int b = blk * 16 + 4 * c4;
-                float4 o = make_float4(__uint_as_float(v[b + 0]), __uint_as_float(v[b + 1]),
-                                       __uint_as_float(v[b + 2]), __uint_as_float(v[b + 3]));
-                if (p.accumulate) {
-                  const float4 prev = dst[c4];
-                  o.x += prev.x;
-                  o.y += prev.y;
-                  o.z += prev.z;
-                  o.w += prev.w;
-                }
-                dst[c4] = o;
+                const uint32_t off = row_off + ((static_cast<uint32_t>(c4) ^ row_swz) << 4);
+                *reinterpret_cast<uint4*>(st + off) = make_uint4(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
               }
+              ptx::fence_proxy_async_smem();
+              ptx::named_bar(1, 128);
+              if (store_thread) {
+                const int kb = kb0 + j * (DW / 16) + blk;
+                if (p.accumulate)
+                  ptx::tma_reduce_add_5d(&tmap_out, st, 0, q0, p0, kb, n0);
+                else
+                  ptx::tma_store_5d(&tmap_out, st, 0, q0, p0, kb, n0);
+                ptx::bulk_commit();
+              }
+              ostage ^= 1;
             }
           }
         }
@@ -411,6 +423,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         __syncwarp();
       }
     }
+    if (store_thread) ptx::bulk_wait_all();  // stores complete before smem is released
   } else if (SPLIT3) {
     // ------------------------------------------------------------ splitter
     // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
