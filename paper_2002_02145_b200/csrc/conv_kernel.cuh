@@ -74,7 +74,8 @@ struct KernelCfg {
   // 227 KB per CTA = stages + 2 output staging blocks + barriers + alignment slack
   static constexpr int kBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  // small stages (small BN): keep up to 16 in flight for HBM-streaming layers
+  static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
   // TMEM (per CTA: 128 lanes x BN columns per accumulator)
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
   static constexpr int kSumCol = kAccBufs * BN;

@@ -14,6 +14,7 @@ import os
 import statistics
 
 from . import ConfigRejectedError, ConvPlan, ConvPreset, fill_filter, fill_input, select_topk
+from .timing import L2Flush
 
 CACHE_ENV = "PSCONV_PLAN_CACHE"
 
@@ -50,7 +51,7 @@ def time_recipe(preset, mode, recipe, x, w, y, flush, stream, reps=5, warm=2) ->
         f()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -82,7 +83,7 @@ def autotune(preset: ConvPreset, mode: str = "3xtf32", k: int = 4, device: int =
     y = torch.empty(preset.output_elems(), dtype=torch.float32, device=dev)
     fill_input(preset, seeds[0], x, c_logical=c_logical)
     fill_filter(preset, seeds[1], w, c_logical=c_logical)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    flush = L2Flush(dev)
     rows = []
     for rid in _variants(preset, mode, k):
         try:

@@ -12,6 +12,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2002_02145_b200 as ps  # noqa: E402
+from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
 from paper_2002_02145_b200.workloads import ALL, seeds  # noqa: E402
 
 
@@ -30,7 +31,7 @@ def main():
     sx, sw = seeds(cid)
     ps.fill_input(p, sx, x, c_logical=c_log)
     ps.fill_filter(p, sw, w, c_logical=c_log)
-    flush = torch.empty(64 << 20, device=dev)
+    flush = L2Flush(dev)
     hbm, bf16, _ = bench.peaks()
     peak = bf16 / 2 / (3 if mode == "3xtf32" else 1)
     flops = p.flops(c_log)
@@ -43,7 +44,7 @@ def main():
             f()
         ts = []
         for _ in range(10):
-            flush.zero_()
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             f()

@@ -17,6 +17,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2002_02145_b200 as ps  # noqa: E402
+from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
 from paper_2002_02145_b200.workloads import ALL, seeds  # noqa: E402
 
 
@@ -26,7 +27,7 @@ def time_it(fn, flush, steps, warm, stream):
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for e0, e1 in ev:
-        flush.zero_()
+        flush()
         e0.record(stream)
         fn()
         e1.record(stream)
@@ -49,7 +50,7 @@ def main():
     hbm, bf16, src = bench.peaks()
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream()
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush = L2Flush(dev)  # write + read 256 MiB (> 126 MB L2)
     names = args.only.split(",") if args.only else list(ALL)
     recs = []
     for name in names:
