@@ -239,7 +239,10 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
+    // accumulation chunks must hold whole pipeline stages (KPS k-steps each)
+    ConvParams q = prm;
+    q.chunk_ksteps = ((prm.chunk_ksteps + Cfg::KPS - 1) / Cfg::KPS) * Cfg::KPS;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, q, a, b, blo, o));
   }
 }
 
@@ -471,6 +474,12 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.chunk_ksteps = s.chunk > 0 ? s.chunk : prm.ksteps;
     for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
     prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
+    // profiling switch (never set in production; results are wrong when non-zero)
+    static const int debug_env = [] {
+      const char* e = std::getenv("PSCONV_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    prm.debug = debug_env;
     prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
     prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
     if (split3)

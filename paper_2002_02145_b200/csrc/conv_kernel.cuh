@@ -58,6 +58,7 @@ struct ConvParams {
   int chunk_ksteps;               // k-steps per TMEM accumulation chunk
   int kord[3];                    // k-step order outer->inner over {0 ifm_tile, 1 kj, 2 ki}
   int accumulate;                 // out += conv
+  int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
 };
@@ -69,13 +70,23 @@ struct KernelCfg {
   static constexpr int kABytes = 128 * 64;    // 128 pixels x 16 fp32 channels
   static constexpr int kBBytes = kBRows * 64; // kBRows output channels x 16 input channels
   // stage: [A | A_lo (3x) | B_hi | B_lo (3x)]
-  static constexpr int kStageBytes = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);
+  // Each pipeline stage carries KPS k-steps: the per-stage synchronisation
+  // (mbarrier waits ~90 cycles even when complete, expect_tx, TMA issue, MMA
+  // commit) measured as a ~330-cycle floor per stage on the single producer /
+  // MMA threads, independent of the tile's MMA size.
+  // stage: [A x KPS | A_lo x KPS (3x) | B_hi x KPS | B_lo x KPS (3x)]
   static constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
   // 227 KB per CTA = stages + 2 output staging blocks + barriers + alignment slack
   static constexpr int kBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
+  static constexpr int kStage1 = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);  // one k-step
+  static constexpr int KPS = (kBudget / (2 * kStage1) >= 3) ? 2 : 1;     // keep >= 3 stages
+  static constexpr int kALoOff = KPS * kABytes;
+  static constexpr int kBOff = KPS * kABytes * (SPLIT3 ? 2 : 1);
+  static constexpr int kBLoOff = kBOff + KPS * kBBytes;
+  static constexpr int kStageBytes = KPS * kStage1;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
-  // small stages (small BN): keep up to 16 in flight for HBM-streaming layers
-  static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
+  // small stages (small BN): keep up to 12 in flight for HBM-streaming layers
+  static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
   // TMEM (per CTA: 128 lanes x BN columns per accumulator)
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
   static constexpr int kSumCol = kAccBufs * BN;
@@ -147,12 +158,17 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   // same in both CTAs of a pair, which the pair MMA relies on.
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  auto a_buf = [&](int s) { return smem + s * Cfg::kStageBytes; };
-  auto alo_buf = [&](int s) { return smem + s * Cfg::kStageBytes + Cfg::kABytes; };
-  auto b_buf = [&](int s) {
-    return smem + s * Cfg::kStageBytes + Cfg::kABytes * (SPLIT3 ? 2 : 1);
+  constexpr int KPS = Cfg::KPS;
+  auto a_buf = [&](int s, int j) { return smem + s * Cfg::kStageBytes + j * Cfg::kABytes; };
+  auto alo_buf = [&](int s, int j) {
+    return smem + s * Cfg::kStageBytes + Cfg::kALoOff + j * Cfg::kABytes;
   };
-  auto blo_buf = [&](int s) { return b_buf(s) + Cfg::kBBytes; };
+  auto b_buf = [&](int s, int j) {
+    return smem + s * Cfg::kStageBytes + Cfg::kBOff + j * Cfg::kBBytes;
+  };
+  auto blo_buf = [&](int s, int j) {
+    return smem + s * Cfg::kStageBytes + Cfg::kBLoOff + j * Cfg::kBBytes;
+  };
 
   uint8_t* out_stage = smem + kStages * Cfg::kStageBytes;  // 2 x 8 KB (1024-B aligned)
   uint64_t* bars =
@@ -211,7 +227,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
     // PAIR: both CTAs' loads complete on the LEADER's full barrier (the leader
     // expects both shares); the second CTA never arrives on its own.
-    const uint32_t tx = (a_bytes + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;
+    const bool skip_a = (p.debug & 1) != 0;
+    const uint32_t tx1 =
+        ((skip_a ? 0u : a_bytes) + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;  // per k-step
     const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
     const int d0 = p.kord[0], d1 = p.kord[1], d2 = p.kord[2];
     const int e1 = d1 == 0 ? p.Cb : (d1 == 1 ? p.R : p.S);
@@ -225,33 +243,42 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const int n0 = tc.tn * p.Nb;
       const int k0 = tc.tk * BN + rank * Cfg::kBRows;
       int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
-      for (int ks = 0; ks < p.ksteps; ++ks) {
-        const int cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
-        const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
-        const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
-        const int crs = (cb * p.R + r) * p.S + s;
+      for (int ks = 0; ks < p.ksteps; ks += KPS) {
+        const int nk = min(KPS, p.ksteps - ks);
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        if (ptx::elect_one()) {
-          if (!PAIR) {
-            ptx::mbar_expect_tx(&full[stage], tx);
-            ptx::tma_load_5d(a_buf(stage), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
-            ptx::tma_load_3d(b_buf(stage), &tmap_flt, &full[stage], 0, k0, crs);
-            if (SPLIT3) ptx::tma_load_3d(blo_buf(stage), &tmap_flt_lo, &full[stage], 0, k0, crs);
-          } else {
-            if (leader) ptx::mbar_expect_tx(&full[stage], tx);
-            const uint32_t fb = full_leader + 8u * stage;
-            ptx::tma_load_5d_cb(a_buf(stage), &tmap_in, fb, 0, wq + s, hp + r, cb, n0);
-            ptx::tma_load_3d_cb(b_buf(stage), &tmap_flt, fb, 0, k0, crs);
+        const bool issuer = ptx::elect_one();
+        if (issuer && (!PAIR || leader)) ptx::mbar_expect_tx(&full[stage], tx1 * nk);
+#pragma unroll
+        for (int j = 0; j < KPS; ++j) {
+          if (j < nk) {
+            const int cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
+            const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
+            const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
+            const int crs = (cb * p.R + r) * p.S + s;
+            if (issuer) {
+              if (!PAIR) {
+                if (!skip_a)
+                  ptx::tma_load_5d(a_buf(stage, j), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
+                ptx::tma_load_3d(b_buf(stage, j), &tmap_flt, &full[stage], 0, k0, crs);
+                if (SPLIT3)
+                  ptx::tma_load_3d(blo_buf(stage, j), &tmap_flt_lo, &full[stage], 0, k0, crs);
+              } else {
+                const uint32_t fb = full_leader + 8u * stage;
+                if (!skip_a)
+                  ptx::tma_load_5d_cb(a_buf(stage, j), &tmap_in, fb, 0, wq + s, hp + r, cb, n0);
+                ptx::tma_load_3d_cb(b_buf(stage, j), &tmap_flt, fb, 0, k0, crs);
+              }
+            }
+            if (++v2 == e2) {
+              v2 = 0;
+              if (++v1 == e1) {
+                v1 = 0;
+                ++v0;
+              }
+            }
           }
         }
         __syncwarp();
-        if (++v2 == e2) {
-          v2 = 0;
-          if (++v1 == e1) {
-            v1 = 0;
-            ++v0;
-          }
-        }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
@@ -265,9 +292,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // apart); K half h (channels 8h..8h+7) starts 32 B (2 x 16 B) into the row.
     const uint64_t desc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
     constexpr uint32_t kStageDesc = Cfg::kStageBytes >> 4;
-    constexpr uint32_t kAloDesc = Cfg::kABytes >> 4;
-    constexpr uint32_t kBDesc = (Cfg::kABytes * (SPLIT3 ? 2 : 1)) >> 4;
-    constexpr uint32_t kBloDesc = kBDesc + (Cfg::kBBytes >> 4);
+    constexpr uint32_t kAStepDesc = Cfg::kABytes >> 4;  // next k-step's A tile in the stage
+    constexpr uint32_t kBStepDesc = Cfg::kBBytes >> 4;
+    constexpr uint32_t kAloDesc = Cfg::kALoOff >> 4;
+    constexpr uint32_t kBDesc = Cfg::kBOff >> 4;
+    constexpr uint32_t kBloDesc = Cfg::kBLoOff >> 4;
     int stage = 0;
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
@@ -283,34 +312,40 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
         const int ks0 = c * p.chunk_ksteps;
         const int ks_end = min(p.ksteps, ks0 + p.chunk_ksteps);
-        for (int ks = ks0; ks < ks_end; ++ks) {
+        for (int ks = ks0; ks < ks_end; ks += KPS) {
+          const int nk = min(KPS, ks_end - ks);
           ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ds = desc0 + static_cast<uint64_t>(stage) * kStageDesc;
           if (ptx::elect_one()) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint64_t da_hi = ds + h * 2;
-              const uint64_t db_hi = ds + kBDesc + h * 2;
-              const uint32_t acc_in = (ks == ks0 && h == 0) ? 0u : 1u;
-              if (SPLIT3) {
-                const uint64_t da_lo = ds + kAloDesc + h * 2;
-                const uint64_t db_lo = ds + kBloDesc + h * 2;
-                if (PAIR) {
-                  ptx::mma_tf32_pair(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small terms first
-                  ptx::mma_tf32_pair(d_tmem, da_hi, db_lo, kIdesc, 1u);
-                  ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, 1u);
-                } else {
-                  ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);
-                  ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
-                  ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
+            for (int j = 0; j < KPS; ++j) {
+              if (j < nk && !(p.debug & 2)) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const uint64_t da_hi = ds + j * kAStepDesc + h * 2;
+                  const uint64_t db_hi = ds + kBDesc + j * kBStepDesc + h * 2;
+                  const uint32_t acc_in = (ks == ks0 && j == 0 && h == 0) ? 0u : 1u;
+                  if (SPLIT3) {
+                    const uint64_t da_lo = ds + kAloDesc + j * kAStepDesc + h * 2;
+                    const uint64_t db_lo = ds + kBloDesc + j * kBStepDesc + h * 2;
+                    if (PAIR) {
+                      ptx::mma_tf32_pair(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small first
+                      ptx::mma_tf32_pair(d_tmem, da_hi, db_lo, kIdesc, 1u);
+                      ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, 1u);
+                    } else {
+                      ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);
+                      ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
+                      ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
+                    }
+                  } else {
+                    if (PAIR)
+                      ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, acc_in);
+                    else
+                      ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
+                  }
                 }
-              } else {
-                if (PAIR)
-                  ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, acc_in);
-                else
-                  ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
               }
             }
             if (PAIR)
@@ -362,7 +397,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
         const bool last = c == nchunks - 1;
+#ifdef PSCONV_EPI_SLEEP
         ptx::mbar_wait_sleep(&acc_full[buf], acc_phase);
+#else
+        ptx::mbar_wait(&acc_full[buf], acc_phase);
+#endif
         ptx::tc_fence_after();
         const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
@@ -400,7 +439,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               }
               ptx::fence_proxy_async_smem();
               ptx::named_bar(1, 128);
-              if (store_thread) {
+              if (store_thread && !(p.debug & 4)) {
                 const int kb = kb0 + j * (DW / 16) + blk;
                 if (p.accumulate)
                   ptx::tma_reduce_add_5d(&tmap_out, st, 0, q0, p0, kb, n0);
@@ -432,20 +471,26 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int g = cluster; g < p.groups; g += nclusters) {
-      for (int ks = 0; ks < p.ksteps; ++ks) {
+      for (int ks = 0; ks < p.ksteps; ks += KPS) {
+        const int nk = min(KPS, p.ksteps - ks);
         ptx::mbar_wait(&full[stage], phase);
-        const float4* a = reinterpret_cast<const float4*>(a_buf(stage));
-        float4* alo = reinterpret_cast<float4*>(alo_buf(stage));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = tid + i * 128;
-          const float4 x = a[idx];
-          float4 lo;
-          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          alo[idx] = lo;
+        for (int j = 0; j < KPS; ++j) {
+          if (j < nk) {
+            const float4* a = reinterpret_cast<const float4*>(a_buf(stage, j));
+            float4* alo = reinterpret_cast<float4*>(alo_buf(stage, j));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int idx = tid + i * 128;
+              const float4 x = a[idx];
+              float4 lo;
+              lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+              lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+              lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+              lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+              alo[idx] = lo;
+            }
+          }
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);
