@@ -16,6 +16,9 @@
 #include "internal.hpp"
 #include "seeded.hpp"
 
+static_assert(psconv::kSmemStageBudget == psconv::kStageBudget, "stage budget");
+static_assert(psconv::kSmemMaxStages == psconv::kMaxStages, "max stages");
+
 struct conv_plan {
   conv_desc d;
   int mode;
@@ -239,10 +242,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // accumulation chunks must hold whole pipeline stages (KPS k-steps each)
-    ConvParams q = prm;
-    q.chunk_ksteps = ((prm.chunk_ksteps + Cfg::KPS - 1) / Cfg::KPS) * Cfg::KPS;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, q, a, b, blo, o));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
   }
 }
 
@@ -410,14 +410,18 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
       encode(&tout, base, 5, dims, strides, box, estr);
     }
+    // A: input NCHW16c [img_count][Cb][H][W][16] viewed with its dims ordered
+    // [16c][W][H][img][Cb] (TMA dims need not follow memory order): the box
+    // [16][Qb*sw][Pb*sh][Nb][kps] lands as kps contiguous 128-row tiles, one per
+    // input-channel block of the stage.
     {
       const float* base = in + img_begin * int64_t(Cb) * H * W * 16;
-      const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(Cb),
-                                  cuuint64_t(img_count)};
-      const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(H) * W * 64,
-                                     cuuint64_t(Cb) * H * W * 64};
+      const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(img_count),
+                                  cuuint64_t(Cb)};
+      const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
+                                     cuuint64_t(H) * W * 64};
       const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
-                                 1, cuuint32_t(s.nb)};
+                                 cuuint32_t(s.nb), cuuint32_t(s.kps)};
       const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
       encode(&ta, base, 5, dims, strides, box, estr);
     }
@@ -430,13 +434,14 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       launch_prepack(P, flt, st);
       P->prepacked = false;  // buffer now holds this call's filter
     }
+    // B viewed as [16c][K][R*S][Cb] (crs = cb*R*S + r*S + s): box {16, rows, 1, kps}
     {
-      const cuuint64_t dims[3] = {16, cuuint64_t(K), cuuint64_t(CRS)};
-      const cuuint64_t strides[2] = {64, cuuint64_t(K) * 64};
-      const cuuint32_t box[3] = {16, cuuint32_t(s.bn / s.cs), 1};  // one cluster CTA's piece
-      const cuuint32_t estr[3] = {1, 1, 1};
-      encode(&tb, b_hi, 3, dims, strides, box, estr);
-      encode(&tblo, b_lo, 3, dims, strides, box, estr);
+      const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
+      const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
+      const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps)};
+      const cuuint32_t estr[4] = {1, 1, 1, 1};
+      encode(&tb, b_hi, 4, dims, strides, box, estr);
+      encode(&tblo, b_lo, 4, dims, strides, box, estr);
     }
     ConvParams prm{};
     prm.img_count = int(img_count);
@@ -471,7 +476,23 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.m_order = pos[0] < pos[2] ? 0 : 1;
     prm.k_outer = pos[1] == 0 ? 1 : 0;
     prm.ksteps = Cb * R * S;
-    prm.chunk_ksteps = s.chunk > 0 ? s.chunk : prm.ksteps;
+    prm.kps = s.kps;
+    prm.cbg = Cb / s.kps;
+    prm.stages = s.stages;
+    {
+      const int mult = split3 ? 2 : 1;
+      const int brows = s.bn / s.cs;
+      prm.stage_bytes = stage_bytes(s, P->mode);
+      prm.a_pitch = s.qb * s.pb * s.nb * 64;
+      prm.a_lo_off = s.kps * 8192;
+      prm.b_off = s.kps * 8192 * mult;
+      prm.b_lo_off = prm.b_off + s.kps * brows * 64;
+      if (prm.stages < 2 || prm.stages > kMaxStages || prm.stages * prm.stage_bytes > kStageBudget ||
+          Cb % s.kps != 0)
+        throw RuntimeError("internal: bad pipeline stage plan");
+    }
+    const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
+    prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
     for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
     prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
     // profiling switch (never set in production; results are wrong when non-zero)

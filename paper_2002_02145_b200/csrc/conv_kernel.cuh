@@ -7,7 +7,7 @@
 //                      &flt[ofm_tile][ifm_tile][kj][ki][0][0],
 //                      &in[img][ifm_tile][oj*sh+kj][ki][0])
 // Here the same contraction is one implicit GEMM per launch:
-//   M = pixels (img, oj, oi)   -> 128-row tiles = TMA box [16c][Qb][Pb][1][Nb]
+//   M = pixels (img, oj, oi)   -> 128-row tiles = TMA box [16c][Qb][Pb][Nb][kps blocks]
 //   N = output channels        -> BN = 16 * (ofm_tile block count)
 //   K = (ifm_tile, kj, ki, ifm)-> one k-step = one (ifm_tile,kj,ki) triple =
 //                                 16 channels = two tcgen05 K=8 tf32 MMAs
@@ -36,7 +36,7 @@
 // A_lo = x - trunc(x) is materialised. The tensor-core accumulation into TMEM
 // loses ~2^-25 of the running sum per MMA (error grows linearly with the MMA
 // chain), so in 3xTF32 mode the reduction is split into chunks of
-// `chunk_ksteps` k-steps: each chunk restarts its TMEM accumulator and the
+// `chunk_stages` pipeline stages: each chunk restarts its TMEM accumulator and the
 // epilogue adds the chunks in fp32 (round-to-nearest) into a TMEM running sum.
 #pragma once
 #include <cstdint>
@@ -55,13 +55,31 @@ struct ConvParams {
   int m_order;                    // 0: img outer of oj, 1: oj outer of img (oi innermost)
   int k_outer;                    // 1: ofm_tile outer of the pixel loops (recipe order)
   int ksteps;                     // Cb*R*S
-  int chunk_ksteps;               // k-steps per TMEM accumulation chunk
-  int kord[3];                    // k-step order outer->inner over {0 ifm_tile, 1 kj, 2 ki}
+  int kps;                        // k-steps per pipeline stage (input-channel blocks per TMA box)
+  int cbg;                        // Cb / kps
+  int stages;                     // pipeline stages in the ring (<= kMaxStages)
+  int stage_bytes;                // [A x kps | A_lo x kps (3x) | B x kps | B_lo x kps (3x)]
+  int a_pitch;                    // bytes between the kps A tiles of a stage (box rows x 64)
+  int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
+  int chunk_stages;               // stages per TMEM accumulation chunk
+  int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int accumulate;                 // out += conv
   int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
 };
+
+// Shared-memory plan (per CTA, one CTA per SM): a ring of `stages` pipeline
+// stages inside kStageBudget, then two output staging blocks, then barriers.
+// A stage carries `kps` k-steps loaded by ONE TMA box per operand (the box
+// spans kps input-channel blocks): the producer and MMA threads are single
+// warps whose per-stage work (barrier wait, expect_tx, TMA issue, commit,
+// coordinate update) measured ~270 cycles on B200 (tools/conv_times.py with
+// PSCONV_DEBUG=7 on cfg1), which exceeded the 64-cycle MMA time of a BN=64
+// k-step; grouping amortises it over kps k-steps.
+constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
+constexpr int kStageBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
+constexpr int kMaxStages = 16;
 
 template <int BN, bool SPLIT3, bool PAIR>
 struct KernelCfg {
@@ -69,24 +87,7 @@ struct KernelCfg {
   static constexpr int kBRows = BN / kCS;     // B rows staged per CTA
   static constexpr int kABytes = 128 * 64;    // 128 pixels x 16 fp32 channels
   static constexpr int kBBytes = kBRows * 64; // kBRows output channels x 16 input channels
-  // stage: [A | A_lo (3x) | B_hi | B_lo (3x)]
-  // Each pipeline stage carries KPS k-steps: the per-stage synchronisation
-  // (mbarrier waits ~90 cycles even when complete, expect_tx, TMA issue, MMA
-  // commit) measured as a ~330-cycle floor per stage on the single producer /
-  // MMA threads, independent of the tile's MMA size.
-  // stage: [A x KPS | A_lo x KPS (3x) | B_hi x KPS | B_lo x KPS (3x)]
-  static constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
-  // 227 KB per CTA = stages + 2 output staging blocks + barriers + alignment slack
-  static constexpr int kBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
-  static constexpr int kStage1 = (kABytes + kBBytes) * (SPLIT3 ? 2 : 1);  // one k-step
-  static constexpr int KPS = (kBudget / (2 * kStage1) >= 3) ? 2 : 1;     // keep >= 3 stages
-  static constexpr int kALoOff = KPS * kABytes;
-  static constexpr int kBOff = KPS * kABytes * (SPLIT3 ? 2 : 1);
-  static constexpr int kBLoOff = kBOff + KPS * kBBytes;
-  static constexpr int kStageBytes = KPS * kStage1;
-  static constexpr int kStagesRaw = kBudget / kStageBytes;
-  // small stages (small BN): keep up to 12 in flight for HBM-streaming layers
-  static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
+  static constexpr int kOutStageBytes = psconv::kOutStageBytes;
   // TMEM (per CTA: 128 lanes x BN columns per accumulator)
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
   static constexpr int kSumCol = kAccBufs * BN;
@@ -99,12 +100,13 @@ struct KernelCfg {
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + 2 * kOutStageBytes + kBarBytes + 1024;  // +align slack
+      kStageBudget + 2 * kOutStageBytes + kBarBytes + 1024;  // +align slack
   static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
-  static_assert(kStages >= 2, "stages");
-  static_assert(kStages * kStageBytes + 2 * kOutStageBytes + 1024 + 1024 <= 227 * 1024, "smem");
+  static_assert(2 * (kABytes + kBBytes) * (SPLIT3 ? 2 : 1) <= kStageBudget, "two stages of one k-step");
+  static_assert(kSmemBytes <= 227 * 1024, "smem");
+  static_assert(4 * kMaxStages * 8 + 4 * 8 + 4 <= kBarBytes, "barriers");
   static_assert(kColsNeeded <= 512, "TMEM");
   // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
   // a cluster-scope release per k-step (MEMBAR.GPU, measured ~3x slower).
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
   constexpr int CS = Cfg::kCS;
-  constexpr int kStages = Cfg::kStages;
+  const int kStages = p.stages;
   constexpr int kAccBufs = Cfg::kAccBufs;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
 
@@ -158,27 +160,15 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   // same in both CTAs of a pair, which the pair MMA relies on.
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  constexpr int KPS = Cfg::KPS;
-  auto a_buf = [&](int s, int j) { return smem + s * Cfg::kStageBytes + j * Cfg::kABytes; };
-  auto alo_buf = [&](int s, int j) {
-    return smem + s * Cfg::kStageBytes + Cfg::kALoOff + j * Cfg::kABytes;
-  };
-  auto b_buf = [&](int s, int j) {
-    return smem + s * Cfg::kStageBytes + Cfg::kBOff + j * Cfg::kBBytes;
-  };
-  auto blo_buf = [&](int s, int j) {
-    return smem + s * Cfg::kStageBytes + Cfg::kBLoOff + j * Cfg::kBBytes;
-  };
+  auto stage_base = [&](int s) { return smem + s * p.stage_bytes; };
 
-  uint8_t* out_stage = smem + kStages * Cfg::kStageBytes;  // 2 x 8 KB (1024-B aligned)
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes + 2 * Cfg::kOutStageBytes);
-  uint64_t* full = bars;                     // own TMA landed (1 arrive + tx)
-  uint64_t* split_full = bars + kStages;     // own splitter done (count 128)
-  uint64_t* empty = bars + 2 * kStages;      // MMA consumed the stage (commit, pair: both CTAs)
-  uint64_t* peer_full = bars + 3 * kStages;  // leader: the peer's stage is ready (count 1, remote)
-  uint64_t* acc_full = bars + 4 * kStages;   // chunk accumulator ready   [kAccBufs]
-  uint64_t* acc_empty = acc_full + 2;        // chunk accumulator drained [kAccBufs] (4 warps x CS)
+  uint8_t* out_stage = smem + kStageBudget;  // 2 x 8 KB (1024-B aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStageBudget + 2 * Cfg::kOutStageBytes);
+  uint64_t* full = bars;                         // own TMA landed (1 arrive + tx)
+  uint64_t* split_full = bars + kMaxStages;      // own splitter done (count 128)
+  uint64_t* empty = bars + 2 * kMaxStages;       // MMA consumed the stage (commit, pair: both CTAs)
+  uint64_t* acc_full = bars + 3 * kMaxStages;    // chunk accumulator ready   [kAccBufs]
+  uint64_t* acc_empty = acc_full + 2;            // chunk accumulator drained [kAccBufs] (4 warps x CS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
@@ -186,14 +176,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / CS;
   const int nclusters = gridDim.x / CS;
-  const int nchunks = (p.ksteps + p.chunk_ksteps - 1) / p.chunk_ksteps;
+  const int nst = p.ksteps / p.kps;  // pipeline stages per tile
+  const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&split_full[s], 128);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&peer_full[s], 1);
     }
     for (int a = 0; a < kAccBufs; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
@@ -224,16 +214,19 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       if (SPLIT3) ptx::prefetch_tmap(&tmap_flt_lo);
     }
     __syncwarp();
-    const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
+    // one box per operand per stage: A spans kps channel blocks (tensor map
+    // dims [16c][W][H][img][Cb], so each block's rows land contiguously),
+    // B spans the same kps blocks of the prepacked filter ([16c][K][R*S][Cb])
+    const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64 * p.kps);
     // PAIR: both CTAs' loads complete on the LEADER's full barrier (the leader
     // expects both shares); the second CTA never arrives on its own.
     const bool skip_a = (p.debug & 1) != 0;
-    const uint32_t tx1 =
-        ((skip_a ? 0u : a_bytes) + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;  // per k-step
+    const uint32_t tx =
+        ((skip_a ? 0u : a_bytes) + Cfg::kBBytes * p.kps * (SPLIT3 ? 2 : 1)) * CS;  // per stage
     const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
     const int d0 = p.kord[0], d1 = p.kord[1], d2 = p.kord[2];
-    const int e1 = d1 == 0 ? p.Cb : (d1 == 1 ? p.R : p.S);
-    const int e2 = d2 == 0 ? p.Cb : (d2 == 1 ? p.R : p.S);
+    const int e1 = d1 == 0 ? p.cbg : (d1 == 1 ? p.R : p.S);
+    const int e2 = d2 == 0 ? p.cbg : (d2 == 1 ? p.R : p.S);
     int stage = 0;
     uint32_t phase = 0;
     for (int g = cluster; g < p.groups; g += nclusters) {
@@ -243,42 +236,34 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const int n0 = tc.tn * p.Nb;
       const int k0 = tc.tk * BN + rank * Cfg::kBRows;
       int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
-      for (int ks = 0; ks < p.ksteps; ks += KPS) {
-        const int nk = min(KPS, p.ksteps - ks);
+      for (int it = 0; it < nst; ++it) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        const bool issuer = ptx::elect_one();
-        if (issuer && (!PAIR || leader)) ptx::mbar_expect_tx(&full[stage], tx1 * nk);
-#pragma unroll
-        for (int j = 0; j < KPS; ++j) {
-          if (j < nk) {
-            const int cb = d0 == 0 ? v0 : (d1 == 0 ? v1 : v2);
-            const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
-            const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
-            const int crs = (cb * p.R + r) * p.S + s;
-            if (issuer) {
-              if (!PAIR) {
-                if (!skip_a)
-                  ptx::tma_load_5d(a_buf(stage, j), &tmap_in, &full[stage], 0, wq + s, hp + r, cb, n0);
-                ptx::tma_load_3d(b_buf(stage, j), &tmap_flt, &full[stage], 0, k0, crs);
-                if (SPLIT3)
-                  ptx::tma_load_3d(blo_buf(stage, j), &tmap_flt_lo, &full[stage], 0, k0, crs);
-              } else {
-                const uint32_t fb = full_leader + 8u * stage;
-                if (!skip_a)
-                  ptx::tma_load_5d_cb(a_buf(stage, j), &tmap_in, fb, 0, wq + s, hp + r, cb, n0);
-                ptx::tma_load_3d_cb(b_buf(stage, j), &tmap_flt, fb, 0, k0, crs);
-              }
-            }
-            if (++v2 == e2) {
-              v2 = 0;
-              if (++v1 == e1) {
-                v1 = 0;
-                ++v0;
-              }
-            }
+        if (ptx::elect_one()) {
+          const int cb = (d0 == 0 ? v0 : (d1 == 0 ? v1 : v2)) * p.kps;
+          const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
+          const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
+          const int rs = r * p.S + s;
+          uint8_t* sb = stage_base(stage);
+          if (!PAIR) {
+            ptx::mbar_expect_tx(&full[stage], tx);
+            if (!skip_a) ptx::tma_load_5d(sb, &tmap_in, &full[stage], 0, wq + s, hp + r, n0, cb);
+            ptx::tma_load_4d(sb + p.b_off, &tmap_flt, &full[stage], 0, k0, rs, cb);
+            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs, cb);
+          } else {
+            if (leader) ptx::mbar_expect_tx(&full[stage], tx);
+            const uint32_t fb = full_leader + 8u * stage;
+            if (!skip_a) ptx::tma_load_5d_cb(sb, &tmap_in, fb, 0, wq + s, hp + r, n0, cb);
+            ptx::tma_load_4d_cb(sb + p.b_off, &tmap_flt, fb, 0, k0, rs, cb);
           }
         }
         __syncwarp();
+        if (++v2 == e2) {
+          v2 = 0;
+          if (++v1 == e1) {
+            v1 = 0;
+            ++v0;
+          }
+        }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
@@ -291,12 +276,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // Descriptors: A and B are K-major SW64 (64-B rows, 8-row groups 512 B
     // apart); K half h (channels 8h..8h+7) starts 32 B (2 x 16 B) into the row.
     const uint64_t desc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
-    constexpr uint32_t kStageDesc = Cfg::kStageBytes >> 4;
-    constexpr uint32_t kAStepDesc = Cfg::kABytes >> 4;  // next k-step's A tile in the stage
-    constexpr uint32_t kBStepDesc = Cfg::kBBytes >> 4;
-    constexpr uint32_t kAloDesc = Cfg::kALoOff >> 4;
-    constexpr uint32_t kBDesc = Cfg::kBOff >> 4;
-    constexpr uint32_t kBloDesc = Cfg::kBLoOff >> 4;
+    const uint32_t stage_desc = static_cast<uint32_t>(p.stage_bytes) >> 4;
+    const uint32_t a_step = static_cast<uint32_t>(p.a_pitch) >> 4;  // next k-step's A tile
+    constexpr uint32_t kBStep = Cfg::kBBytes >> 4;
+    const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
+    const uint32_t b_off = static_cast<uint32_t>(p.b_off) >> 4;
+    const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
+    const int kps = p.kps;
+    const bool skip_mma = (p.debug & 2) != 0;
     int stage = 0;
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
@@ -310,43 +297,34 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
-        const int ks0 = c * p.chunk_ksteps;
-        const int ks_end = min(p.ksteps, ks0 + p.chunk_ksteps);
-        for (int ks = ks0; ks < ks_end; ks += KPS) {
-          const int nk = min(KPS, ks_end - ks);
+        const int it0 = c * p.chunk_stages;
+        const int it_end = min(nst, it0 + p.chunk_stages);
+        for (int it = it0; it < it_end; ++it) {
           ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t ds = desc0 + static_cast<uint64_t>(stage) * kStageDesc;
           if (ptx::elect_one()) {
+            uint64_t da = desc0 + static_cast<uint64_t>(stage) * stage_desc;
+            uint64_t db = da + b_off;
+            uint32_t acc_in = it == it0 ? 0u : 1u;
+            for (int j = 0; j < kps && !skip_mma; ++j) {
 #pragma unroll
-            for (int j = 0; j < KPS; ++j) {
-              if (j < nk && !(p.debug & 2)) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const uint64_t da_hi = ds + j * kAStepDesc + h * 2;
-                  const uint64_t db_hi = ds + kBDesc + j * kBStepDesc + h * 2;
-                  const uint32_t acc_in = (ks == ks0 && j == 0 && h == 0) ? 0u : 1u;
-                  if (SPLIT3) {
-                    const uint64_t da_lo = ds + kAloDesc + j * kAStepDesc + h * 2;
-                    const uint64_t db_lo = ds + kBloDesc + j * kBStepDesc + h * 2;
-                    if (PAIR) {
-                      ptx::mma_tf32_pair(d_tmem, da_lo, db_hi, kIdesc, acc_in);  // small first
-                      ptx::mma_tf32_pair(d_tmem, da_hi, db_lo, kIdesc, 1u);
-                      ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, 1u);
-                    } else {
-                      ptx::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, acc_in);
-                      ptx::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
-                      ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, 1u);
-                    }
-                  } else {
-                    if (PAIR)
-                      ptx::mma_tf32_pair(d_tmem, da_hi, db_hi, kIdesc, acc_in);
-                    else
-                      ptx::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, acc_in);
-                  }
+              for (int h = 0; h < 2; ++h) {
+                if (SPLIT3) {
+                  const uint64_t da_lo = da + alo_off + h * 2;
+                  const uint64_t db_lo = db - b_off + blo_off + h * 2;
+                  ptx::mma_tf32(d_tmem, da_lo, db + h * 2, kIdesc, acc_in);  // small terms first
+                  ptx::mma_tf32(d_tmem, da + h * 2, db_lo, kIdesc, 1u);
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc, 1u);
+                } else if (PAIR) {
+                  ptx::mma_tf32_pair(d_tmem, da + h * 2, db + h * 2, kIdesc, acc_in);
+                } else {
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc, acc_in);
                 }
+                acc_in = 1u;
               }
+              da += a_step;
+              db += kBStep;
             }
             if (PAIR)
               ptx::mma_commit_pair(&empty[stage]);
@@ -471,26 +449,22 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int g = cluster; g < p.groups; g += nclusters) {
-      for (int ks = 0; ks < p.ksteps; ks += KPS) {
-        const int nk = min(KPS, p.ksteps - ks);
+      for (int it = 0; it < nst; ++it) {
         ptx::mbar_wait(&full[stage], phase);
-#pragma unroll
-        for (int j = 0; j < KPS; ++j) {
-          if (j < nk) {
-            const float4* a = reinterpret_cast<const float4*>(a_buf(stage, j));
-            float4* alo = reinterpret_cast<float4*>(alo_buf(stage, j));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int idx = tid + i * 128;
-              const float4 x = a[idx];
-              float4 lo;
-              lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-              lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-              lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-              lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-              alo[idx] = lo;
-            }
-          }
+        // the stage's kps A tiles are one contiguous box image (same swizzle
+        // phase in the lo region: both offsets are multiples of 512 B)
+        const float4* a = reinterpret_cast<const float4*>(stage_base(stage));
+        float4* alo = reinterpret_cast<float4*>(stage_base(stage) + p.a_lo_off);
+        const int n4 = (p.kps * p.a_pitch) >> 4;
+#pragma unroll 4
+        for (int idx = tid; idx < n4; idx += 128) {
+          const float4 x = a[idx];
+          float4 lo;
+          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          alo[idx] = lo;
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);

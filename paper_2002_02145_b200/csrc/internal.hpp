@@ -52,6 +52,7 @@ struct Recipe {
   int bn = 0;                                                 // 0 = selector decides
   int box_q = 0, box_p = 0, box_n = 0;                        // 0 = selector decides
   int stages = 0;                                             // informational
+  int kg = 0;                                                 // k-steps per stage, 0 = auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -67,6 +68,8 @@ struct Schedule {
   int oj_tile;         // reference tile=oj:T (0 = untiled)
   int chunk;           // k-steps per TMEM accumulation chunk (0 = whole reduction)
   int cs;              // CTAs per cluster sharing (multicasting) the filter block
+  int kps;             // k-steps (input-channel blocks) per pipeline stage
+  int stages;          // pipeline stages in the shared-memory ring
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;
@@ -75,6 +78,12 @@ struct Schedule {
 // Resolves a recipe (possibly partial) against a descriptor; throws ConfigError
 // for illegal recipes (same checks as variants.hpp:186-228 plan_recipe).
 Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gpu = true);
+
+// Shared-memory pipeline geometry (conv_kernel.cuh): k-steps per stage and ring depth.
+constexpr int kSmemStageBudget = 227 * 1024 - 2 * 128 * 64 - 2048 - 1024;
+constexpr int kSmemMaxStages = 16;
+int stage_bytes(const Schedule& s, int mode);  // bytes of one stage of s.kps k-steps
+void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg);  // throws ConfigError
 
 // Closed-form model (select.cpp).
 struct ModelBreakdown {

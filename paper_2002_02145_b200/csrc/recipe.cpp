@@ -96,6 +96,10 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "cl") {
           r.cs = static_cast<int>(parse_int(val, "gpu cluster size"));
           if (r.cs != 1 && r.cs != 2) throw ConfigError("gpu cl must be 1 (single CTA) or 2 (CTA pair)");
+        } else if (key == "kg") {
+          r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
+          if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
+            throw ConfigError("gpu kg must be 1, 2, 4 or 8");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -123,6 +127,7 @@ std::string Recipe::id() const {
     s += ";gpu=bn:" + std::to_string(bn) + ",box:" + std::to_string(box_q) + "x" +
          std::to_string(box_p) + "x" + std::to_string(box_n);
     if (cs) s += ",cl:" + std::to_string(cs);
+    if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
   return s;
@@ -281,9 +286,49 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   // (error ~1.2e-7 per k-step of chunk, tools/chunk_sweep.py: ch 32 -> 3.5e-6)
   s.chunk = r.chunk ? r.chunk : (mode == PSCONV_MODE_3XTF32 ? (s.bn == 256 ? 32 : 16) : ksteps);
   if (s.chunk > ksteps) s.chunk = ksteps;
+  plan_stages(d, s, mode, r.kg);
+  s.chunk = (s.chunk + s.kps - 1) / s.kps * s.kps;  // chunks hold whole stages
   canon.chunk = (mode == PSCONV_MODE_3XTF32 || r.chunk) ? s.chunk : 0;
+  canon.kg = r.kg ? s.kps : 0;
   s.recipe_id = canon.id();
   return s;
+}
+
+int stage_bytes(const Schedule& s, int mode) {
+  const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
+  return s.kps * (128 * 64 + (s.bn / s.cs) * 64) * mult;
+}
+
+// One pipeline stage carries kps k-steps = kps consecutive input-channel blocks
+// at one (kj, ki), loaded by one TMA box per operand. Auto: the largest of
+// {4, 2} dividing Cb that keeps >= 3 stages in the ring; the box rows of the
+// kps A tiles must stay whole 8-row swizzle atoms.
+void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
+  const int Cb = static_cast<int>(d.nIfm / 16);
+  const int rows = s.qb * s.pb * s.nb;
+  auto ring = [&](int k) {
+    Schedule t = s;
+    t.kps = k;
+    return std::min(kSmemMaxStages, kSmemStageBudget / stage_bytes(t, mode));
+  };
+  int kps = 1;
+  if (kg) {
+    if (Cb % kg != 0)
+      throw ConfigError("GPU tile: kg=" + std::to_string(kg) + " does not divide nIfm/16=" +
+                        std::to_string(Cb));
+    if (kg > 1 && rows % 8 != 0)
+      throw ConfigError("GPU tile: kg > 1 needs the box to hold a multiple of 8 pixels");
+    if (ring(kg) < 2) throw ConfigError("GPU tile: kg=" + std::to_string(kg) + " leaves < 2 stages");
+    kps = kg;
+  } else if (rows % 8 == 0) {
+    for (int k : {4, 2})
+      if (Cb % k == 0 && ring(k) >= 3) {
+        kps = k;
+        break;
+      }
+  }
+  s.kps = kps;
+  s.stages = ring(kps);
 }
 
 }  // namespace psconv

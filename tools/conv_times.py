@@ -42,6 +42,21 @@ def main():
         ms = statistics.median(ts)
         print(f"{conv} {mode} {ms * 1e3:8.1f} us {p.flops() / ms / 1e9:8.1f} TFLOP/s  {plan.recipe}",
               flush=True)
+        if os.environ.get("CT_DIAG"):
+            import time
+            torch.cuda.synchronize()
+            h0 = time.perf_counter()
+            for _ in range(50):
+                f()
+            h1 = time.perf_counter()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(50):
+                f()
+            e1.record(st)
+            torch.cuda.synchronize()
+            print(f"   host {1e6 * (h1 - h0) / 50:.1f} us/call; back-to-back {e0.elapsed_time(e1) * 20:.1f} us/call")
         plan.close()
 
 
