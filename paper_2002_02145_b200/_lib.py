@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsconv.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("PSCONV_LIB_NAME", "libpsconv.so"))  # A/B builds (tools)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

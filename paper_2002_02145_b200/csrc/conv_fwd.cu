@@ -233,7 +233,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CS);
     cfg.blockDim = dim3(Cfg::kThreads);
-    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.dynamicSmemBytes = Cfg::smem_bytes(prm.ring_bytes);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -241,7 +241,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CS > 1 ? 1 : 0;  // plain launch for single-CTA clusters
     CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
   }
 }
@@ -410,6 +410,9 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
       encode(&tout, base, 5, dims, strides, box, estr);
     }
+    const int rows = s.qb * s.pb * s.nb;
+    const bool a_packed = rows % 8 == 0;
+    const bool a_group = Cb % s.kps == 0 && a_packed;  // one A box spans the stage's blocks
     // A: input NCHW16c [img_count][Cb][H][W][16] viewed with its dims ordered
     // [16c][W][H][img][Cb] (TMA dims need not follow memory order): the box
     // [16][Qb*sw][Pb*sh][Nb][kps] lands as kps contiguous 128-row tiles, one per
@@ -421,7 +424,7 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
                                      cuuint64_t(H) * W * 64};
       const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
-                                 cuuint32_t(s.nb), cuuint32_t(s.kps)};
+                                 cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
       const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
       encode(&ta, base, 5, dims, strides, box, estr);
     }
@@ -438,7 +441,7 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     {
       const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
       const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
-      const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps)};
+      const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
       const cuuint32_t estr[4] = {1, 1, 1, 1};
       encode(&tb, b_hi, 4, dims, strides, box, estr);
       encode(&tblo, b_lo, 4, dims, strides, box, estr);
@@ -477,18 +480,23 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.k_outer = pos[1] == 0 ? 1 : 0;
     prm.ksteps = Cb * R * S;
     prm.kps = s.kps;
-    prm.cbg = Cb / s.kps;
+    prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
+    prm.cbg = prm.cb_group ? Cb / s.kps : Cb;
+    prm.nst = (prm.ksteps + s.kps - 1) / s.kps;
     prm.stages = s.stages;
     {
       const int mult = split3 ? 2 : 1;
       const int brows = s.bn / s.cs;
       prm.stage_bytes = stage_bytes(s, P->mode);
-      prm.a_pitch = s.qb * s.pb * s.nb * 64;
+      // one A box for the stage's channel blocks when its rows are whole 8-row
+      // swizzle atoms; else one box per block at 8 KB pitch
+      prm.a_boxes = (prm.cb_group && a_packed) ? 1 : (prm.cb_group ? s.kps : 1);
+      prm.a_pitch = (prm.cb_group && a_packed) ? rows * 64 : 8192;
       prm.a_lo_off = s.kps * 8192;
       prm.b_off = s.kps * 8192 * mult;
       prm.b_lo_off = prm.b_off + s.kps * brows * 64;
-      if (prm.stages < 2 || prm.stages > kMaxStages || prm.stages * prm.stage_bytes > kStageBudget ||
-          Cb % s.kps != 0)
+      prm.ring_bytes = (prm.stages * prm.stage_bytes + 1023) / 1024 * 1024;
+      if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)
         throw RuntimeError("internal: bad pipeline stage plan");
     }
     const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
@@ -501,12 +509,31 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       return e ? std::atoi(e) : 0;
     }();
     prm.debug = debug_env;
+    static unsigned long long* trace_buf = nullptr;
+    if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, (8 * kTraceStages + 8) * 8));
+    prm.debug = debug_env & 7;
+    prm.trace = (debug_env & 8) ? trace_buf : nullptr;
     prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
     prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
     if (split3)
       dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
     else
       dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
+    if (prm.trace) {  // profiling: dump CTA 0's per-stage clocks (producer | MMA issuer)
+      unsigned long long h[8 * kTraceStages + 8];
+      CUDA_OK(cudaStreamSynchronize(st));
+      CUDA_OK(cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost));
+      const unsigned long long t0 = h[8 * kTraceStages];
+      std::fprintf(stderr, "events: setup %lld first-acc %lld last-store %lld stores-done %lld exit %lld\n",
+                   (long long)(h[8 * kTraceStages + 1] - t0), (long long)(h[8 * kTraceStages + 4] - t0),
+                   (long long)(h[8 * kTraceStages + 5] - t0), (long long)(h[8 * kTraceStages + 6] - t0),
+                   (long long)(h[8 * kTraceStages + 7] - t0));
+      for (int i = 0; i < kTraceStages; ++i)
+        std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld\n", i,
+                     (long long)(h[i * 4] - t0), (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
+                     (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
+                     (long long)(h[4 * kTraceStages + i * 4 + 2] - t0));
+    }
   });
 }
 

@@ -56,10 +56,16 @@ struct ConvParams {
   int k_outer;                    // 1: ofm_tile outer of the pixel loops (recipe order)
   int ksteps;                     // Cb*R*S
   int kps;                        // k-steps per pipeline stage (input-channel blocks per TMA box)
-  int cbg;                        // Cb / kps
+  int cbg;                        // extent of the channel-block counter (Cb / kps or Cb)
   int stages;                     // pipeline stages in the ring (<= kMaxStages)
   int stage_bytes;                // [A x kps | A_lo x kps (3x) | B x kps | B_lo x kps (3x)]
-  int a_pitch;                    // bytes between the kps A tiles of a stage (box rows x 64)
+  int ring_bytes;                 // stages * stage_bytes rounded up to 1 KB
+  int a_pitch;                    // bytes between the kps A tiles of a stage
+  int cb_group;                   // 1: a stage = kps channel blocks at one (kj, ki), one B box
+                                  // spanning them; 0: kps consecutive k-steps, one box each
+  int a_boxes;                    // A boxes per coordinate step: 1 (spans the step's blocks;
+                                  // a_pitch = box rows x 64 or 8 KB) or kps (one per block, 8 KB)
+  int nst;                        // stages per tile = ceil(ksteps / kps)
   int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
   int chunk_stages;               // stages per TMEM accumulation chunk
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
@@ -67,7 +73,9 @@ struct ConvParams {
   int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
+  unsigned long long* trace;      // profiling only (PSCONV_DEBUG & 8): CTA 0 stage timestamps
 };
+constexpr int kTraceStages = 128;
 
 // Shared-memory plan (per CTA, one CTA per SM): a ring of `stages` pipeline
 // stages inside kStageBudget, then two output staging blocks, then barriers.
@@ -100,7 +108,8 @@ struct KernelCfg {
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
-      kStageBudget + 2 * kOutStageBytes + kBarBytes + 1024;  // +align slack
+      kStageBudget + 2 * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
+  static constexpr int smem_bytes(int ring_bytes) { return ring_bytes + 2 * kOutStageBytes + kBarBytes + 1024; }
   static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
@@ -155,6 +164,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   constexpr int kAccBufs = Cfg::kAccBufs;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
 
+  const long long t_entry = clock64();
+  unsigned long long* ev = (p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * kTraceStages : nullptr;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B). The offset is the
   // same in both CTAs of a pair, which the pair MMA relies on.
@@ -162,8 +173,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   auto stage_base = [&](int s) { return smem + s * p.stage_bytes; };
 
-  uint8_t* out_stage = smem + kStageBudget;  // 2 x 8 KB (1024-B aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStageBudget + 2 * Cfg::kOutStageBytes);
+  uint8_t* out_stage = smem + p.ring_bytes;  // 2 x 8 KB (1024-B aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.ring_bytes + 2 * Cfg::kOutStageBytes);
   uint64_t* full = bars;                         // own TMA landed (1 arrive + tx)
   uint64_t* split_full = bars + kMaxStages;      // own splitter done (count 128)
   uint64_t* empty = bars + 2 * kMaxStages;       // MMA consumed the stage (commit, pair: both CTAs)
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / CS;
   const int nclusters = gridDim.x / CS;
-  const int nst = p.ksteps / p.kps;  // pipeline stages per tile
+  const int nst = p.nst;  // pipeline stages per tile
   const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
 
   if (threadIdx.x == 0) {
@@ -202,6 +213,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   if (PAIR) ptx::cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (ev && threadIdx.x == 0) {
+    ev[0] = t_entry;
+    ev[1] = clock64();  // barriers initialised, TMEM allocated
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -217,17 +232,21 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // one box per operand per stage: A spans kps channel blocks (tensor map
     // dims [16c][W][H][img][Cb], so each block's rows land contiguously),
     // B spans the same kps blocks of the prepacked filter ([16c][K][R*S][Cb])
-    const uint32_t a_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64 * p.kps);
+    const uint32_t a_step_bytes = static_cast<uint32_t>(p.Qb * p.Pb * p.Nb * 64);
     // PAIR: both CTAs' loads complete on the LEADER's full barrier (the leader
     // expects both shares); the second CTA never arrives on its own.
     const bool skip_a = (p.debug & 1) != 0;
-    const uint32_t tx =
-        ((skip_a ? 0u : a_bytes) + Cfg::kBBytes * p.kps * (SPLIT3 ? 2 : 1)) * CS;  // per stage
+    const uint32_t tx1 =
+        ((skip_a ? 0u : a_step_bytes) + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;  // per k-step
     const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
+    // cb_group: one coordinate step per stage, boxes span kps channel blocks;
+    // otherwise kps coordinate steps per stage (the last stage may be partial)
+    const int nsub = p.cb_group ? 1 : p.kps;
+    const int cb_mul = p.cb_group ? p.kps : 1;
     const int d0 = p.kord[0], d1 = p.kord[1], d2 = p.kord[2];
     const int e1 = d1 == 0 ? p.cbg : (d1 == 1 ? p.R : p.S);
     const int e2 = d2 == 0 ? p.cbg : (d2 == 1 ? p.R : p.S);
-    int stage = 0;
+    int stage = 0, gs = 0;
     uint32_t phase = 0;
     for (int g = cluster; g < p.groups; g += nclusters) {
       const TileCoord tc = decode_group(p, g, rank, CS);
@@ -236,34 +255,49 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const int n0 = tc.tn * p.Nb;
       const int k0 = tc.tk * BN + rank * Cfg::kBRows;
       int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
-      for (int it = 0; it < nst; ++it) {
+      for (int it = 0; it < p.nst; ++it) {
+        const int nk = min(p.kps, p.ksteps - it * p.kps);
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        if (tr) p.trace[gs * 4 + 0] = clock64();
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        if (ptx::elect_one()) {
-          const int cb = (d0 == 0 ? v0 : (d1 == 0 ? v1 : v2)) * p.kps;
+        if (tr) p.trace[gs * 4 + 1] = clock64();
+        uint8_t* sb = stage_base(stage);
+        const bool issuer = ptx::elect_one();
+        if (issuer && (!PAIR || leader)) ptx::mbar_expect_tx(&full[stage], tx1 * nk);
+        for (int j = 0; j < nsub && j < nk; ++j) {
+          const int cb = (d0 == 0 ? v0 : (d1 == 0 ? v1 : v2)) * cb_mul;
           const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
           const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
           const int rs = r * p.S + s;
-          uint8_t* sb = stage_base(stage);
-          if (!PAIR) {
-            ptx::mbar_expect_tx(&full[stage], tx);
-            if (!skip_a) ptx::tma_load_5d(sb, &tmap_in, &full[stage], 0, wq + s, hp + r, n0, cb);
-            ptx::tma_load_4d(sb + p.b_off, &tmap_flt, &full[stage], 0, k0, rs, cb);
-            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs, cb);
-          } else {
-            if (leader) ptx::mbar_expect_tx(&full[stage], tx);
-            const uint32_t fb = full_leader + 8u * stage;
-            if (!skip_a) ptx::tma_load_5d_cb(sb, &tmap_in, fb, 0, wq + s, hp + r, n0, cb);
-            ptx::tma_load_4d_cb(sb + p.b_off, &tmap_flt, fb, 0, k0, rs, cb);
+          if (issuer) {
+            uint8_t* sa = sb + j * p.a_boxes * p.a_pitch;
+            uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes;
+            if (!PAIR) {
+              if (!skip_a)
+                for (int i = 0; i < p.a_boxes; ++i)
+                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + s, hp + r, n0, cb + i);
+              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb);
+              if (SPLIT3)
+                ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs, cb);
+            } else {
+              const uint32_t fb = full_leader + 8u * stage;
+              if (!skip_a)
+                for (int i = 0; i < p.a_boxes; ++i)
+                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + s, hp + r, n0, cb + i);
+              ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb);
+            }
+          }
+          if (++v2 == e2) {
+            v2 = 0;
+            if (++v1 == e1) {
+              v1 = 0;
+              ++v0;
+            }
           }
         }
         __syncwarp();
-        if (++v2 == e2) {
-          v2 = 0;
-          if (++v1 == e1) {
-            v1 = 0;
-            ++v0;
-          }
-        }
+        if (tr) p.trace[gs * 4 + 2] = clock64();
+        ++gs;
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
@@ -284,7 +318,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
     const int kps = p.kps;
     const bool skip_mma = (p.debug & 2) != 0;
-    int stage = 0;
+    int stage = 0, gs = 0;
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
     for (int g = cluster; g < p.groups; g += nclusters) {
@@ -300,14 +334,18 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const int it0 = c * p.chunk_stages;
         const int it_end = min(nst, it0 + p.chunk_stages);
         for (int it = it0; it < it_end; ++it) {
+          const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+          if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
           ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
           ptx::tc_fence_after();
+          if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
           if (ptx::elect_one()) {
             uint64_t da = desc0 + static_cast<uint64_t>(stage) * stage_desc;
             uint64_t db = da + b_off;
             uint32_t acc_in = it == it0 ? 0u : 1u;
-            for (int j = 0; j < kps && !skip_mma; ++j) {
+            const int nk = min(kps, p.ksteps - it * kps);  // partial last stage (cb_group = 0)
+            for (int j = 0; j < nk && !skip_mma; ++j) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 if (SPLIT3) {
@@ -332,6 +370,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               ptx::mma_commit(&empty[stage]);
           }
           __syncwarp();
+          if (tr) p.trace[4 * kTraceStages + gs * 4 + 2] = clock64();
+          ++gs;
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -380,6 +420,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
 #else
         ptx::mbar_wait(&acc_full[buf], acc_phase);
 #endif
+        if (ev && store_thread && cit == 0) ev[4] = clock64();
         ptx::tc_fence_after();
         const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
@@ -441,7 +482,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         __syncwarp();
       }
     }
+    if (ev && store_thread) ev[5] = clock64();  // last store issued
     if (store_thread) ptx::bulk_wait_all();  // stores complete before smem is released
+    if (ev && store_thread) ev[6] = clock64();
   } else if (SPLIT3) {
     // ------------------------------------------------------------ splitter
     // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
@@ -451,20 +494,28 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     for (int g = cluster; g < p.groups; g += nclusters) {
       for (int it = 0; it < nst; ++it) {
         ptx::mbar_wait(&full[stage], phase);
-        // the stage's kps A tiles are one contiguous box image (same swizzle
-        // phase in the lo region: both offsets are multiples of 512 B)
+        // A tiles of the stage: kps x a_pitch bytes (packed box image, or 8 KB
+        // tiles); the lo region mirrors it (offsets are multiples of 512 B, so
+        // the swizzle phase matches). Loads are batched 4 deep for ILP.
         const float4* a = reinterpret_cast<const float4*>(stage_base(stage));
         float4* alo = reinterpret_cast<float4*>(stage_base(stage) + p.a_lo_off);
-        const int n4 = (p.kps * p.a_pitch) >> 4;
-#pragma unroll 4
-        for (int idx = tid; idx < n4; idx += 128) {
-          const float4 x = a[idx];
-          float4 lo;
-          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          alo[idx] = lo;
+        const int n4 = (min(p.kps, p.ksteps - it * p.kps) * p.a_pitch) >> 4;
+        for (int base = tid; base < n4; base += 512) {
+          float4 x[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (base + i * 128 < n4) x[i] = a[base + i * 128];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (base + i * 128 < n4) {
+              float4 lo;
+              lo.x = x[i].x - __uint_as_float(__float_as_uint(x[i].x) & 0xFFFFE000u);
+              lo.y = x[i].y - __uint_as_float(__float_as_uint(x[i].y) & 0xFFFFE000u);
+              lo.z = x[i].z - __uint_as_float(__float_as_uint(x[i].z) & 0xFFFFE000u);
+              lo.w = x[i].w - __uint_as_float(__float_as_uint(x[i].w) & 0xFFFFE000u);
+              alo[base + i * 128] = lo;
+            }
+          }
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);
@@ -479,6 +530,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (PAIR) ptx::cluster_sync_all();  // no CTA leaves while the pair still uses it
+  if (ev && threadIdx.x == 0) ev[7] = clock64();
   if (warp == 1) {
     ptx::tc_fence_after();
     if (PAIR)

@@ -299,13 +299,15 @@ int stage_bytes(const Schedule& s, int mode) {
   return s.kps * (128 * 64 + (s.bn / s.cs) * 64) * mult;
 }
 
-// One pipeline stage carries kps k-steps = kps consecutive input-channel blocks
-// at one (kj, ki), loaded by one TMA box per operand. Auto: the largest of
-// {4, 2} dividing Cb that keeps >= 3 stages in the ring; the box rows of the
-// kps A tiles must stay whole 8-row swizzle atoms.
+// One pipeline stage carries kps k-steps. When kps divides Cb they are kps
+// consecutive input-channel blocks at one (kj, ki), loaded by one TMA box per
+// operand (conv_fwd.cu; the A box is split per block when its rows are not
+// whole 8-row swizzle atoms); otherwise kps consecutive k-steps of the
+// reduction order with one box each (e.g. the stem, Cb = 1). Auto: the largest
+// of {4, 2} that keeps >= 3 stages in the ring, preferring divisors of Cb.
 void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   const int Cb = static_cast<int>(d.nIfm / 16);
-  const int rows = s.qb * s.pb * s.nb;
+  const int ksteps = static_cast<int>(Cb * d.kh * d.kw);
   auto ring = [&](int k) {
     Schedule t = s;
     t.kps = k;
@@ -313,19 +315,21 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   };
   int kps = 1;
   if (kg) {
-    if (Cb % kg != 0)
-      throw ConfigError("GPU tile: kg=" + std::to_string(kg) + " does not divide nIfm/16=" +
-                        std::to_string(Cb));
-    if (kg > 1 && rows % 8 != 0)
-      throw ConfigError("GPU tile: kg > 1 needs the box to hold a multiple of 8 pixels");
+    if (kg > ksteps) throw ConfigError("GPU tile: kg=" + std::to_string(kg) + " exceeds the reduction");
     if (ring(kg) < 2) throw ConfigError("GPU tile: kg=" + std::to_string(kg) + " leaves < 2 stages");
     kps = kg;
-  } else if (rows % 8 == 0) {
+  } else {
     for (int k : {4, 2})
       if (Cb % k == 0 && ring(k) >= 3) {
         kps = k;
         break;
       }
+    if (kps == 1 && ksteps > 1)
+      for (int k : {4, 2})
+        if (k <= ksteps && ring(k) >= 3) {
+          kps = k;
+          break;
+        }
   }
   s.kps = kps;
   s.stages = ring(kps);

@@ -88,6 +88,29 @@ def test_recipes(recipe):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    # Cb=4: channel-block groups, one packed A box per stage (64 rows per block)
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,cl:1,kg:4"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,cl:1,kg:2"),
+    # box rows not a multiple of 8 -> one A box per channel block (8 KB pitch)
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:32,box:7x3x2,cl:1,kg:4"),
+    # Cb=3 (kg does not divide it): kps consecutive k-steps, partial last stage (27 = 6*4+3)
+    ("conv:2,32,48,9,9,3,3,1,1,16,1,1,9,9", 48, "gpu=bn:32,box:9x9x1,cl:1,kg:4"),
+    ("conv:2,32,48,9,9,3,3,2,2,16,1,1,18,18", 48, "gpu=bn:16,box:9x9x1,cl:1,kg:2"),
+    # stem-like: Cb=1, 7x7/s2, 49 k-steps
+    ("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32", 3, "gpu=bn:64,box:16x8x1,cl:1,kg:4"),
+])
+def test_stage_geometry(conv, c_log, recipe, mode):
+    """Pipeline stages of kps k-steps: grouped channel blocks (packed or per-block A boxes)
+    and consecutive-k-step stages with a partial last stage; CTA pair where the mode allows."""
+    _check("stages", conv, c_log, 7, mode, ps.ConvPreset.parse(conv).nImg, recipe)
+    if mode == "tf32":
+        _check("stages-pair", conv, c_log, 7, mode, ps.ConvPreset.parse(conv).nImg,
+               recipe.replace("cl:1", "cl:2"))
+
+
+@pytest.mark.gpu
 def test_image_range_and_accumulate():
     """conv_fwd on [img_begin, img_begin+count) touches only those images; FLAG_ACCUMULATE
     reproduces the reference body's `+=` (presets.hpp:112)."""
