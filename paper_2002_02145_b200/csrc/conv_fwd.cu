@@ -25,7 +25,8 @@ struct conv_plan {
   int device;
   int num_sms;
   psconv::Schedule sched;
-  float* flt_pack = nullptr;   // prepacked K-major filter [CRS][K][16c]: hi (| lo for 3xTF32)
+  float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
+  bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
 };
@@ -61,32 +62,41 @@ EncodeTiledFn encode_fn() {
 }
 
 void encode(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
-            const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr) {
+            const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr,
+            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
   const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base),
                                  dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw RuntimeError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
 // ---------------------------------------------------------------- helpers
-// Filter prepack: KCRS16c16k [Kb][C*R*S/16 blocks][16c][16k] -> K-major
-// [CRS][K][16c] (one 64-B row of 16 input channels per output channel), which
-// is the B-operand layout tcgen05 kind::tf32 accepts (K-major SWIZZLE_64B).
+// Filter prepack: KCRS16c16k [Kb][C*R*S/16 blocks][16c][16k] -> K-major rows
+// (one row of input channels per output channel), the B-operand layout
+// tcgen05 kind::tf32 accepts (K-major; MN-major reads as zeros, probe2.cu):
+//   b128 = 0: [Cb][R*S][K][16c]      64-B rows, SWIZZLE_64B
+//   b128 = 1: [Cb/2][R*S][K][32c]   128-B rows holding channel blocks 2i, 2i+1
+//             (SWIZZLE_128B): half the TMA row requests per k-step, which is
+//             what bounds operand delivery (tools/probe_tma_issue.cu).
 // 3xTF32: also split x -> hi = x with the 13 low mantissa bits cleared
 // (exactly representable in tf32) and lo = x - hi (exact in fp32).
 // One 256-thread block per 16x16 [c][k] block, transposed through smem.
 __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __restrict__ hi,
-                                      float* __restrict__ lo, int K, int CRS, int split) {
+                                      float* __restrict__ lo, int K, int CRS, int RS, int split,
+                                      int b128) {
   __shared__ float tile[16][17];
-  const int blk = blockIdx.x;  // = kb * CRS + crs
+  const int blk = blockIdx.x;  // = kb * CRS + crs, crs = cb * RS + rs
   const int kb = blk / CRS, crs = blk % CRS;
   const int t = threadIdx.x;
   tile[t >> 4][t & 15] = flt[static_cast<int64_t>(blk) * 256 + t];  // [c][k]
   __syncthreads();
   const int k16 = t >> 4, c16 = t & 15;
   const float x = tile[c16][k16];
-  const int64_t o = (static_cast<int64_t>(crs) * K + kb * 16 + k16) * 16 + c16;
+  const int cb = crs / RS, rs = crs % RS;
+  const int64_t k = kb * 16 + k16;
+  const int64_t o = b128 ? ((static_cast<int64_t>(cb >> 1) * RS + rs) * K + k) * 32 + (cb & 1) * 16 + c16
+                         : ((static_cast<int64_t>(cb) * RS + rs) * K + k) * 16 + c16;
   if (split) {
     const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     hi[o] = h;
@@ -201,7 +211,8 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
   const bool split3 = P->mode == PSCONV_MODE_3XTF32;
   prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
                                                   split3 ? P->flt_pack + P->flt_elems : nullptr,
-                                                  int(P->d.nOfm), CRS, split3 ? 1 : 0);
+                                                  int(P->d.nOfm), CRS, int(P->d.kh * P->d.kw),
+                                                  split3 ? 1 : 0, P->b128 ? 1 : 0);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -322,6 +333,8 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     P->device = device;
     P->num_sms = prop.multiProcessorCount;
     P->sched = s;
+    // 128-B filter rows pair channel blocks inside a stage: needs even kps dividing Cb
+    P->b128 = s.kps % 2 == 0 && (d.nIfm / 16) % s.kps == 0 && std::getenv("PSCONV_NO_B128") == nullptr;
     P->flt_elems = d.nOfm * d.nIfm * d.kh * d.kw;
     {
       int prev = 0;
@@ -437,8 +450,15 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       launch_prepack(P, flt, st);
       P->prepacked = false;  // buffer now holds this call's filter
     }
-    // B viewed as [16c][K][R*S][Cb] (crs = cb*R*S + r*S + s): box {16, rows, 1, kps}
-    {
+    // B viewed as [16c][K][R*S][Cb] (b128: [32c][K][R*S][Cb/2]); box {c, rows, 1, blocks}
+    if (P->b128) {
+      const cuuint64_t dims[4] = {32, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
+      const cuuint64_t strides[3] = {128, cuuint64_t(K) * 128, cuuint64_t(K) * 128 * R * S};
+      const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps / 2)};
+      const cuuint32_t estr[4] = {1, 1, 1, 1};
+      encode(&tb, b_hi, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+      encode(&tblo, b_lo, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
       const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
       const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
       const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
@@ -481,6 +501,7 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     prm.ksteps = Cb * R * S;
     prm.kps = s.kps;
     prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
+    prm.b128 = P->b128 ? 1 : 0;
     prm.cbg = prm.cb_group ? Cb / s.kps : Cb;
     prm.nst = (prm.ksteps + s.kps - 1) / s.kps;
     prm.stages = s.stages;

@@ -61,6 +61,7 @@ struct ConvParams {
   int stage_bytes;                // [A x kps | A_lo x kps (3x) | B x kps | B_lo x kps (3x)]
   int ring_bytes;                 // stages * stage_bytes rounded up to 1 KB
   int a_pitch;                    // bytes between the kps A tiles of a stage
+  int b128;                       // filter rows hold 2 channel blocks (128 B, SWIZZLE_128B)
   int cb_group;                   // 1: a stage = kps channel blocks at one (kj, ki), one B box
                                   // spanning them; 0: kps consecutive k-steps, one box each
   int a_boxes;                    // A boxes per coordinate step: 1 (spans the step's blocks;
@@ -276,15 +277,16 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + s, hp + r, n0, cb + i);
-              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb);
+              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb >> p.b128);
               if (SPLIT3)
-                ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs, cb);
+                ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
+                                 cb >> p.b128);
             } else {
               const uint32_t fb = full_leader + 8u * stage;
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + s, hp + r, n0, cb + i);
-              ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb);
+              ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
             }
           }
           if (++v2 == e2) {
@@ -310,9 +312,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // Descriptors: A and B are K-major SW64 (64-B rows, 8-row groups 512 B
     // apart); K half h (channels 8h..8h+7) starts 32 B (2 x 16 B) into the row.
     const uint64_t desc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
+    // B: SW64 rows of one channel block, or (b128) SW128 rows of a block pair:
+    // k-step j of the pair sits 64 B into the row, 8-row atoms 1024 B apart
+    const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : desc0;
+    const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);                 // after an even j
+    const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
     const uint32_t stage_desc = static_cast<uint32_t>(p.stage_bytes) >> 4;
     const uint32_t a_step = static_cast<uint32_t>(p.a_pitch) >> 4;  // next k-step's A tile
-    constexpr uint32_t kBStep = Cfg::kBBytes >> 4;
     const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
     const uint32_t b_off = static_cast<uint32_t>(p.b_off) >> 4;
     const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
           if (ptx::elect_one()) {
             uint64_t da = desc0 + static_cast<uint64_t>(stage) * stage_desc;
-            uint64_t db = da + b_off;
+            uint64_t db = bdesc0 + static_cast<uint64_t>(stage) * stage_desc + b_off;
             uint32_t acc_in = it == it0 ? 0u : 1u;
             const int nk = min(kps, p.ksteps - it * kps);  // partial last stage (cb_group = 0)
             for (int j = 0; j < nk && !skip_mma; ++j) {
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
                 acc_in = 1u;
               }
               da += a_step;
-              db += kBStep;
+              db += (j & 1) ? b_odd : b_even;
             }
             if (PAIR)
               ptx::mma_commit_pair(&empty[stage]);

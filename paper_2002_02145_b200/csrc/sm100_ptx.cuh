@@ -341,6 +341,13 @@ __device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr, uint32_t lbo,
          (4ull << 61);   // layout type: SWIZZLE_64B
 }
 
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) |
+         (static_cast<uint64_t>(lbo >> 4) << 16) | (static_cast<uint64_t>(sbo >> 4) << 32) |
+         (1ull << 46) |  // descriptor version (sm_100)
+         (2ull << 61);   // layout type: SWIZZLE_128B
+}
+
 // Instruction descriptor: kind::tf32, D=f32, A and B K-major, M=128.
 // (Measured on B200: kind::tf32 with an MN-major SWIZZLE_64B B operand
 // silently yields zeros -- tools/probe2.cu -- so B is prepacked K-major.)
