@@ -436,10 +436,17 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
                                   cuuint64_t(Cb)};
       const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
                                      cuuint64_t(H) * W * 64};
-      const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
-                                 cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
-      const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
-      encode(&ta, base, 5, dims, strides, box, estr);
+      if (s.halo) {  // halo box: hr padded rows of hw pixels, kps blocks
+        const HaloGeom h = halo_geom(d, s, P->mode);
+        const cuuint32_t box[5] = {16, cuuint32_t(h.hw), cuuint32_t(h.hr), 1, cuuint32_t(s.kps)};
+        const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+        encode(&ta, base, 5, dims, strides, box, estr);
+      } else {
+        const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
+                                   cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
+        const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
+        encode(&ta, base, 5, dims, strides, box, estr);
+      }
     }
     // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
     const int CRS = Cb * R * S;
@@ -517,6 +524,23 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
       prm.b_off = s.kps * 8192 * mult;
       prm.b_lo_off = prm.b_off + s.kps * brows * 64;
       prm.ring_bytes = (prm.stages * prm.stage_bytes + 1023) / 1024 * 1024;
+      if (s.halo) {
+        const HaloGeom h = halo_geom(d, s, P->mode);
+        prm.halo = 1;
+        prm.hw = h.hw;
+        prm.hr = h.hr;
+        prm.a_tile = h.a_tile;
+        prm.stage_bytes = h.a_stage;
+        prm.a_lo_off = h.a_lo_off;
+        prm.hb_stages = s.hb_stages;
+        prm.hb_stage_bytes = h.b_stage;
+        prm.b_lo_off = h.b_lo_off;
+        prm.hb_ring_off = prm.stages * h.a_stage;
+        prm.ring_bytes = prm.hb_ring_off + prm.hb_stages * h.b_stage;
+        prm.nst = prm.cbg * R * S;  // taps per tile (B stages)
+        if (prm.stages > kHaloB || prm.hb_stages < 2 || prm.hb_stages > kMaxStages - kHaloB)
+          throw RuntimeError("internal: bad halo stage plan");
+      }
       if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)
         throw RuntimeError("internal: bad pipeline stage plan");
     }

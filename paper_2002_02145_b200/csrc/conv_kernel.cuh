@@ -62,6 +62,16 @@ struct ConvParams {
   int ring_bytes;                 // stages * stage_bytes rounded up to 1 KB
   int a_pitch;                    // bytes between the kps A tiles of a stage
   int b128;                       // filter rows hold 2 channel blocks (128 B, SWIZZLE_128B)
+  // halo mode (stride-1 R x S > 1): the M tile is Pb whole output rows of one
+  // image laid out at the padded input pitch hw = Q + S - 1 (columns q >= Q
+  // are junk rows); one TMA box loads the input halo (hr = Pb + R - 1 rows of
+  // hw pixels) per channel block ONCE, and the R*S shifted operands are read
+  // in place at row offset kj*hw + ki (any 64-B row start is legal for the
+  // SW64 descriptor, tools/probe_shift.cu). A ring: `stages` x `stage_bytes`
+  // (kps halo tiles, a_tile bytes apart); B ring: hb_stages x hb_stage_bytes
+  // (one (kj, ki) filter box over the kps blocks) at hb_ring_off.
+  int halo, hw, hr, a_tile;
+  int hb_stages, hb_stage_bytes, hb_ring_off;
   int cb_group;                   // 1: a stage = kps channel blocks at one (kj, ki), one B box
                                   // spanning them; 0: kps consecutive k-steps, one box each
   int a_boxes;                    // A boxes per coordinate step: 1 (spans the step's blocks;
@@ -77,6 +87,7 @@ struct ConvParams {
   unsigned long long* trace;      // profiling only (PSCONV_DEBUG & 8): CTA 0 stage timestamps
 };
 constexpr int kTraceStages = 128;
+constexpr int kHaloB = 8;  // halo mode: B-ring barriers follow 8 A-ring slots
 
 // Shared-memory plan (per CTA, one CTA per SM): a ring of `stages` pipeline
 // stages inside kStageBudget, then two output staging blocks, then barriers.
@@ -152,6 +163,203 @@ __device__ __forceinline__ TileCoord decode_group(const ConvParams& p, int g, in
   return c;
 }
 
+// lo = x - trunc_tf32(x) over n4 float4s (128 splitter threads), loads batched
+// 4 deep for ILP
+__device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, int tid) {
+  for (int base = tid; base < n4; base += 512) {
+    float4 x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (base + i * 128 < n4) x[i] = a[base + i * 128];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (base + i * 128 < n4) {
+        float4 lo;
+        lo.x = x[i].x - __uint_as_float(__float_as_uint(x[i].x) & 0xFFFFE000u);
+        lo.y = x[i].y - __uint_as_float(__float_as_uint(x[i].y) & 0xFFFFE000u);
+        lo.z = x[i].z - __uint_as_float(__float_as_uint(x[i].z) & 0xFFFFE000u);
+        lo.w = x[i].w - __uint_as_float(__float_as_uint(x[i].w) & 0xFFFFE000u);
+        alo[base + i * 128] = lo;
+      }
+    }
+  }
+}
+
+// Halo-mode producer (warp 0; warp-uniform loop, one elected lane issues).
+// Per M tile and input-channel group: one halo box into the A ring, then one
+// filter box per (kj, ki) tap into the B ring.
+template <int BN, bool SPLIT3, bool PAIR>
+__device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem, uint64_t* full,
+                                              uint64_t* empty, int cluster, int nclusters, int rank,
+                                              bool leader, const CUtensorMap* tmap_in,
+                                              const CUtensorMap* tmap_flt, const CUtensorMap* tmap_flt_lo) {
+  using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+  constexpr int CS = Cfg::kCS;
+  const bool skip_a = (p.debug & 1) != 0;
+  const uint32_t a_tx = (skip_a ? 0u : static_cast<uint32_t>(p.kps * p.hr * p.hw * 64)) * CS;
+  const uint32_t b_tx = static_cast<uint32_t>(Cfg::kBBytes * p.kps * (SPLIT3 ? 2 : 1)) * CS;
+  const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
+  const int taps = p.R * p.S;
+  int as = 0, bs = 0, gs = 0;
+  uint32_t aph = 0, bph = 0;
+  for (int g = cluster; g < p.groups; g += nclusters) {
+    const TileCoord tc = decode_group(p, g, rank, CS);
+    const int hp = tc.tp * p.Pb - p.ph;
+    const int n0 = tc.tn;
+    const int k0 = tc.tk * BN + rank * Cfg::kBRows;
+    for (int cg = 0; cg < p.cbg; ++cg) {
+      const int cb = cg * p.kps;
+      ptx::mbar_wait(&empty[as], aph ^ 1);
+      if (ptx::elect_one()) {
+        uint8_t* sa = smem + as * p.stage_bytes;
+        if (!PAIR) {
+          ptx::mbar_expect_tx(&full[as], a_tx);
+          if (!skip_a) ptx::tma_load_5d(sa, tmap_in, &full[as], 0, -p.pw, hp, n0, cb);
+        } else {
+          if (leader) ptx::mbar_expect_tx(&full[as], a_tx);
+          if (!skip_a) ptx::tma_load_5d_cb(sa, tmap_in, full_leader + 8u * as, 0, -p.pw, hp, n0, cb);
+        }
+      }
+      __syncwarp();
+      if (++as == p.stages) {
+        as = 0;
+        aph ^= 1;
+      }
+      for (int t = 0; t < taps; ++t) {
+        const int bi = kHaloB + bs;
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        if (tr) p.trace[gs * 4 + 0] = clock64();
+        ptx::mbar_wait(&empty[bi], bph ^ 1);
+        if (tr) p.trace[gs * 4 + 1] = clock64();
+        if (ptx::elect_one()) {
+          uint8_t* sb = smem + p.hb_ring_off + bs * p.hb_stage_bytes;
+          if (!PAIR) {
+            ptx::mbar_expect_tx(&full[bi], b_tx);
+            ptx::tma_load_4d(sb, tmap_flt, &full[bi], 0, k0, t, cb >> p.b128);
+            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[bi], 0, k0, t, cb >> p.b128);
+          } else {
+            if (leader) ptx::mbar_expect_tx(&full[bi], b_tx);
+            ptx::tma_load_4d_cb(sb, tmap_flt, full_leader + 8u * bi, 0, k0, t, cb >> p.b128);
+          }
+        }
+        __syncwarp();
+        if (tr) p.trace[gs * 4 + 2] = clock64();
+        ++gs;
+        if (++bs == p.hb_stages) {
+          bs = 0;
+          bph ^= 1;
+        }
+      }
+    }
+  }
+}
+
+// Halo-mode MMA issuer (warp 1 of the single CTA / pair leader). Walks the same
+// (channel group, tap) sequence; accumulation chunks are counted in taps.
+template <int BN, bool SPLIT3, bool PAIR>
+__device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uint64_t* full,
+                                         uint64_t* split_full, uint64_t* empty, uint64_t* acc_full,
+                                         uint64_t* acc_empty, uint32_t tmem_base, int cluster,
+                                         int nclusters, uint32_t idesc) {
+  using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+  constexpr int kAccBufs = Cfg::kAccBufs;
+  const uint64_t adesc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
+  const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : adesc0;
+  const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);
+  const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
+  const uint32_t a_tile = static_cast<uint32_t>(p.a_tile) >> 4;
+  const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
+  const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
+  const int taps = p.R * p.S;
+  const int kps = p.kps;
+  const bool skip_mma = (p.debug & 2) != 0;
+  int as = 0, bs = 0, cit = 0, gs = 0;
+  uint32_t aph = 0, bph = 0;
+  for (int g = cluster; g < p.groups; g += nclusters) {
+    int tg = 0;  // tap index within the tile's reduction
+    int cc = 0;  // taps into the current accumulation chunk
+    int buf = 0;
+    uint32_t d_tmem = tmem_base;
+    for (int cg = 0; cg < p.cbg; ++cg) {
+      ptx::mbar_wait(&full[as], aph);  // PAIR: both CTAs' halos landed
+      if (SPLIT3) ptx::mbar_wait(&split_full[as], aph);
+      int r = 0, sx = 0;
+      for (int t = 0; t < taps; ++t, ++tg) {
+        const bool chunk_start = cc == 0;
+        const bool chunk_end = cc + 1 == p.chunk_stages || tg + 1 == p.nst;
+        if (chunk_start) {
+          buf = kAccBufs == 1 ? 0 : (cit & 1);
+          const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
+          if (PAIR)
+            ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
+          else
+            ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
+          d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+        }
+        const int bi = kHaloB + bs;
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
+        ptx::mbar_wait(&full[bi], bph);
+        ptx::tc_fence_after();
+        if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
+        if (ptx::elect_one()) {
+          uint64_t da = adesc0 + ((static_cast<uint32_t>(as * p.stage_bytes) +
+                                   static_cast<uint32_t>(r * p.hw + sx) * 64u) >> 4);
+          uint64_t db = bdesc0 + ((static_cast<uint32_t>(p.hb_ring_off + bs * p.hb_stage_bytes)) >> 4);
+          uint32_t acc_in = chunk_start ? 0u : 1u;
+          for (int j = 0; j < kps && !skip_mma; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (SPLIT3) {
+                ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, acc_in);
+                ptx::mma_tf32(d_tmem, da + h * 2, db + blo_off + h * 2, idesc, 1u);
+                ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, 1u);
+              } else if (PAIR) {
+                ptx::mma_tf32_pair(d_tmem, da + h * 2, db + h * 2, idesc, acc_in);
+              } else {
+                ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, acc_in);
+              }
+              acc_in = 1u;
+            }
+            da += a_tile;
+            db += (j & 1) ? b_odd : b_even;
+          }
+          if (PAIR) {
+            ptx::mma_commit_pair(&empty[bi]);
+            if (t == taps - 1) ptx::mma_commit_pair(&empty[as]);
+            if (chunk_end) ptx::mma_commit_pair(&acc_full[buf]);
+          } else {
+            ptx::mma_commit(&empty[bi]);
+            if (t == taps - 1) ptx::mma_commit(&empty[as]);
+            if (chunk_end) ptx::mma_commit(&acc_full[buf]);
+          }
+        }
+        __syncwarp();
+        if (tr) p.trace[4 * kTraceStages + gs * 4 + 2] = clock64();
+        ++gs;
+        if (chunk_end) {
+          ++cit;
+          cc = 0;
+        } else {
+          ++cc;
+        }
+        if (++sx == p.S) {
+          sx = 0;
+          ++r;
+        }
+        if (++bs == p.hb_stages) {
+          bs = 0;
+          bph ^= 1;
+        }
+      }
+      if (++as == p.stages) {
+        as = 0;
+        aph ^= 1;
+      }
+    }
+  }
+}
+
 template <int BN, bool SPLIT3, bool PAIR>
 __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
@@ -197,6 +405,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       ptx::mbar_init(&split_full[s], 128);
       ptx::mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < (p.halo ? p.hb_stages : 0); ++s) {  // halo B ring: barriers 8..
+      ptx::mbar_init(&full[kHaloB + s], 1);
+      ptx::mbar_init(&empty[kHaloB + s], 1);
+    }
     for (int a = 0; a < kAccBufs; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
       ptx::mbar_init(&acc_empty[a], 4 * CS);
@@ -230,6 +442,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       if (SPLIT3) ptx::prefetch_tmap(&tmap_flt_lo);
     }
     __syncwarp();
+    if (p.halo) {
+      halo_producer<BN, SPLIT3, PAIR>(p, smem, full, empty, cluster, nclusters, rank, leader,
+                                      &tmap_in, &tmap_flt, &tmap_flt_lo);
+    } else {
     // one box per operand per stage: A spans kps channel blocks (tensor map
     // dims [16c][W][H][img][Cb], so each block's rows land contiguously),
     // B spans the same kps blocks of the prepacked filter ([16c][K][R*S][Cb])
@@ -306,6 +522,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         }
       }
     }
+    }  // !halo
+  } else if (warp == 1 && leader && p.halo) {
+    halo_mma<BN, SPLIT3, PAIR>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
+                               cluster, nclusters, kIdesc);
   } else if (warp == 1 && leader) {
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues tcgen05.mma / commit.
@@ -408,8 +628,18 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const bool store_thread = threadIdx.x == 64;  // first epilogue thread issues TMA stores
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
-    const uint32_t row_off = static_cast<uint32_t>(row) * 64u;
-    const uint32_t row_swz = (static_cast<uint32_t>(row) >> 1) & 3u;  // SW64: chunk ^= bits[7:8]
+    // staged row of this lane: the tile row itself, or (halo) its pixel
+    // (pr, q) = (row / hw, row % hw) packed at pitch Q; junk lanes (q >= Q or
+    // pr >= Pb) stage nothing
+    int srow = row;
+    bool row_valid = true;
+    if (p.halo) {
+      const int pr = row / p.hw, q = row - pr * p.hw;
+      row_valid = q < p.Q && pr < p.Pb;
+      srow = pr * p.Q + q;
+    }
+    const uint32_t row_off = static_cast<uint32_t>(srow) * 64u;
+    const uint32_t row_swz = (static_cast<uint32_t>(srow) >> 1) & 3u;  // SW64: chunk ^= bits[7:8]
     int ostage = 0;                                                  // staging buffer toggle
     if (store_thread) ptx::prefetch_tmap(&tmap_out);
     int cit = 0;
@@ -456,11 +686,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               // staging buffer free? (the store issued two blocks ago has read it)
               if (store_thread) ptx::bulk_wait_read<1>();
               ptx::named_bar(1, 128);
+              if (row_valid) {
 #pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4) {
-                const int b = blk * 16 + 4 * c4;
-                const uint32_t off = row_off + ((static_cast<uint32_t>(c4) ^ row_swz) << 4);
-                *reinterpret_cast<uint4*>(st + off) = make_uint4(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
+                for (int c4 = 0; c4 < 4; ++c4) {
+                  const int b = blk * 16 + 4 * c4;
+                  const uint32_t off = row_off + ((static_cast<uint32_t>(c4) ^ row_swz) << 4);
+                  *reinterpret_cast<uint4*>(st + off) = make_uint4(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
+                }
               }
               ptx::fence_proxy_async_smem();
               ptx::named_bar(1, 128);
@@ -497,6 +729,22 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const int tid = threadIdx.x - 192;
     int stage = 0;
     uint32_t phase = 0;
+    if (p.halo) {
+      // one split per halo tile (kps blocks x hr*hw rows), reused by all R*S taps
+      const int n4 = (p.kps * p.a_tile) >> 4;
+      for (int g = cluster; g < p.groups; g += nclusters)
+        for (int cg = 0; cg < p.cbg; ++cg) {
+          ptx::mbar_wait(&full[stage], phase);
+          split_lo(reinterpret_cast<const float4*>(stage_base(stage)),
+                   reinterpret_cast<float4*>(stage_base(stage) + p.a_lo_off), n4, tid);
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&split_full[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+    } else
     for (int g = cluster; g < p.groups; g += nclusters) {
       for (int it = 0; it < nst; ++it) {
         ptx::mbar_wait(&full[stage], phase);
@@ -506,23 +754,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const float4* a = reinterpret_cast<const float4*>(stage_base(stage));
         float4* alo = reinterpret_cast<float4*>(stage_base(stage) + p.a_lo_off);
         const int n4 = (min(p.kps, p.ksteps - it * p.kps) * p.a_pitch) >> 4;
-        for (int base = tid; base < n4; base += 512) {
-          float4 x[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (base + i * 128 < n4) x[i] = a[base + i * 128];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (base + i * 128 < n4) {
-              float4 lo;
-              lo.x = x[i].x - __uint_as_float(__float_as_uint(x[i].x) & 0xFFFFE000u);
-              lo.y = x[i].y - __uint_as_float(__float_as_uint(x[i].y) & 0xFFFFE000u);
-              lo.z = x[i].z - __uint_as_float(__float_as_uint(x[i].z) & 0xFFFFE000u);
-              lo.w = x[i].w - __uint_as_float(__float_as_uint(x[i].w) & 0xFFFFE000u);
-              alo[base + i * 128] = lo;
-            }
-          }
-        }
+        split_lo(a, alo, n4, tid);
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);
         if (++stage == kStages) {

@@ -53,6 +53,7 @@ struct Recipe {
   int box_q = 0, box_p = 0, box_n = 0;                        // 0 = selector decides
   int stages = 0;                                             // informational
   int kg = 0;                                                 // k-steps per stage, 0 = auto
+  int halo = 0;                                               // 1: halo mode (stride-1 R x S)
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -69,7 +70,9 @@ struct Schedule {
   int chunk;           // k-steps per TMEM accumulation chunk (0 = whole reduction)
   int cs;              // CTAs per cluster sharing (multicasting) the filter block
   int kps;             // k-steps (input-channel blocks) per pipeline stage
-  int stages;          // pipeline stages in the shared-memory ring
+  int stages;          // pipeline stages in the shared-memory ring (halo: A ring)
+  int halo = 0;        // halo mode: Pb whole output rows, input halo loaded once per block
+  int hb_stages = 0;   // halo: B-ring stages
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;
@@ -84,6 +87,15 @@ constexpr int kSmemStageBudget = 227 * 1024 - 2 * 128 * 64 - 2048 - 1024;
 constexpr int kSmemMaxStages = 16;
 int stage_bytes(const Schedule& s, int mode);  // bytes of one stage of s.kps k-steps
 void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg);  // throws ConfigError
+
+// Halo-mode geometry (conv_kernel.cuh ConvParams::halo): padded row pitch hw,
+// halo rows hr, byte sizes of one A stage (kps halo tiles + junk-row slack,
+// A_lo mirror in 3xTF32) and one B stage (one tap over kps blocks).
+struct HaloGeom {
+  int hw, hr, a_tile, a_lo_off, a_stage, b_lo_off, b_stage;
+};
+bool halo_eligible(const conv_desc& d);
+HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode);
 
 // Closed-form model (select.cpp).
 struct ModelBreakdown {

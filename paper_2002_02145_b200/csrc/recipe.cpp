@@ -100,6 +100,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
           if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
+        } else if (key == "halo") {
+          r.halo = static_cast<int>(parse_int(val, "gpu halo"));
+          if (r.halo != 0 && r.halo != 1) throw ConfigError("gpu halo must be 0 or 1");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -127,6 +130,7 @@ std::string Recipe::id() const {
     s += ";gpu=bn:" + std::to_string(bn) + ",box:" + std::to_string(box_q) + "x" +
          std::to_string(box_p) + "x" + std::to_string(box_n);
     if (cs) s += ",cl:" + std::to_string(cs);
+    if (halo) s += ",halo:1";
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -250,7 +254,17 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
 
   int fix_p = tile_of.count("oj") ? static_cast<int>(std::min<int64_t>(tile_of["oj"], d.ofh)) : 0;
   int fix_n = tile_of.count("img") ? static_cast<int>(std::min<int64_t>(tile_of["img"], d.nImg)) : 0;
-  if (r.box_q || r.box_p || r.box_n) {
+  if (r.halo) {
+    // halo mode: whole output rows of one image at the padded pitch hw
+    if (!halo_eligible(d))
+      throw ConfigError("GPU tile: halo mode needs stride 1, a filter larger than 1x1 and ofw + kw - 1 <= 128");
+    const int hw = static_cast<int>(d.ofw + d.kw - 1);
+    s.qb = static_cast<int>(d.ofw);
+    s.pb = static_cast<int>(std::min<int64_t>(128 / hw, d.ofh));
+    if (fix_p) s.pb = std::min(s.pb, fix_p);
+    s.nb = 1;
+    s.halo = 1;
+  } else if (r.box_q || r.box_p || r.box_n) {
     s.qb = r.box_q;
     s.pb = r.box_p;
     s.nb = r.box_n;
@@ -272,6 +286,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.box_q = s.qb;
   canon.box_p = s.pb;
   canon.box_n = s.nb;
+  canon.halo = s.halo;
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
@@ -305,8 +320,48 @@ int stage_bytes(const Schedule& s, int mode) {
 // whole 8-row swizzle atoms); otherwise kps consecutive k-steps of the
 // reduction order with one box each (e.g. the stem, Cb = 1). Auto: the largest
 // of {4, 2} that keeps >= 3 stages in the ring, preferring divisors of Cb.
+bool halo_eligible(const conv_desc& d) {
+  return d.stride_h == 1 && d.stride_w == 1 && d.kh * d.kw > 1 && d.ofw + d.kw - 1 <= 128 &&
+         d.ofh + d.kh - 1 <= 256;
+}
+
+HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode) {
+  HaloGeom h{};
+  const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
+  h.hw = static_cast<int>(d.ofw + d.kw - 1);
+  h.hr = s.pb + static_cast<int>(d.kh) - 1;
+  h.a_tile = h.hr * h.hw * 64;
+  // the last block's shifted operands read up to (kh-1)*hw + kw-1 + 127 rows in
+  const int rows = (s.kps - 1) * h.hr * h.hw + static_cast<int>(d.kh - 1) * h.hw +
+                   static_cast<int>(d.kw - 1) + 128;
+  h.a_lo_off = (rows * 64 + 1023) / 1024 * 1024;
+  h.a_stage = h.a_lo_off * mult;
+  h.b_lo_off = s.kps * (s.bn / s.cs) * 64;
+  h.b_stage = h.b_lo_off * mult;
+  return h;
+}
+
 void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   const int Cb = static_cast<int>(d.nIfm / 16);
+  if (s.halo) {
+    // A ring of 2 halo stages, the rest B stages (<= 8 each); largest kps in
+    // {4, 2, 1} dividing Cb that leaves >= 3 B stages
+    for (int k : {4, 2, 1}) {
+      if (kg && k != kg) continue;
+      if (Cb % k) continue;
+      Schedule t = s;
+      t.kps = k;
+      const HaloGeom h = halo_geom(d, t, mode);
+      const int hb = std::min(8, (kSmemStageBudget - 2 * h.a_stage) / h.b_stage);
+      if (hb >= 3 || (k == 1 && hb >= 2) || (kg && hb >= 2)) {
+        s.kps = k;
+        s.stages = 2;
+        s.hb_stages = hb;
+        return;
+      }
+    }
+    throw ConfigError("GPU tile: halo tile does not fit in shared memory");
+  }
   const int ksteps = static_cast<int>(Cb * d.kh * d.kw);
   auto ring = [&](int k) {
     Schedule t = s;

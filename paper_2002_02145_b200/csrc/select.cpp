@@ -43,6 +43,7 @@ struct Machine {
   double port_bytes_per_cycle = 110.0;  // ~0.85 x 128 B/cycle L2->SMEM per SM
   double kstep_sync_cyc = 30.0;  // mbarrier round trips per k-step
   double drain_round_trip_cyc = 100.0;  // one 32-column TMEM drain step
+  double row_requests_per_cycle = 0.75;  // TMA rows per cycle per SM, all SMs loading
 };
 const Machine kB200{};
 
@@ -117,15 +118,24 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const double b_rows = double(s.bn) / cs;
   const double deliver_b = a_box + b_rows * 64.0 * (mult > 1 ? 2 : 1);
   const double mma_cyc = s.bn * mult;
-  const double del_cyc = deliver_b / m.port_bytes_per_cycle;
+  // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows
+  // per cycle per SM with every SM loading, for 64-B and 128-B rows alike
+  // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows
+  // are 128 B when a stage pairs channel blocks (b128), halving their count.
+  const bool b128 = s.kps % 2 == 0 && g.Cb % std::max(1, s.kps) == 0;
+  const double rows = double(s.qb) * s.pb * s.nb + b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0);
+  const double del_cyc = rows / m.row_requests_per_cycle;
   const double tc_reads = 2.0 * mult * (4096.0 + b_rows * 32.0);
   // (the splitter's LSU traffic only partly competes with the async-proxy traffic)
   const double smem_cyc = 0.94 * (tc_reads + deliver_b + (mult > 1 ? 4096.0 : 0.0)) / 128.0;
   const double busy = std::max(mma_cyc, smem_cyc);
   const double other = std::min(mma_cyc, smem_cyc);
   double kstep_cyc = busy * std::pow(1.0 + std::pow(other / busy, 4.0), 0.25);
-  // + TMA descriptor traversal: one request per contiguous pixel run of the box
-  kstep_cyc = std::max(kstep_cyc, del_cyc) + m.kstep_sync_cyc + 0.5 * s.pb * s.nb;
+  // + per-stage issue cost (barrier round trip, TMA issue ~45 cycles each, MMA
+  // commit) amortised over the stage's kps k-steps
+  const double boxes = s.kps > 1 && g.Cb % s.kps == 0 ? 2.0 : 2.0 * std::max(1, s.kps);
+  const double stage_cyc = m.kstep_sync_cyc * 4 + 45.0 * boxes;
+  kstep_cyc = std::max(kstep_cyc, del_cyc) + stage_cyc / std::max(1, s.kps);
   const int chunk = s.chunk > 0 ? s.chunk : static_cast<int>(ksteps);
   const double nchunks = std::ceil(double(ksteps) / chunk);
   // 3xTF32 chunk drain: tcgen05.ld acc + sum, fadd, tcgen05.st, 32 columns per

@@ -111,6 +111,30 @@ def test_stage_geometry(conv, c_log, recipe, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,halo:1"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:32,halo:1,kg:1"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,halo:1,kg:2"),
+    ("conv:2,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,halo:1"),
+    ("conv:4,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, "gpu=bn:256,halo:1"),
+    ("conv:4,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, "gpu=bn:128,halo:1"),
+    # ragged last row block (21 = 3*6 + 3), non-square, Cb = 3
+    ("conv:2,32,48,21,19,3,3,1,1,16,1,1,21,19", 48, "gpu=bn:32,halo:1"),
+    # 5x5 / pad 2, and an unpadded ("valid") 3x3
+    ("conv:2,32,32,12,12,5,5,1,1,16,2,2,12,12", 32, "gpu=bn:32,halo:1"),
+    ("conv:2,32,32,10,10,3,3,1,1,16,0,0,12,12", 32, "gpu=bn:32,halo:1"),
+])
+def test_halo_mode(conv, c_log, recipe, mode):
+    """Halo mode: whole output rows at the padded pitch, the input halo loaded once per
+    channel block and the R*S shifted operands addressed in place."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("halo", conv, c_log, 9, mode, n, recipe + (",cl:1" if mode == "tf32" else ""))
+    if mode == "tf32":
+        _check("halo-pair", conv, c_log, 9, mode, n, recipe + ",cl:2")
+
+
+@pytest.mark.gpu
 def test_image_range_and_accumulate():
     """conv_fwd on [img_begin, img_begin+count) touches only those images; FLAG_ACCUMULATE
     reproduces the reference body's `+=` (presets.hpp:112)."""

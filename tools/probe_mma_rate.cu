@@ -1,0 +1,81 @@
+// Probe: tcgen05.mma kind::tf32 issue / execution rate from one thread
+// (M=128, K=8, N = 64 / 128 / 256), operands in SWIZZLE_64B shared memory.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2002_02145_b200/csrc \
+//        tools/probe_mma_rate.cu -o tools/probe_mma_rate
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "sm100_ptx.cuh"
+using namespace psconv;
+
+template <int N, int UNROLL>
+__global__ void k_rate(int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < (64 * 1024) / 4; i += blockDim.x) ((float*)sm)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc(&slot, 256);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = ptx::idesc_tf32_m128<N>();
+    const uint64_t da = ptx::smem_desc_sw64(ptx::smem_u32(sm), 16, 512);
+    const uint64_t db = ptx::smem_desc_sw64(ptx::smem_u32(sm + 8192), 16, 512);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        ptx::mma_tf32(tmem, da + 2 * (u & 1), db + 2 * (u & 1), idesc, 1u);
+    }
+    long long t1 = clock64();
+    ptx::mma_commit(&bar);
+    ptx::mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    if (blockIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
+  }
+}
+
+template <int N, int U>
+void run(int grid) {
+  long long* out;
+  cudaMalloc(&out, 16);
+  cudaFuncSetAttribute(k_rate<N, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  const int iters = 256 / U;
+  k_rate<N, U><<<grid, 128, 80 * 1024>>>(iters, out);
+  k_rate<N, U><<<grid, 128, 80 * 1024>>>(iters, out);
+  long long h[2];
+  cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+  printf("grid %3d N=%3d unroll %d: issue %6.1f cyc/mma, complete %6.1f cyc/mma (ideal %d at 4096 flop/cyc)\n",
+         grid, N, U, double(h[0]) / 256, double(h[1]) / 256, 128 * N * 8 * 2 / 4096);
+  cudaFree(out);
+}
+
+int main() {
+  for (int grid : {1, 148}) {
+    run<64, 1>(grid);
+    run<64, 8>(grid);
+    run<128, 8>(grid);
+    run<256, 8>(grid);
+  }
+  printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
