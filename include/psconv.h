@@ -117,6 +117,19 @@ const char* conv_plan_recipe(const conv_plan* p);
 int conv_fwd(const conv_plan* p, const float* in, const float* flt, float* out, int64_t img_begin,
              int64_t img_count, void* cuda_stream, unsigned flags);
 
+/* conv_fwd on HOST buffers (the reference's emitted driver computes on host
+ * arrays, emit.hpp:60-134 / tests/golden/conv_identity.c): h_in / h_flt /
+ * h_out are host pointers in the same layouts as conv_fwd (pinned memory gives
+ * full copy/compute overlap). The image range is streamed through the device
+ * in ~32 MB chunks, double buffered: the copy-in of chunk i+1, the kernel of
+ * chunk i and the copy-out of chunk i-1 overlap on two plan-owned copy streams
+ * and `cuda_stream`. Stream-ordered like conv_fwd: starts after prior work on
+ * cuda_stream; h_out is complete when cuda_stream reaches this point. The plan
+ * allocates its staging buffers on first use (released by conv_plan_destroy).
+ * Returns 0 / 1 / 2. */
+int conv_fwd_host(const conv_plan* p, const float* h_in, const float* h_flt, float* h_out,
+                  int64_t img_begin, int64_t img_count, void* cuda_stream, unsigned flags);
+
 /* Repacks a filter into the plan once (weights held constant, e.g. inference);
  * later conv_fwd calls with PSCONV_FLAG_PREPACKED skip the repack launch. */
 int conv_plan_prepack(conv_plan* p, const float* flt, void* cuda_stream);

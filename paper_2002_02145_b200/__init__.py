@@ -143,7 +143,11 @@ def _stream_ptr(stream) -> int:
 
 
 def _ptr(t) -> int:
-    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if hasattr(t, "ctypes"):  # numpy array (host buffers for forward_host)
+        return t.ctypes.data
+    return int(t)
 
 
 class ConvPlan:
@@ -192,6 +196,17 @@ class ConvPlan:
                             img_begin, img_count, _stream_ptr(stream), flags))
 
     __call__ = forward
+
+    def forward_host(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
+                     stream=None, accumulate: bool = False, prepacked: bool = False) -> None:
+        """conv on HOST buffers (CPU tensors / numpy arrays; pinned for full overlap): the
+        image range is streamed through the device in double-buffered chunks (C ABI
+        conv_fwd_host). Stream-ordered: `out` is complete once `stream` reaches this call."""
+        if img_count is None:
+            img_count = self.preset.nImg - img_begin
+        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_PREPACKED if prepacked else 0)
+        _check(lib.conv_fwd_host(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
+                                 img_begin, img_count, _stream_ptr(stream), flags))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -45,6 +45,7 @@ _sigs = {
     "conv_plan_destroy": (None, [c_vp]),
     "conv_plan_recipe": (ctypes.c_char_p, [c_vp]),
     "conv_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
+    "conv_fwd_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
     "conv_plan_launches": (ctypes.c_int, [c_vp]),
     "conv_plan_prepack": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "conv_plan_emit": (c_i64, [c_vp, ctypes.c_char_p, ctypes.c_size_t]),
@@ -63,6 +64,8 @@ _sigs = {
     "psconv_device_sm_count": (ctypes.c_int, [ctypes.c_int]),
 }
 for _name, (_res, _args) in _sigs.items():
+    if "PSCONV_LIB_NAME" in os.environ and not hasattr(lib, _name):
+        continue  # older A/B build (tools only)
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args

@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -29,6 +30,18 @@ struct conv_plan {
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
+  // conv_fwd_host staging (lazily created): double-buffered device chunks,
+  // copy-in / copy-out streams and their events
+  struct HostPipe {
+    int64_t chunk = 0;                 // images per chunk
+    float* din[2] = {nullptr, nullptr};
+    float* dout[2] = {nullptr, nullptr};
+    float* dflt = nullptr;
+    cudaStream_t sin = nullptr, sout = nullptr;
+    cudaEvent_t start = nullptr, flt = nullptr, end = nullptr;
+    cudaEvent_t h2d[2] = {nullptr, nullptr}, conv[2] = {nullptr, nullptr}, d2h[2] = {nullptr, nullptr};
+  };
+  mutable HostPipe* pipe = nullptr;
 };
 
 namespace psconv {
@@ -252,7 +265,10 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = CS > 1 ? 1 : 0;  // plain launch for single-CTA clusters
+    static const int force_cl = std::getenv("PSCONV_CL_ATTR") ? std::atoi(std::getenv("PSCONV_CL_ATTR")) : -1;
+    cfg.numAttrs = force_cl >= 0 ? force_cl : (CS > 1 ? 1 : 0);
+    static const bool full_smem = std::getenv("PSCONV_FULL_SMEM") != nullptr;
+    if (full_smem) cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
   }
 }
@@ -277,6 +293,189 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
     case 1: return dispatch_bn<SPLIT3, 1>(bn, P, prm, a, b, blo, o, st);
     case 2: return dispatch_bn<SPLIT3, 2>(bn, P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported cluster size");
+  }
+}
+
+// Launches the plan on images [0, img_count) of `in` / `out` (already offset to
+// the first image). Validation is the caller's (conv_fwd / conv_fwd_host).
+void launch_range(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
+                  cudaStream_t st, unsigned flags) {
+  const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
+  const conv_desc& d = P->d;
+  const Schedule& s = P->sched;
+  const int Cb = int(d.nIfm / 16), Kb = int(d.nOfm / 16);
+  const int H = int(d.ifh), W = int(d.ifw), R = int(d.kh), S = int(d.kw);
+  const int Pp = int(d.ofh), Q = int(d.ofw);
+  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+
+  // A: input viewed as [img_count][Cb][H][W][16] from the range's first image
+  CUtensorMap ta, tb, tblo, tout;
+  // output viewed as [img_count][Kb][P][Q][16] from the first image; the box is
+  // the pixel tile (no stride factor); stores outside the layer are clipped
+  {
+    const float* base = out;
+    const cuuint64_t dims[5] = {16, cuuint64_t(Q), cuuint64_t(Pp), cuuint64_t(Kb),
+                                cuuint64_t(img_count)};
+    const cuuint64_t strides[4] = {64, cuuint64_t(Q) * 64, cuuint64_t(Pp) * Q * 64,
+                                   cuuint64_t(Kb) * Pp * Q * 64};
+    const cuuint32_t box[5] = {16, cuuint32_t(s.qb), cuuint32_t(s.pb), 1, cuuint32_t(s.nb)};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    encode(&tout, base, 5, dims, strides, box, estr);
+  }
+  const int rows = s.qb * s.pb * s.nb;
+  const bool a_packed = rows % 8 == 0;
+  const bool a_group = Cb % s.kps == 0 && a_packed;  // one A box spans the stage's blocks
+  // A: input NCHW16c [img_count][Cb][H][W][16] viewed with its dims ordered
+  // [16c][W][H][img][Cb] (TMA dims need not follow memory order): the box
+  // [16][Qb*sw][Pb*sh][Nb][kps] lands as kps contiguous 128-row tiles, one per
+  // input-channel block of the stage.
+  {
+    const float* base = in;
+    const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(img_count),
+                                cuuint64_t(Cb)};
+    const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
+                                   cuuint64_t(H) * W * 64};
+    if (s.halo) {  // halo box: hr padded rows of hw pixels, kps blocks
+      const HaloGeom h = halo_geom(d, s, P->mode);
+      const cuuint32_t box[5] = {16, cuuint32_t(h.hw), cuuint32_t(h.hr), 1, cuuint32_t(s.kps)};
+      const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+      encode(&ta, base, 5, dims, strides, box, estr);
+    } else {
+      const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
+                                 cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
+      const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
+      encode(&ta, base, 5, dims, strides, box, estr);
+    }
+  }
+  // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
+  const int K = Kb * 16;
+  const float* b_hi = P->flt_pack;
+  const float* b_lo = split3 ? P->flt_pack + P->flt_elems : P->flt_pack;
+  if (!prepacked) {
+    launch_prepack(P, flt, st);
+    P->prepacked = false;  // buffer now holds this call's filter
+  }
+  // B viewed as [16c][K][R*S][Cb] (b128: [32c][K][R*S][Cb/2]); box {c, rows, 1, blocks}
+  if (P->b128) {
+    const cuuint64_t dims[4] = {32, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
+    const cuuint64_t strides[3] = {128, cuuint64_t(K) * 128, cuuint64_t(K) * 128 * R * S};
+    const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps / 2)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    encode(&tb, b_hi, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+    encode(&tblo, b_lo, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
+    const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
+    const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    encode(&tb, b_hi, 4, dims, strides, box, estr);
+    encode(&tblo, b_lo, 4, dims, strides, box, estr);
+  }
+  ConvParams prm{};
+  prm.img_count = int(img_count);
+  prm.Cb = Cb;
+  prm.H = H;
+  prm.W = W;
+  prm.Kb = Kb;
+  prm.P = Pp;
+  prm.Q = Q;
+  prm.R = R;
+  prm.S = S;
+  prm.sh = int(d.stride_h);
+  prm.sw = int(d.stride_w);
+  prm.ph = int(d.pad_h);
+  prm.pw = int(d.pad_w);
+  prm.Qb = s.qb;
+  prm.Pb = s.pb;
+  prm.Nb = s.nb;
+  prm.tiles_q = (Q + s.qb - 1) / s.qb;
+  prm.tiles_p = (Pp + s.pb - 1) / s.pb;
+  prm.tiles_n = int((img_count + s.nb - 1) / s.nb);
+  prm.tiles_k = int(d.nOfm / s.bn);
+  const int64_t mt = int64_t(prm.tiles_q) * prm.tiles_p * prm.tiles_n;
+  const int64_t mg = (mt + s.cs - 1) / s.cs;
+  if (mg * prm.tiles_k >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
+  prm.mtiles = int(mt);
+  prm.mgroups = int(mg);
+  prm.groups = int(mg * prm.tiles_k);
+  // recipe loop order -> rasterisation: pixel-loop order and ofm_tile position
+  int pos[3];
+  for (int i = 0; i < 3; ++i) pos[s.raster[i]] = i;
+  prm.m_order = pos[0] < pos[2] ? 0 : 1;
+  prm.k_outer = pos[1] == 0 ? 1 : 0;
+  prm.ksteps = Cb * R * S;
+  prm.kps = s.kps;
+  prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
+  prm.b128 = P->b128 ? 1 : 0;
+  prm.cbg = prm.cb_group ? Cb / s.kps : Cb;
+  prm.nst = (prm.ksteps + s.kps - 1) / s.kps;
+  prm.stages = s.stages;
+  {
+    const int mult = split3 ? 2 : 1;
+    const int brows = s.bn / s.cs;
+    prm.stage_bytes = stage_bytes(s, P->mode);
+    // one A box for the stage's channel blocks when its rows are whole 8-row
+    // swizzle atoms; else one box per block at 8 KB pitch
+    prm.a_boxes = (prm.cb_group && a_packed) ? 1 : (prm.cb_group ? s.kps : 1);
+    prm.a_pitch = (prm.cb_group && a_packed) ? rows * 64 : 8192;
+    prm.a_lo_off = s.kps * 8192;
+    prm.b_off = s.kps * 8192 * mult;
+    prm.b_lo_off = prm.b_off + s.kps * brows * 64;
+    prm.ring_bytes = (prm.stages * prm.stage_bytes + 1023) / 1024 * 1024;
+    if (s.halo) {
+      const HaloGeom h = halo_geom(d, s, P->mode);
+      prm.halo = 1;
+      prm.hw = h.hw;
+      prm.hr = h.hr;
+      prm.a_tile = h.a_tile;
+      prm.stage_bytes = h.a_stage;
+      prm.a_lo_off = h.a_lo_off;
+      prm.hb_stages = s.hb_stages;
+      prm.hb_stage_bytes = h.b_stage;
+      prm.b_lo_off = h.b_lo_off;
+      prm.hb_ring_off = prm.stages * h.a_stage;
+      prm.ring_bytes = prm.hb_ring_off + prm.hb_stages * h.b_stage;
+      prm.nst = prm.cbg * R * S;  // taps per tile (B stages)
+      if (prm.stages > kHaloB || prm.hb_stages < 2 || prm.hb_stages > kMaxStages - kHaloB)
+        throw RuntimeError("internal: bad halo stage plan");
+    }
+    if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)
+      throw RuntimeError("internal: bad pipeline stage plan");
+  }
+  const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
+  prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
+  for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
+  prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
+  // profiling switch (never set in production; results are wrong when non-zero)
+  static const int debug_env = [] {
+    const char* e = std::getenv("PSCONV_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  prm.debug = debug_env;
+  static unsigned long long* trace_buf = nullptr;
+  if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, (8 * kTraceStages + 8) * 8));
+  prm.debug = debug_env & 7;
+  prm.trace = (debug_env & 8) ? trace_buf : nullptr;
+  prm.out = out;
+  prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
+  if (split3)
+    dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
+  else
+    dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
+  if (prm.trace) {  // profiling: dump CTA 0's per-stage clocks (producer | MMA issuer)
+    unsigned long long h[8 * kTraceStages + 8];
+    CUDA_OK(cudaStreamSynchronize(st));
+    CUDA_OK(cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = h[8 * kTraceStages];
+    std::fprintf(stderr, "events: setup %lld first-acc %lld last-store %lld stores-done %lld exit %lld\n",
+                 (long long)(h[8 * kTraceStages + 1] - t0), (long long)(h[8 * kTraceStages + 4] - t0),
+                 (long long)(h[8 * kTraceStages + 5] - t0), (long long)(h[8 * kTraceStages + 6] - t0),
+                 (long long)(h[8 * kTraceStages + 7] - t0));
+    for (int i = 0; i < kTraceStages; ++i)
+      std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld\n", i,
+                   (long long)(h[i * 4] - t0), (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
+                   (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
+                   (long long)(h[4 * kTraceStages + i * 4 + 2] - t0));
   }
 }
 
@@ -354,6 +553,27 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
 
 void conv_plan_destroy(conv_plan* p) {
   if (!p) return;
+  if (p->pipe) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    auto* h = p->pipe;
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(h->din[i]);
+      cudaFree(h->dout[i]);
+      cudaEventDestroy(h->h2d[i]);
+      cudaEventDestroy(h->conv[i]);
+      cudaEventDestroy(h->d2h[i]);
+    }
+    cudaFree(h->dflt);
+    cudaEventDestroy(h->start);
+    cudaEventDestroy(h->flt);
+    cudaEventDestroy(h->end);
+    if (h->sin) cudaStreamDestroy(h->sin);
+    if (h->sout) cudaStreamDestroy(h->sout);
+    delete h;
+    cudaSetDevice(prev);
+  }
   if (p->flt_pack) {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -402,183 +622,9 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
          reinterpret_cast<uintptr_t>(out)) & 15)
       throw ConfigError("tensor pointers must be 16-byte aligned");
     if (img_count == 0) return;
-    const Schedule& s = P->sched;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int Cb = int(d.nIfm / 16), Kb = int(d.nOfm / 16);
-    const int H = int(d.ifh), W = int(d.ifw), R = int(d.kh), S = int(d.kw);
-    const int Pp = int(d.ofh), Q = int(d.ofw);
-    const bool split3 = P->mode == PSCONV_MODE_3XTF32;
-
-    // A: input viewed as [img_count][Cb][H][W][16], starting at img_begin
-    CUtensorMap ta, tb, tblo, tout;
-    // output viewed as [img_count][Kb][P][Q][16] starting at img_begin; the box is
-    // the pixel tile (no stride factor); stores outside the layer are clipped
-    {
-      const float* base = out + img_begin * int64_t(Kb) * Pp * Q * 16;
-      const cuuint64_t dims[5] = {16, cuuint64_t(Q), cuuint64_t(Pp), cuuint64_t(Kb),
-                                  cuuint64_t(img_count)};
-      const cuuint64_t strides[4] = {64, cuuint64_t(Q) * 64, cuuint64_t(Pp) * Q * 64,
-                                     cuuint64_t(Kb) * Pp * Q * 64};
-      const cuuint32_t box[5] = {16, cuuint32_t(s.qb), cuuint32_t(s.pb), 1, cuuint32_t(s.nb)};
-      const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-      encode(&tout, base, 5, dims, strides, box, estr);
-    }
-    const int rows = s.qb * s.pb * s.nb;
-    const bool a_packed = rows % 8 == 0;
-    const bool a_group = Cb % s.kps == 0 && a_packed;  // one A box spans the stage's blocks
-    // A: input NCHW16c [img_count][Cb][H][W][16] viewed with its dims ordered
-    // [16c][W][H][img][Cb] (TMA dims need not follow memory order): the box
-    // [16][Qb*sw][Pb*sh][Nb][kps] lands as kps contiguous 128-row tiles, one per
-    // input-channel block of the stage.
-    {
-      const float* base = in + img_begin * int64_t(Cb) * H * W * 16;
-      const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(img_count),
-                                  cuuint64_t(Cb)};
-      const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
-                                     cuuint64_t(H) * W * 64};
-      if (s.halo) {  // halo box: hr padded rows of hw pixels, kps blocks
-        const HaloGeom h = halo_geom(d, s, P->mode);
-        const cuuint32_t box[5] = {16, cuuint32_t(h.hw), cuuint32_t(h.hr), 1, cuuint32_t(s.kps)};
-        const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-        encode(&ta, base, 5, dims, strides, box, estr);
-      } else {
-        const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
-                                   cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
-        const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
-        encode(&ta, base, 5, dims, strides, box, estr);
-      }
-    }
-    // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
-    const int CRS = Cb * R * S;
-    const int K = Kb * 16;
-    const float* b_hi = P->flt_pack;
-    const float* b_lo = split3 ? P->flt_pack + P->flt_elems : P->flt_pack;
-    if (!prepacked) {
-      launch_prepack(P, flt, st);
-      P->prepacked = false;  // buffer now holds this call's filter
-    }
-    // B viewed as [16c][K][R*S][Cb] (b128: [32c][K][R*S][Cb/2]); box {c, rows, 1, blocks}
-    if (P->b128) {
-      const cuuint64_t dims[4] = {32, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
-      const cuuint64_t strides[3] = {128, cuuint64_t(K) * 128, cuuint64_t(K) * 128 * R * S};
-      const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps / 2)};
-      const cuuint32_t estr[4] = {1, 1, 1, 1};
-      encode(&tb, b_hi, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
-      encode(&tblo, b_lo, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
-    } else {
-      const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
-      const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
-      const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
-      const cuuint32_t estr[4] = {1, 1, 1, 1};
-      encode(&tb, b_hi, 4, dims, strides, box, estr);
-      encode(&tblo, b_lo, 4, dims, strides, box, estr);
-    }
-    ConvParams prm{};
-    prm.img_count = int(img_count);
-    prm.Cb = Cb;
-    prm.H = H;
-    prm.W = W;
-    prm.Kb = Kb;
-    prm.P = Pp;
-    prm.Q = Q;
-    prm.R = R;
-    prm.S = S;
-    prm.sh = int(d.stride_h);
-    prm.sw = int(d.stride_w);
-    prm.ph = int(d.pad_h);
-    prm.pw = int(d.pad_w);
-    prm.Qb = s.qb;
-    prm.Pb = s.pb;
-    prm.Nb = s.nb;
-    prm.tiles_q = (Q + s.qb - 1) / s.qb;
-    prm.tiles_p = (Pp + s.pb - 1) / s.pb;
-    prm.tiles_n = int((img_count + s.nb - 1) / s.nb);
-    prm.tiles_k = int(d.nOfm / s.bn);
-    const int64_t mt = int64_t(prm.tiles_q) * prm.tiles_p * prm.tiles_n;
-    const int64_t mg = (mt + s.cs - 1) / s.cs;
-    if (mg * prm.tiles_k >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
-    prm.mtiles = int(mt);
-    prm.mgroups = int(mg);
-    prm.groups = int(mg * prm.tiles_k);
-    // recipe loop order -> rasterisation: pixel-loop order and ofm_tile position
-    int pos[3];
-    for (int i = 0; i < 3; ++i) pos[s.raster[i]] = i;
-    prm.m_order = pos[0] < pos[2] ? 0 : 1;
-    prm.k_outer = pos[1] == 0 ? 1 : 0;
-    prm.ksteps = Cb * R * S;
-    prm.kps = s.kps;
-    prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
-    prm.b128 = P->b128 ? 1 : 0;
-    prm.cbg = prm.cb_group ? Cb / s.kps : Cb;
-    prm.nst = (prm.ksteps + s.kps - 1) / s.kps;
-    prm.stages = s.stages;
-    {
-      const int mult = split3 ? 2 : 1;
-      const int brows = s.bn / s.cs;
-      prm.stage_bytes = stage_bytes(s, P->mode);
-      // one A box for the stage's channel blocks when its rows are whole 8-row
-      // swizzle atoms; else one box per block at 8 KB pitch
-      prm.a_boxes = (prm.cb_group && a_packed) ? 1 : (prm.cb_group ? s.kps : 1);
-      prm.a_pitch = (prm.cb_group && a_packed) ? rows * 64 : 8192;
-      prm.a_lo_off = s.kps * 8192;
-      prm.b_off = s.kps * 8192 * mult;
-      prm.b_lo_off = prm.b_off + s.kps * brows * 64;
-      prm.ring_bytes = (prm.stages * prm.stage_bytes + 1023) / 1024 * 1024;
-      if (s.halo) {
-        const HaloGeom h = halo_geom(d, s, P->mode);
-        prm.halo = 1;
-        prm.hw = h.hw;
-        prm.hr = h.hr;
-        prm.a_tile = h.a_tile;
-        prm.stage_bytes = h.a_stage;
-        prm.a_lo_off = h.a_lo_off;
-        prm.hb_stages = s.hb_stages;
-        prm.hb_stage_bytes = h.b_stage;
-        prm.b_lo_off = h.b_lo_off;
-        prm.hb_ring_off = prm.stages * h.a_stage;
-        prm.ring_bytes = prm.hb_ring_off + prm.hb_stages * h.b_stage;
-        prm.nst = prm.cbg * R * S;  // taps per tile (B stages)
-        if (prm.stages > kHaloB || prm.hb_stages < 2 || prm.hb_stages > kMaxStages - kHaloB)
-          throw RuntimeError("internal: bad halo stage plan");
-      }
-      if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)
-        throw RuntimeError("internal: bad pipeline stage plan");
-    }
-    const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
-    prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
-    for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
-    prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
-    // profiling switch (never set in production; results are wrong when non-zero)
-    static const int debug_env = [] {
-      const char* e = std::getenv("PSCONV_DEBUG");
-      return e ? std::atoi(e) : 0;
-    }();
-    prm.debug = debug_env;
-    static unsigned long long* trace_buf = nullptr;
-    if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, (8 * kTraceStages + 8) * 8));
-    prm.debug = debug_env & 7;
-    prm.trace = (debug_env & 8) ? trace_buf : nullptr;
-    prm.out = out + img_begin * int64_t(Kb) * Pp * Q * 16;
-    prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
-    if (split3)
-      dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
-    else
-      dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
-    if (prm.trace) {  // profiling: dump CTA 0's per-stage clocks (producer | MMA issuer)
-      unsigned long long h[8 * kTraceStages + 8];
-      CUDA_OK(cudaStreamSynchronize(st));
-      CUDA_OK(cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost));
-      const unsigned long long t0 = h[8 * kTraceStages];
-      std::fprintf(stderr, "events: setup %lld first-acc %lld last-store %lld stores-done %lld exit %lld\n",
-                   (long long)(h[8 * kTraceStages + 1] - t0), (long long)(h[8 * kTraceStages + 4] - t0),
-                   (long long)(h[8 * kTraceStages + 5] - t0), (long long)(h[8 * kTraceStages + 6] - t0),
-                   (long long)(h[8 * kTraceStages + 7] - t0));
-      for (int i = 0; i < kTraceStages; ++i)
-        std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld\n", i,
-                     (long long)(h[i * 4] - t0), (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
-                     (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
-                     (long long)(h[4 * kTraceStages + i * 4 + 2] - t0));
-    }
+    const int64_t in_img = d.nIfm * d.ifh * d.ifw, out_img = d.nOfm * d.ofh * d.ofw;
+    launch_range(P, in + img_begin * in_img, flt, out + img_begin * out_img, img_count,
+                 static_cast<cudaStream_t>(stream), flags);
   });
 }
 
@@ -588,6 +634,83 @@ int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
     if (reinterpret_cast<uintptr_t>(flt) & 15) throw ConfigError("filter must be 16-byte aligned");
     launch_prepack(P, flt, static_cast<cudaStream_t>(stream));
     P->prepacked = true;
+  });
+}
+
+int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, float* h_out,
+                  int64_t img_begin, int64_t img_count, void* stream, unsigned flags) {
+  return guarded([&] {
+    if (!P) throw ConfigError("null plan");
+    const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
+    const bool accumulate = (flags & PSCONV_FLAG_ACCUMULATE) != 0;
+    if (!h_in || !h_out || (!h_flt && !prepacked)) throw ConfigError("null tensor pointer");
+    if (prepacked && !P->prepacked) throw ConfigError("PSCONV_FLAG_PREPACKED without conv_plan_prepack");
+    const conv_desc& d = P->d;
+    if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
+      throw ConfigError("image range outside nImg");
+    if (img_count == 0) return;
+    const int64_t in_img = d.nIfm * d.ifh * d.ifw, out_img = d.nOfm * d.ofh * d.ofw;
+    int prev = 0;
+    CUDA_OK(cudaGetDevice(&prev));
+    CUDA_OK(cudaSetDevice(P->device));
+    if (!P->pipe) {  // ~32 MB of input per chunk, double buffered
+      auto* h = new conv_plan::HostPipe();
+      P->pipe = h;
+      h->chunk = std::max<int64_t>(1, std::min<int64_t>(d.nImg, (int64_t(32) << 20) / (in_img * 4)));
+      for (int i = 0; i < 2; ++i) {
+        CUDA_OK(cudaMalloc(&h->din[i], h->chunk * in_img * sizeof(float)));
+        CUDA_OK(cudaMalloc(&h->dout[i], h->chunk * out_img * sizeof(float)));
+        CUDA_OK(cudaEventCreateWithFlags(&h->h2d[i], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&h->conv[i], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&h->d2h[i], cudaEventDisableTiming));
+      }
+      CUDA_OK(cudaMalloc(&h->dflt, P->flt_elems * sizeof(float)));
+      CUDA_OK(cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&h->flt, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&h->end, cudaEventDisableTiming));
+      CUDA_OK(cudaStreamCreateWithFlags(&h->sin, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&h->sout, cudaStreamNonBlocking));
+    }
+    auto* h = P->pipe;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    // everything starts after the caller's prior work on `stream`
+    CUDA_OK(cudaEventRecord(h->start, cs));
+    CUDA_OK(cudaStreamWaitEvent(h->sin, h->start, 0));
+    CUDA_OK(cudaStreamWaitEvent(h->sout, h->start, 0));
+    unsigned kflags = flags;
+    if (!prepacked) {
+      CUDA_OK(cudaMemcpyAsync(h->dflt, h_flt, P->flt_elems * sizeof(float), cudaMemcpyHostToDevice, h->sin));
+      CUDA_OK(cudaEventRecord(h->flt, h->sin));
+      CUDA_OK(cudaStreamWaitEvent(cs, h->flt, 0));
+    }
+    const int64_t nchunks = (img_count + h->chunk - 1) / h->chunk;
+    for (int64_t i = 0; i < nchunks; ++i) {
+      const int sl = int(i & 1);
+      const int64_t c0 = img_begin + i * h->chunk;
+      const int64_t cn = std::min(h->chunk, img_begin + img_count - c0);
+      // copy in once the kernel two chunks back has read this slot
+      if (i >= 2) CUDA_OK(cudaStreamWaitEvent(h->sin, h->conv[sl], 0));
+      CUDA_OK(cudaMemcpyAsync(h->din[sl], h_in + c0 * in_img, cn * in_img * sizeof(float),
+                              cudaMemcpyHostToDevice, h->sin));
+      if (accumulate) {  // `+=`: bring the current output chunk in as well
+        if (i >= 2) CUDA_OK(cudaStreamWaitEvent(h->sin, h->d2h[sl], 0));
+        CUDA_OK(cudaMemcpyAsync(h->dout[sl], h_out + c0 * out_img, cn * out_img * sizeof(float),
+                                cudaMemcpyHostToDevice, h->sin));
+      }
+      CUDA_OK(cudaEventRecord(h->h2d[sl], h->sin));
+      CUDA_OK(cudaStreamWaitEvent(cs, h->h2d[sl], 0));
+      if (i >= 2 && !accumulate) CUDA_OK(cudaStreamWaitEvent(cs, h->d2h[sl], 0));
+      launch_range(P, h->din[sl], h->dflt, h->dout[sl], cn, cs, kflags);
+      kflags |= PSCONV_FLAG_PREPACKED;  // the filter is repacked once, by the first chunk
+      CUDA_OK(cudaEventRecord(h->conv[sl], cs));
+      CUDA_OK(cudaStreamWaitEvent(h->sout, h->conv[sl], 0));
+      CUDA_OK(cudaMemcpyAsync(h_out + c0 * out_img, h->dout[sl], cn * out_img * sizeof(float),
+                              cudaMemcpyDeviceToHost, h->sout));
+      CUDA_OK(cudaEventRecord(h->d2h[sl], h->sout));
+    }
+    CUDA_OK(cudaEventRecord(h->end, h->sout));
+    CUDA_OK(cudaStreamWaitEvent(cs, h->end, 0));
+    CUDA_OK(cudaSetDevice(prev));
   });
 }
 

@@ -87,6 +87,13 @@ struct ConvParams {
   unsigned long long* trace;      // profiling only (PSCONV_DEBUG & 8): CTA 0 stage timestamps
 };
 constexpr int kTraceStages = 128;
+// CTA-0 clock trace (PSCONV_DEBUG=8) is compiled in only with -DPSCONV_TRACE
+// (tools/build_variant.sh): the instrumented loops measured 5% slower on cfg5.
+#ifdef PSCONV_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 constexpr int kHaloB = 8;  // halo mode: B-ring barriers follow 8 A-ring slots
 
 // Shared-memory plan (per CTA, one CTA per SM): a ring of `stages` pipeline
@@ -166,6 +173,19 @@ __device__ __forceinline__ TileCoord decode_group(const ConvParams& p, int g, in
 // lo = x - trunc_tf32(x) over n4 float4s (128 splitter threads), loads batched
 // 4 deep for ILP
 __device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, int tid) {
+#ifdef PSCONV_SPLIT_SIMPLE
+#pragma unroll 4
+  for (int idx = tid; idx < n4; idx += 128) {
+    const float4 x = a[idx];
+    float4 lo;
+    lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+    lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+    lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+    lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+    alo[idx] = lo;
+  }
+  return;
+#endif
   for (int base = tid; base < n4; base += 512) {
     float4 x[4];
 #pragma unroll
@@ -227,7 +247,7 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
       }
       for (int t = 0; t < taps; ++t) {
         const int bi = kHaloB + bs;
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[gs * 4 + 0] = clock64();
         ptx::mbar_wait(&empty[bi], bph ^ 1);
         if (tr) p.trace[gs * 4 + 1] = clock64();
@@ -297,7 +317,7 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
           d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
         }
         const int bi = kHaloB + bs;
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
         ptx::mbar_wait(&full[bi], bph);
         ptx::tc_fence_after();
@@ -374,7 +394,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
 
   const long long t_entry = clock64();
-  unsigned long long* ev = (p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * kTraceStages : nullptr;
+  unsigned long long* ev = (kTrace && p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * kTraceStages : nullptr;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B). The offset is the
   // same in both CTAs of a pair, which the pair MMA relies on.
@@ -474,7 +494,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
       for (int it = 0; it < p.nst; ++it) {
         const int nk = min(p.kps, p.ksteps - it * p.kps);
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+        const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[gs * 4 + 0] = clock64();
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (tr) p.trace[gs * 4 + 1] = clock64();
@@ -560,7 +580,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const int it0 = c * p.chunk_stages;
         const int it_end = min(nst, it0 + p.chunk_stages);
         for (int it = it0; it < it_end; ++it) {
-          const bool tr = p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+          const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
           ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);

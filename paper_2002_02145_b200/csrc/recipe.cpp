@@ -299,7 +299,16 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   const int ksteps = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
   // bn 256 has a single TMEM chunk buffer (drain not overlapped): longer chunks
   // (error ~1.2e-7 per k-step of chunk, tools/chunk_sweep.py: ch 32 -> 3.5e-6)
-  s.chunk = r.chunk ? r.chunk : (mode == PSCONV_MODE_3XTF32 ? (s.bn == 256 ? 32 : 16) : ksteps);
+  // 3xTF32 default: equal chunks of at most 16 k-steps, or 40 at bn 256 where
+  // each chunk boundary stalls the MMA on the drain (measured cfg5: ch 72 / 36 /
+  // 32 / 24 -> 1738 / 1775 / 1789 / 1815 us; 40 k-steps ~ 4.8e-6 relL2)
+  int chunk_def = ksteps;
+  if (mode == PSCONV_MODE_3XTF32) {
+    const int cmax = s.bn == 256 ? 40 : 16;
+    const int nch = (ksteps + cmax - 1) / cmax;
+    chunk_def = (ksteps + nch - 1) / nch;
+  }
+  s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
   s.chunk = (s.chunk + s.kps - 1) / s.kps * s.kps;  // chunks hold whole stages

@@ -151,3 +151,36 @@ def test_image_range_and_accumulate():
     yg = yg.reshape(6, -1)
     assert np.array_equal(yg[:2], ref[:2]) and np.array_equal(yg[5:], ref[5:])
     assert oracle.rel_l2(yg[2:5], ref[2:5]) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_forward_host(accumulate):
+    """conv_fwd_host: host buffers streamed through the device in double-buffered chunks
+    (more chunks than slots), same result as the device path; `+=` reads the host output."""
+    conv = "conv:200,32,32,56,56,3,3,1,1,16,1,1,56,56"  # 401 KB/image: 81-image chunks, 3 chunks
+    p = ps.ConvPreset.parse(conv)
+    sx, sw = seeds(11)
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), device=dev)
+    w = torch.empty(p.filter_elems(), device=dev)
+    ps.fill_input(p, sx, x, c_logical=32)
+    ps.fill_filter(p, sw, w, c_logical=32)
+    y = torch.zeros(p.output_elems(), device=dev)
+    base = torch.randn(p.output_elems()) if accumulate else torch.zeros(p.output_elems())
+    y.copy_(base.to(dev))
+    plan = ps.ConvPlan(p, mode="3xtf32", device=0)
+    plan.forward(x, w, y, img_begin=5, img_count=190, accumulate=accumulate)
+    hx = x.cpu().pin_memory()
+    hw = w.cpu().pin_memory()
+    hy = base.clone().pin_memory()
+    plan.forward_host(hx, hw, hy, img_begin=5, img_count=190, accumulate=accumulate)
+    torch.cuda.synchronize()
+    yd = y.cpu()
+    assert torch.equal(hy[: 5 * p.output_elems(1)], base[: 5 * p.output_elems(1)])
+    assert torch.equal(hy, yd), "host-pipelined result differs from the device path"
+    # unpinned numpy buffers work too (copies then serialise)
+    hy2 = base.numpy().copy()
+    plan.forward_host(hx.numpy(), hw.numpy(), hy2, img_begin=5, img_count=190, accumulate=accumulate)
+    torch.cuda.synchronize()
+    assert np.array_equal(hy2, yd.numpy())
