@@ -41,6 +41,8 @@ extern "C" {
                                      presets.hpp:112); default overwrites   */
 #define PSCONV_FLAG_PREPACKED 2u  /* use the filter already prepacked into the
                                      plan by conv_plan_prepack (flt ignored) */
+#define PSCONV_FLAG_RELU 4u       /* fused epilogue: out = max(conv (+ bias), 0);
+                                     not with PSCONV_FLAG_ACCUMULATE            */
 
 /*
  * Conv-layer descriptor. Replaces nestrank::ConvPreset (presets.hpp:13-23):
@@ -70,6 +72,33 @@ int conv_desc_validate(conv_desc* d);
  * extension fields are at their defaults, else 14). Returns 0, or 2 when
  * the buffer is too small. */
 int conv_desc_format(const conv_desc* d, char* buf, size_t len);
+
+/* ---------------------------------------------------------------------------
+ * Nest-document front end. Reads the reference's textual
+ * loop-nest format (parse_nest, loopnest.hpp:340-523; samples/conv2d.nest,
+ * samples/matmul.nest) and recognises the computation:
+ *   NEST_KIND_CONV  the blocked direct convolution of presets.hpp:60-127 with
+ *                   any variable names and outer-loop order -> desc + recipe
+ *                   ("perm=..." over the reference loop names, variants.hpp);
+ *   NEST_KIND_GEMM  C[i][j] += A[i][k] * B[k][j] -> M, N, K, and desc = the
+ *                   same product as a 1x1 convolution over M "images": row-major
+ *                   A[M][K] IS NCHW16c and C[M][N] IS NKPQ16k at H = W = 1;
+ *                   B[K][N] is blocked by gemm_pack_b (desc is validated and
+ *                   runnable only when N, K % 16 == 0).
+ * Returns 0, or 2 (parse error / unsupported computation; conv_last_error). */
+#define NEST_KIND_CONV 1
+#define NEST_KIND_GEMM 2
+typedef struct nest_info {
+  int32_t kind, reserved;
+  conv_desc desc;
+  int64_t M, N, K;
+  char recipe[256];
+} nest_info;
+int nest_parse(const char* text, nest_info* out);
+
+/* Row-major B[K][N] (device) -> the KCRS16c16k filter of the 1x1 convolution
+ * that computes C = A * B (K input channels, N output channels). */
+int gemm_pack_b(const float* b_rowmajor, float* b_blocked, int64_t K, int64_t N, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * CPU microkernel with the reference's call convention. Replaces the external
@@ -116,6 +145,14 @@ const char* conv_plan_recipe(const conv_plan* p);
  * use one plan per concurrent stream. */
 int conv_fwd(const conv_plan* p, const float* in, const float* flt, float* out, int64_t img_begin,
              int64_t img_count, void* cuda_stream, unsigned flags);
+
+/* conv_fwd with a fused epilogue (the reference body is a
+ * bare `+=`, presets.hpp:112): out = conv(in, flt) + bias[k] (bias: nOfm fp32
+ * device values, or NULL), then ReLU when PSCONV_FLAG_RELU. With
+ * PSCONV_FLAG_ACCUMULATE the bias is added into out as well (no ReLU).
+ * conv_fwd(...) == conv_fwd_ex(..., bias = NULL, ...). */
+int conv_fwd_ex(const conv_plan* p, const float* in, const float* flt, float* out, const float* bias,
+                int64_t img_begin, int64_t img_count, void* cuda_stream, unsigned flags);
 
 /* conv_fwd on HOST buffers (the reference's emitted driver computes on host
  * arrays, emit.hpp:60-134 / tests/golden/conv_identity.c): h_in / h_flt /

@@ -27,13 +27,14 @@ from ._lib import conv_desc, lib
 __all__ = [
     "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
     "MODE_TF32", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
-    "brgemm", "fill_input", "fill_filter", "version",
+    "brgemm", "fill_input", "fill_filter", "version", "parse_nest", "NestInfo", "GemmPlan",
 ]
 
 MODE_3XTF32 = 0
 MODE_TF32 = 1
 FLAG_ACCUMULATE = 1
 FLAG_PREPACKED = 2
+FLAG_RELU = 4
 _MODES = {"3xtf32": MODE_3XTF32, "tf32": MODE_TF32}
 
 
@@ -187,13 +188,17 @@ class ConvPlan:
         _check(lib.conv_plan_prepack(self._h, _ptr(flt), _stream_ptr(stream)))
 
     def forward(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
-                stream=None, accumulate: bool = False, prepacked: bool = False) -> None:
-        """Device pointers or CUDA tensors in NCHW16c / KCRS16c16k / NKPQ16k."""
+                stream=None, accumulate: bool = False, prepacked: bool = False,
+                bias=None, relu: bool = False) -> None:
+        """Device pointers or CUDA tensors in NCHW16c / KCRS16c16k / NKPQ16k. Optional fused
+        epilogue: + bias[nOfm] (device), ReLU (C ABI conv_fwd_ex)."""
         if img_count is None:
             img_count = self.preset.nImg - img_begin
-        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_PREPACKED if prepacked else 0)
-        _check(lib.conv_fwd(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
-                            img_begin, img_count, _stream_ptr(stream), flags))
+        flags = ((FLAG_ACCUMULATE if accumulate else 0) | (FLAG_PREPACKED if prepacked else 0)
+                 | (FLAG_RELU if relu else 0))
+        _check(lib.conv_fwd_ex(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
+                               0 if bias is None else _ptr(bias), img_begin, img_count,
+                               _stream_ptr(stream), flags))
 
     __call__ = forward
 
@@ -218,6 +223,53 @@ class ConvPlan:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+@dataclass
+class NestInfo:
+    """What a reference nest document computes (C ABI nest_parse)."""
+    kind: str                    # "conv" or "gemm"
+    preset: ConvPreset           # the conv descriptor (gemm: the equivalent 1x1 conv)
+    recipe: str                  # conv: outer-loop order as a reference recipe id
+    M: int = 0
+    N: int = 0
+    K: int = 0
+
+
+def parse_nest(text: str) -> NestInfo:
+    """Reads a reference nest document (loopnest.hpp:340-523 grammar; e.g. samples/conv2d.nest,
+    samples/matmul.nest) and recognises the computation."""
+    info = _lib.nest_info()
+    _check(lib.nest_parse(text.encode(), ctypes.byref(info)))
+    kind = {1: "conv", 2: "gemm"}[info.kind]
+    return NestInfo(kind, ConvPreset._from_c(info.desc), info.recipe.decode(), info.M, info.N, info.K)
+
+
+class GemmPlan:
+    """C[M][N] = A[M][K] @ B[K][N] (row-major fp32, device) on the conv kernel: row-major A
+    is NCHW16c and C is NKPQ16k at H = W = 1, so the product is a 1x1 convolution over M
+    "images"; B is blocked once per call by gemm_pack_b (N, K multiples of 16)."""
+
+    def __init__(self, M: int, N: int, K: int, mode="3xtf32", device: int = 0,
+                 recipe: str | None = None):
+        self.M, self.N, self.K = M, N, K
+        self.conv = ConvPlan(ConvPreset.parse(f"conv:{M},{N},{K},1,1,1,1,1,1,16"), mode=mode,
+                             device=device, recipe=recipe)
+        self._bblk = None
+
+    @property
+    def recipe(self) -> str:
+        return self.conv.recipe
+
+    def forward(self, a, b, c, stream=None) -> None:
+        import torch
+        if self._bblk is None:
+            self._bblk = torch.empty(self.K * self.N, dtype=torch.float32,
+                                     device=torch.device("cuda", self.conv.device))
+        _check(lib.gemm_pack_b(_ptr(b), _ptr(self._bblk), self.K, self.N, _stream_ptr(stream)))
+        self.conv.forward(a, self._bblk, c, stream=stream)
+
+    __call__ = forward
 
 
 def emit_driver(preset: ConvPreset, recipe: str | None = None) -> str:

@@ -29,6 +29,11 @@ class conv_desc(ctypes.Structure):
         "pad_h", "pad_w", "ifh", "ifw")]
 
 
+class nest_info(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("desc", conv_desc),
+                ("M", c_i64), ("N", c_i64), ("K", c_i64), ("recipe", ctypes.c_char * 256)]
+
+
 gemm_microkernel_fn = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_float),
                                        ctypes.POINTER(ctypes.c_float),
                                        ctypes.POINTER(ctypes.c_float))
@@ -45,6 +50,9 @@ _sigs = {
     "conv_plan_destroy": (None, [c_vp]),
     "conv_plan_recipe": (ctypes.c_char_p, [c_vp]),
     "conv_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
+    "nest_parse": (ctypes.c_int, [ctypes.c_char_p, _P(nest_info)]),
+    "gemm_pack_b": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "conv_fwd_ex": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
     "conv_fwd_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
     "conv_plan_launches": (ctypes.c_int, [c_vp]),
     "conv_plan_prepack": (ctypes.c_int, [c_vp, c_vp, c_vp]),

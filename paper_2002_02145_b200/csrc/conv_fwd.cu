@@ -205,6 +205,23 @@ __global__ void pack_filter_kernel(const float* __restrict__ kcrs, float* __rest
   }
 }
 
+// row-major B[K][N] -> KCRS16c16k [N/16][K/16][1][1][16c][16k] (the GEMM's 1x1 filter)
+__global__ void gemm_pack_b_kernel(const float* __restrict__ b, float* __restrict__ out, int64_t K,
+                                   int64_t N) {
+  const int64_t n_elems = K * N;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int k16 = int(t & 15);
+    t >>= 4;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int64_t cb = t % (K / 16);
+    const int64_t kb = t / (K / 16);
+    out[e] = b[(cb * 16 + c16) * N + kb * 16 + k16];
+  }
+}
+
 __global__ void unpack_output_kernel(const float* __restrict__ in16, float* __restrict__ nkpq,
                                      int64_t n_elems, int Kb, int PQ) {
   // element e of NKPQ: ((n*K + k)*PQ + pq)
@@ -299,7 +316,7 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
 // Launches the plan on images [0, img_count) of `in` / `out` (already offset to
 // the first image). Validation is the caller's (conv_fwd / conv_fwd_host).
 void launch_range(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
-                  cudaStream_t st, unsigned flags) {
+                  cudaStream_t st, unsigned flags, const float* bias = nullptr) {
   const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
   const conv_desc& d = P->d;
   const Schedule& s = P->sched;
@@ -446,6 +463,8 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
   prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
+  prm.bias = bias;
+  prm.relu = (flags & PSCONV_FLAG_RELU) ? 1 : 0;
   // profiling switch (never set in production; results are wrong when non-zero)
   static const int debug_env = [] {
     const char* e = std::getenv("PSCONV_DEBUG");
@@ -605,14 +624,17 @@ int conv_plan_launches(const conv_plan* p) {
   return p ? 2 : 0;  // filter prepack + conv
 }
 
-int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_begin,
-             int64_t img_count, void* stream, unsigned flags) {
+int conv_fwd_ex(const conv_plan* P, const float* in, const float* flt, float* out, const float* bias,
+                int64_t img_begin, int64_t img_count, void* stream, unsigned flags) {
   return guarded([&] {
     if (!P) throw ConfigError("null plan");
     const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
     if (!in || !out || (!flt && !prepacked)) throw ConfigError("null tensor pointer");
     if (prepacked && !P->prepacked) throw ConfigError("PSCONV_FLAG_PREPACKED without conv_plan_prepack");
     if (prepacked) flt = in;  // unused; keeps the alignment check below simple
+    if ((flags & PSCONV_FLAG_RELU) && (flags & PSCONV_FLAG_ACCUMULATE))
+      throw ConfigError("PSCONV_FLAG_RELU cannot be combined with PSCONV_FLAG_ACCUMULATE");
+    if (bias && (reinterpret_cast<uintptr_t>(bias) & 3)) throw ConfigError("bias must be 4-byte aligned");
     const conv_desc& d = P->d;
     if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
       throw ConfigError("image range [" + std::to_string(img_begin) + ", " +
@@ -624,8 +646,13 @@ int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, 
     if (img_count == 0) return;
     const int64_t in_img = d.nIfm * d.ifh * d.ifw, out_img = d.nOfm * d.ofh * d.ofw;
     launch_range(P, in + img_begin * in_img, flt, out + img_begin * out_img, img_count,
-                 static_cast<cudaStream_t>(stream), flags);
+                 static_cast<cudaStream_t>(stream), flags, bias);
   });
+}
+
+int conv_fwd(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_begin,
+             int64_t img_count, void* stream, unsigned flags) {
+  return conv_fwd_ex(P, in, flt, out, nullptr, img_begin, img_count, stream, flags);
 }
 
 int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
@@ -711,6 +738,15 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     CUDA_OK(cudaEventRecord(h->end, h->sout));
     CUDA_OK(cudaStreamWaitEvent(cs, h->end, 0));
     CUDA_OK(cudaSetDevice(prev));
+  });
+}
+
+int gemm_pack_b(const float* b, float* out, int64_t K, int64_t N, void* stream) {
+  return guarded([&] {
+    if (!b || !out) throw ConfigError("null argument");
+    if (K <= 0 || N <= 0 || K % 16 || N % 16) throw ConfigError("gemm_pack_b: K and N must be positive multiples of 16");
+    gemm_pack_b_kernel<<<grid_for(K * N), 256, 0, static_cast<cudaStream_t>(stream)>>>(b, out, K, N);
+    CUDA_OK(cudaGetLastError());
   });
 }
 

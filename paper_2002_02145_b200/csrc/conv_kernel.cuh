@@ -81,6 +81,8 @@ struct ConvParams {
   int chunk_stages;               // stages per TMEM accumulation chunk
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int accumulate;                 // out += conv
+  const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
+  int relu;                       // fused epilogue: max(., 0) (not with accumulate)
   int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
@@ -700,6 +702,17 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             if constexpr (DW == 32) ptx::tmem_st32(tsum + j * 32, v);
             else ptx::tmem_st16(tsum + j * 16, v);
           } else if (tc.live) {
+            // fused epilogue on the finished sum: + bias[k], ReLU (the same
+            // value for all lanes: broadcast loads through L1)
+            if (p.bias != nullptr) {
+              const float* bj = p.bias + tc.tk * BN + j * DW;
+#pragma unroll
+              for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __ldg(bj + i));
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(fmaxf(__uint_as_float(v[i]), 0.f));
+            }
 #pragma unroll
             for (int blk = 0; blk < DW / 16; ++blk) {
               uint8_t* st = out_stage + ostage * Cfg::kOutStageBytes;

@@ -95,6 +95,7 @@ struct HaloGeom {
   int hw, hr, a_tile, a_lo_off, a_stage, b_lo_off, b_stage;
 };
 bool halo_eligible(const conv_desc& d);
+void nest_recognise(const std::string& text, nest_info* out);  // nest.cpp, throws ConfigError
 HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode);
 
 // Closed-form model (select.cpp).

@@ -184,3 +184,71 @@ def test_forward_host(accumulate):
     plan.forward_host(hx.numpy(), hw.numpy(), hy2, img_begin=5, img_count=190, accumulate=accumulate)
     torch.cuda.synchronize()
     assert np.array_equal(hy2, yd.numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("recipe", [None, "gpu=bn:64,halo:1"])
+def test_fused_bias_relu(mode, relu, recipe):
+    """fused epilogue out = max(conv + bias, 0) against the oracle conv
+    with the same bias / ReLU applied on the host (3xTF32 uses several accumulation chunks)."""
+    p = ps.ConvPreset.parse("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20")
+    sx, sw = seeds(12)
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), device=dev)
+    w = torch.empty(p.filter_elems(), device=dev)
+    ps.fill_input(p, sx, x, c_logical=64)
+    ps.fill_filter(p, sw, w, c_logical=64)
+    bias = torch.linspace(-3.0, 3.0, p.nOfm, device=dev)
+    y = torch.full((p.output_elems(),), float("nan"), device=dev)
+    plan = ps.ConvPlan(p, mode=mode, device=0, recipe=recipe)
+    plan.forward(x, w, y, bias=bias, relu=relu)
+    torch.cuda.synchronize()
+    ref = oracle.conv(p, oracle.fill_input(p, sx, 64), oracle.fill_filter(p, sw, 64))
+    ref = ref.reshape(p.nImg, p.nOfm // 16, p.ofh, p.ofw, 16)
+    ref = ref + bias.cpu().numpy().reshape(1, p.nOfm // 16, 1, 1, 16)
+    if relu:
+        ref = np.maximum(ref, 0)
+    err = oracle.rel_l2(y.cpu().numpy(), ref.ravel())
+    assert err <= TOL[mode], f"relL2 {err:.3e} ({plan.recipe})"
+    if relu:
+        assert (y >= 0).all()
+
+
+@pytest.mark.gpu
+def test_relu_with_accumulate_rejected():
+    p = ps.ConvPreset.parse("conv:1,16,16,4,4,1,1,1,1,16")
+    plan = ps.ConvPlan(p, mode="tf32", device=0)
+    t = torch.zeros(4096, device="cuda:0")
+    with pytest.raises(ps.ConfigRejectedError):
+        plan.forward(t, t, t, accumulate=True, relu=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_gemm_from_nest_document(mode):
+    """a matmul nest document runs on the conv kernel as a 1x1 conv."""
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "nests", "gemm_96.nest")) as f:
+        info = ps.parse_nest(f.read())
+    g = ps.GemmPlan(info.M, info.N, info.K, mode=mode)
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-1, 1, (info.M, info.K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (info.K, info.N)).astype(np.float32)
+    c = torch.full((info.M, info.N), float("nan"), device="cuda:0")
+    g.forward(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), c)
+    torch.cuda.synchronize()
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    err = oracle.rel_l2(c.cpu().numpy(), ref)
+    assert err <= TOL[mode], f"GEMM relL2 {err:.3e} ({g.recipe})"
+
+
+@pytest.mark.gpu
+def test_conv_from_nest_document():
+    """A permuted, renamed conv document -> descriptor + recipe -> GPU parity."""
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "nests", "conv_cfg3_perm.nest")) as f:
+        info = ps.parse_nest(f.read())
+    conv = "conv:" + ",".join(str(info.preset).split(":")[1].split(","))
+    _check("nest-conv", conv, 128, 13, "3xtf32", info.preset.nImg, info.recipe)
