@@ -54,6 +54,9 @@ struct ConvParams {
   int mtiles, mgroups, groups;    // M tiles; groups of CS M tiles; groups * tiles_k
   int m_order;                    // 0: img outer of oj, 1: oj outer of img (oi innermost)
   int k_outer;                    // 1: ofm_tile outer of the pixel loops (recipe order)
+  int m_block;                    // > 0: grouped raster, blocks of m_block M groups x all N
+                                  // tiles (N outer inside a block) so concurrent CTAs share
+                                  // A rows and B columns in L2 (GEMM-like shapes)
   int ksteps;                     // Cb*R*S
   int kps;                        // k-steps per pipeline stage (input-channel blocks per TMA box)
   int cbg;                        // extent of the channel-block counter (Cb / kps or Cb)
@@ -151,7 +154,15 @@ struct TileCoord {
 __device__ __forceinline__ TileCoord decode_group(const ConvParams& p, int g, int rank, int CS) {
   TileCoord c;
   int mg;
-  if (p.k_outer) {
+  if (p.m_block > 0) {
+    const int per = p.m_block * p.tiles_k;
+    const int b = g / per;
+    const int base = b * p.m_block;
+    const int gm = min(p.m_block, p.mgroups - base);
+    const int r = g - b * per;
+    c.tk = r / gm;
+    mg = base + (r - c.tk * gm);
+  } else if (p.k_outer) {
     c.tk = g / p.mgroups;
     mg = g - c.tk * p.mgroups;
   } else {

@@ -54,6 +54,7 @@ struct Recipe {
   int stages = 0;                                             // informational
   int kg = 0;                                                 // k-steps per stage, 0 = auto
   int halo = 0;                                               // 1: halo mode (stride-1 R x S)
+  int gm = -1;                                                // grouped raster block, -1 = auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -72,6 +73,7 @@ struct Schedule {
   int kps;             // k-steps (input-channel blocks) per pipeline stage
   int stages;          // pipeline stages in the shared-memory ring (halo: A ring)
   int halo = 0;        // halo mode: Pb whole output rows, input halo loaded once per block
+  int m_block = 0;     // grouped raster block (M groups); 0 = the recipe's loop order
   int hb_stages = 0;   // halo: B-ring stages
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner

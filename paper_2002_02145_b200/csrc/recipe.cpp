@@ -100,6 +100,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
           if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
+        } else if (key == "gm") {
+          r.gm = static_cast<int>(parse_int(val, "gpu raster group"));
+          if (r.gm < 0) throw ConfigError("gpu gm must be >= 0");
         } else if (key == "halo") {
           r.halo = static_cast<int>(parse_int(val, "gpu halo"));
           if (r.halo != 0 && r.halo != 1) throw ConfigError("gpu halo must be 0 or 1");
@@ -131,6 +134,7 @@ std::string Recipe::id() const {
          std::to_string(box_p) + "x" + std::to_string(box_n);
     if (cs) s += ",cl:" + std::to_string(cs);
     if (halo) s += ",halo:1";
+    if (gm >= 0) s += ",gm:" + std::to_string(gm);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -311,6 +315,22 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
+  // Grouped raster (auto): when both the activation rows and the filter of all
+  // tiles exceed the L2 share, a wave of 148 concurrent tiles should cover a
+  // ~12 x 12 block of (M group, N tile) so A rows and B columns are reused in
+  // L2 instead of being re-read from HBM per N tile (GEMM-like shapes).
+  {
+    const int64_t tq = (d.ofw + s.qb - 1) / s.qb, tp = (d.ofh + s.pb - 1) / s.pb,
+                  tn = (d.nImg + s.nb - 1) / s.nb;
+    const int64_t mgroups = (tq * tp * tn + std::max(1, s.cs) - 1) / std::max(1, s.cs);
+    const int64_t tiles_k = d.nOfm / s.bn;
+    const double a_bytes = 4.0 * d.nImg * d.nIfm * d.ifh * d.ifw;
+    const double b_bytes = 4.0 * d.nOfm * d.nIfm * d.kh * d.kw * (mode == PSCONV_MODE_3XTF32 ? 2 : 1);
+    int gm = 0;
+    if (tiles_k >= 4 && mgroups >= 24 && a_bytes > 48e6 && b_bytes > 24e6) gm = 12;
+    s.m_block = r.gm >= 0 ? r.gm : gm;
+    canon.gm = r.gm >= 0 ? r.gm : -1;
+  }
   s.chunk = (s.chunk + s.kps - 1) / s.kps * s.kps;  // chunks hold whole stages
   canon.chunk = (mode == PSCONV_MODE_3XTF32 || r.chunk) ? s.chunk : 0;
   canon.kg = r.kg ? s.kps : 0;

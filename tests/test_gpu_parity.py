@@ -252,3 +252,13 @@ def test_conv_from_nest_document():
         info = ps.parse_nest(f.read())
     conv = "conv:" + ",".join(str(info.preset).split(":")[1].split(","))
     _check("nest-conv", conv, 128, 13, "3xtf32", info.preset.nImg, info.recipe)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("recipe", ["gpu=bn:64,box:2x2x32,cl:1,gm:5", "gpu=bn:64,box:2x2x32,cl:2,gm:3",
+                                    "gpu=bn:128,box:2x2x32,cl:1,gm:1"])
+def test_grouped_raster(recipe):
+    """Grouped (M-block x N-tile) rasterisation covers every tile exactly once, including
+    the partial last block."""
+    mode = "tf32" if "cl:2" in recipe else "3xtf32"
+    _check("gm", BASELINE["cfg5"][0], 256, 5, mode, 23, recipe)
