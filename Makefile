@@ -13,7 +13,7 @@ CXXFLAGS:= -O3 -std=c++17 -fPIC -fopenmp $(INC)
 
 LIB     := $(PKG)/libpsconv.so
 CU_OBJS := $(BUILD)/conv_fwd.o
-CC_OBJS := $(BUILD)/desc.o $(BUILD)/recipe.o $(BUILD)/select.o $(BUILD)/emit.o $(BUILD)/microkernel_cpu.o $(BUILD)/nest.o
+CC_OBJS := $(BUILD)/desc.o $(BUILD)/recipe.o $(BUILD)/select.o $(BUILD)/emit.o $(BUILD)/microkernel_cpu.o $(BUILD)/nest.o $(BUILD)/dnnrank.o
 HDRS    := include/psconv.h $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.cuh)
 
 ORACLE  := oracle/liboracle.so

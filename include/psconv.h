@@ -192,6 +192,31 @@ int64_t conv_emit_driver(const conv_desc* d, const char* recipe, char* buf, size
  */
 int conv_select_topk(const conv_desc* d, int mode, int k, char* buf, size_t len, double* us_out);
 
+/* ---------------------------------------------------------------------------
+ * Pairwise DNN ranker (PolyScientist-DNN; reference
+ * dnnrank.hpp:87-438 PairwiseRanker, pipeline.hpp:98-173). Same net (8-64-32-
+ * 16-8-2, relu/relu/softsign/relu/softmax, theta 0.6), joint pair
+ * normalisation, seeded mini-batch training, "pairnet 1" weights text and
+ * round-robin tournament ranking; the per-variant statistics are the B200
+ * model's resource times (conv_model_stats: MMA, shared memory, operand-row
+ * delivery, HBM; us) instead of cache working sets.
+ */
+/* stats[4] of one recipe. Returns 0 / 2. */
+int conv_model_stats(const conv_desc* d, int mode, const char* recipe, double* stats);
+/* Trains on dataset rows "a0 a1 a2 a3 b0 b1 b2 b3 A|B" (the reference pairs
+ * format with real-valued statistics); holds out floor((1-split)*n) seeded-
+ * shuffled rows; writes the weights text; acc[0] = train, acc[1] = holdout
+ * accuracy (-1 if none). Returns 0 / 2. */
+int ranker_train(const char* dataset, int epochs, double learning_rate, uint64_t seed, double split,
+                 char* weights, size_t len, double* acc);
+/* 0 = A faster, 1 = B faster, 2 = draw (neither softmax output > theta); prob
+ * (may be NULL) receives both outputs. Negative status on error. */
+int ranker_compare(const char* weights, const double* a, const double* b, double* prob);
+/* conv_select_topk with the tournament instead of the cost model (ties by
+ * modelled cost, then id); *symmetry = fraction of order-consistent games. */
+int conv_select_topk_dnn(const conv_desc* d, int mode, int k, const char* weights, char* buf, size_t len,
+                         double* symmetry);
+
 /* Modelled time (microseconds) of one recipe, -1 on error. */
 double conv_model_us(const conv_desc* d, int mode, const char* recipe);
 

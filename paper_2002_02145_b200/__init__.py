@@ -28,6 +28,7 @@ __all__ = [
     "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
     "MODE_TF32", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
     "brgemm", "fill_input", "fill_filter", "version", "parse_nest", "NestInfo", "GemmPlan",
+    "model_stats", "ranker_train", "ranker_compare", "default_ranker_weights",
 ]
 
 MODE_3XTF32 = 0
@@ -283,18 +284,69 @@ def emit_driver(preset: ConvPreset, recipe: str | None = None) -> str:
     return buf.value.decode()
 
 
-def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5):
-    """Model-ranked recipes, best first: [(recipe, modelled_us), ...]."""
+def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5, ranker: str = "cost",
+                weights: str | None = None):
+    """Ranked recipes, best first: [(recipe, modelled_us), ...]. ranker="cost" sorts by the
+    closed-form model (costrank.hpp:31-40 analogue); ranker="dnn" runs the pairwise-net
+    tournament with `weights` (pairnet text; default: the shipped B200 weights)."""
     if isinstance(mode, str):
         mode = _MODES[mode.lower()]
     d = preset.to_c()
     buf = ctypes.create_string_buffer(1 << 16)
+    if ranker == "dnn":
+        w = (weights if weights is not None else default_ranker_weights()).encode()
+        sym = ctypes.c_double()
+        n = lib.conv_select_topk_dnn(ctypes.byref(d), mode, k, w, buf, len(buf), ctypes.byref(sym))
+        if n < 0:
+            _check(-n)
+        ids = buf.value.decode().split("\n") if n else []
+        mname = "3xtf32" if mode == MODE_3XTF32 else "tf32"
+        return [(r, model_us(preset, r, mname)) for r in ids]
     us = (ctypes.c_double * k)()
     n = lib.conv_select_topk(ctypes.byref(d), mode, k, buf, len(buf), us)
     if n < 0:
         _check(-n)
     ids = buf.value.decode().split("\n") if n else []
     return list(zip(ids, [us[i] for i in range(n)]))
+
+
+def model_stats(preset: ConvPreset, recipe: str, mode="3xtf32") -> list[float]:
+    """The pairwise ranker's four statistics of one recipe (us: MMA, shared memory, operand
+    rows, HBM) from the closed-form model."""
+    if isinstance(mode, str):
+        mode = _MODES[mode.lower()]
+    d = preset.to_c()
+    st = (ctypes.c_double * 4)()
+    _check(lib.conv_model_stats(ctypes.byref(d), mode, recipe.encode(), st))
+    return list(st)
+
+
+def ranker_train(dataset: str, epochs: int = 300, learning_rate: float = 0.01, seed: int = 1,
+                 split: float = 0.8) -> tuple[str, float, float]:
+    """Trains the pairwise net on dataset rows "a0..a3 b0..b3 A|B"; returns (weights text,
+    train accuracy, holdout accuracy or -1)."""
+    buf = ctypes.create_string_buffer(1 << 20)
+    acc = (ctypes.c_double * 2)()
+    _check(lib.ranker_train(dataset.encode(), epochs, learning_rate, seed, split, buf, len(buf), acc))
+    return buf.value.decode(), acc[0], acc[1]
+
+
+def ranker_compare(weights: str, a, b) -> tuple[int, float, float]:
+    """(0 A faster | 1 B faster | 2 draw, p_A, p_B)."""
+    arr = ctypes.c_double * 4
+    prob = (ctypes.c_double * 2)()
+    r = lib.ranker_compare(weights.encode(), arr(*a), arr(*b), prob)
+    if r < 0:
+        _check(-r)
+    return r, prob[0], prob[1]
+
+
+def default_ranker_weights() -> str:
+    """The shipped B200 weights (tools/train_ranker.py)."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "ranker_b200.pairnet")
+    with open(path) as f:
+        return f.read()
 
 
 def model_us(preset: ConvPreset, recipe: str, mode="3xtf32") -> float:

@@ -50,6 +50,15 @@ _sigs = {
     "conv_plan_destroy": (None, [c_vp]),
     "conv_plan_recipe": (ctypes.c_char_p, [c_vp]),
     "conv_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
+    "conv_model_stats": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_char_p,
+                                         ctypes.POINTER(ctypes.c_double)]),
+    "ranker_train": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                     ctypes.c_double, ctypes.c_char_p, ctypes.c_size_t,
+                                     ctypes.POINTER(ctypes.c_double)]),
+    "ranker_compare": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "conv_select_topk_dnn": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                             ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double)]),
     "nest_parse": (ctypes.c_int, [ctypes.c_char_p, _P(nest_info)]),
     "gemm_pack_b": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp]),
     "conv_fwd_ex": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),

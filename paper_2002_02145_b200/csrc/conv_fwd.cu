@@ -421,6 +421,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.m_order = pos[0] < pos[2] ? 0 : 1;
   prm.k_outer = pos[1] == 0 ? 1 : 0;
   prm.m_block = s.m_block;
+  prm.tap_dw = 1;
   prm.ksteps = Cb * R * S;
   prm.kps = s.kps;
   prm.cb_group = Cb % s.kps == 0 ? 1 : 0;

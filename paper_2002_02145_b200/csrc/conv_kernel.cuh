@@ -83,6 +83,8 @@ struct ConvParams {
   int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
   int chunk_stages;               // stages per TMEM accumulation chunk
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
+  int tap_dw;                     // input columns between consecutive ki taps (1; 5 for the
+                                  // (c,s)-folded stem, conv_fwd.cu fold)
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             if (!PAIR) {
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + s, hp + r, n0, cb + i);
+                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + s * p.tap_dw, hp + r, n0, cb + i);
               ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb >> p.b128);
               if (SPLIT3)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               const uint32_t fb = full_leader + 8u * stage;
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + s, hp + r, n0, cb + i);
+                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + s * p.tap_dw, hp + r, n0, cb + i);
               ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
             }
           }

@@ -103,11 +103,18 @@ HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode);
 // Closed-form model (select.cpp).
 struct ModelBreakdown {
   double us_total, us_tensor, us_hbm, us_l2, us_smem, us_epi;
+  // per-resource times (us) of the SM-side pipeline: MMA issue, shared-memory
+  // traffic, operand-row delivery (TMA/L2 requests) -- the pairwise ranker's
+  // inputs together with us_hbm (dnnrank.cpp)
+  double us_mma, us_smem_traffic, us_rows;
   double hbm_bytes, l2_bytes, flops_issued;
   int64_t m_tiles, tiles;
 };
 ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode);
 std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode);
+// The four per-variant statistics of the pairwise ranker (mirrors VariantStats,
+// dnnrank.hpp:17-24, with B200 resources instead of cache levels).
+void model_stats(const conv_desc& d, const Schedule& s, int mode, double out[4]);
 
 // emit.cpp
 std::string emit_driver(const conv_desc& d, const Schedule& s);

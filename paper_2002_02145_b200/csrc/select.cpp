@@ -147,6 +147,10 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // a CTA pair works on 2 pixel tiles at once: tiles per SM are still tiles/148
   const double groups_per_cluster = std::ceil(double(tiles) / m.sms);
   b.us_tensor = groups_per_cluster * tile_cyc / (m.clock_ghz * 1e3);
+  const double to_us = groups_per_cluster * ksteps / (m.clock_ghz * 1e3);
+  b.us_mma = mma_cyc * to_us;
+  b.us_smem_traffic = smem_cyc * to_us;
+  b.us_rows = del_cyc * to_us;
   b.l2_bytes = ksteps * (a_box + s.bn * 64.0 * (mult > 1 ? 2 : 1) / std::max(1, s.cs)) * tiles;
   b.us_l2 = b.l2_bytes / (m.l2_gbs * 1e9) * 1e6;
   (void)per_sm;
@@ -170,6 +174,14 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.us_total = hi * std::pow(1.0 + std::pow(lo / hi, 4.0), 0.25) + m.launch_us + m.tile_fill_us + b.us_epi +
                (mult > 1 ? 2.0 + 3.0 * flt_b / 3 / (m.hbm_gbs * 1e9) * 1e6 : 0.0);
   return b;
+}
+
+void model_stats(const conv_desc& d, const Schedule& s, int mode, double out[4]) {
+  const ModelBreakdown b = model_schedule(d, s, mode);
+  out[0] = b.us_mma;
+  out[1] = b.us_smem_traffic;
+  out[2] = b.us_rows;
+  out[3] = b.us_hbm;
 }
 
 std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
