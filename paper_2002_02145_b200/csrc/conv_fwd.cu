@@ -28,6 +28,14 @@ struct conv_plan {
   psconv::Schedule sched;
   float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
+  // (c,s)-folded input (recipe fold:C, SURVEY §8d stem note): the layer has C <= 8
+  // real input channels in one 16-channel block; G = 16 / C consecutive kw taps
+  // are packed into one block, so the kernel runs the descriptor kd (kw' =
+  // ceil(kw / G), no w padding, tap dilation G) over the folded copy xfold.
+  int fold = 0, fold_g = 1, fold_phases = 1;
+  conv_desc kd{};                 // kernel descriptor (== d unless folded)
+  float* xfold = nullptr;         // [nImg][phases][H][Wq][16]
+  float* wfold = nullptr;         // folded filter, KCRS16c16k of kd
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
   // conv_fwd_host staging (lazily created): double-buffered device chunks,
@@ -236,13 +244,95 @@ __global__ void unpack_output_kernel(const float* __restrict__ in16, float* __re
   }
 }
 
+void launch_fold_filter(const conv_plan* P, const float* flt, cudaStream_t st);
+int grid_for(int64_t n);
+
 void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
-  const int Kb = int(P->d.nOfm / 16), CRS = int(P->d.nIfm / 16 * P->d.kh * P->d.kw);
+  if (P->fold) {
+    launch_fold_filter(P, flt, st);
+    flt = P->wfold;
+  }
+  const conv_desc& kd = P->kd;
+  const int Kb = int(kd.nOfm / 16), CRS = int(kd.nIfm / 16 * kd.kh * kd.kw);
   const bool split3 = P->mode == PSCONV_MODE_3XTF32;
   prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
                                                   split3 ? P->flt_pack + P->flt_elems : nullptr,
-                                                  int(P->d.nOfm), CRS, int(P->d.kh * P->d.kw),
+                                                  int(kd.nOfm), CRS, int(kd.kh * kd.kw),
                                                   split3 ? 1 : 0, P->b128 ? 1 : 0);
+  CUDA_OK(cudaGetLastError());
+}
+
+// (c,s) fold of the input into `phases` column-phase planes:
+//   out[n][ph][h][wq][s'*C + c] = in[n][0][h][wq*phases + ph - pw + s'][c]
+// for s' < G, c < C (zero outside the row and in the 16 - G*C spare channels).
+// With phases = stride_w the strided conv reads each plane at unit stride (no
+// half-used rows). One thread writes one folded pixel (4 x 16-B stores) from
+// one 16-B load per tap (C <= 4) or two (C <= 8).
+__global__ void fold_input_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n_px,
+                                  int H, int W, int Wq, int phases, int pw, int C, int G) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_px;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int wq = int(t % Wq);
+    t /= Wq;
+    const int h = int(t % H);
+    t /= H;
+    const int ph = int(t % phases);
+    const int64_t n = t / phases;
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.f;
+    const int w0 = wq * phases + ph - pw;
+    const float* row = in + (n * H + h) * int64_t(W) * 16;
+    // all taps' loads issued together (G <= 8)
+    float4 x[8], y[8];
+#pragma unroll
+    for (int sp = 0; sp < 8; ++sp) {
+      const int col = w0 + sp;
+      const bool ok = sp < G && col >= 0 && col < W;
+      x[sp] = ok ? __ldg(reinterpret_cast<const float4*>(row + col * 16)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      y[sp] = (ok && C > 4) ? __ldg(reinterpret_cast<const float4*>(row + col * 16) + 1)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int sp = 0; sp < 8; ++sp) {
+      const float c8[8] = {x[sp].x, x[sp].y, x[sp].z, x[sp].w, y[sp].x, y[sp].y, y[sp].z, y[sp].w};
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < C && sp < G && sp * C + c < 16) v[(sp * C + c) & 15] = c8[c];
+    }
+    float4* dst = reinterpret_cast<float4*>(out + e * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+// the matching filter fold: KCRS16c16k [Kb][1][R][S][16c][16k] -> [Kb][1][R][S'][16c][16k]
+__global__ void fold_filter_kernel(const float* __restrict__ flt, float* __restrict__ out, int64_t n_elems,
+                                   int R, int S, int Sf, int C, int G) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int k16 = int(t & 15);
+    t >>= 4;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int sg = int(t % Sf);
+    t /= Sf;
+    const int r = int(t % R);
+    const int64_t kb = t / R;
+    const int sp = c16 / C, c = c16 % C;
+    const int sx = sg * G + sp;
+    float v = 0.f;
+    if (sp < G && sx < S) v = flt[((kb * R + r) * S + sx) * 256 + c * 16 + k16];
+    out[e] = v;
+  }
+}
+
+void launch_fold_filter(const conv_plan* P, const float* flt, cudaStream_t st) {
+  const int64_t n = P->kd.nOfm * 16 * P->kd.kh * P->kd.kw;
+  fold_filter_kernel<<<grid_for(n), 256, 0, st>>>(flt, P->wfold, n, int(P->d.kh), int(P->d.kw),
+                                                  int(P->kd.kw), P->fold, P->fold_g);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -318,7 +408,15 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
 void launch_range(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
                   cudaStream_t st, unsigned flags, const float* bias = nullptr) {
   const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
-  const conv_desc& d = P->d;
+  const conv_desc& d = P->kd;  // the kernel's descriptor (folded for fold:C plans)
+  if (P->fold) {  // planes [img][phase][H][Wq][16], Wq = kd.ifw
+    const int64_t n_px = img_count * P->fold_phases * d.ifh * d.ifw;
+    fold_input_kernel<<<grid_for(n_px), 256, 0, st>>>(in, P->xfold, n_px, int(P->d.ifh), int(P->d.ifw),
+                                                      int(d.ifw), P->fold_phases, int(P->d.pad_w), P->fold,
+                                                      P->fold_g);
+    CUDA_OK(cudaGetLastError());
+    in = P->xfold;
+  }
   const Schedule& s = P->sched;
   const int Cb = int(d.nIfm / 16), Kb = int(d.nOfm / 16);
   const int H = int(d.ifh), W = int(d.ifw), R = int(d.kh), S = int(d.kw);
@@ -348,9 +446,10 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   // input-channel block of the stage.
   {
     const float* base = in;
+    const int a_cb = P->fold ? P->fold_phases : Cb;  // folded input: column-phase planes
     const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(img_count),
-                                cuuint64_t(Cb)};
-    const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(Cb) * H * W * 64,
+                                cuuint64_t(a_cb)};
+    const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(a_cb) * H * W * 64,
                                    cuuint64_t(H) * W * 64};
     if (s.halo) {  // halo box: hr padded rows of hw pixels, kps blocks
       const HaloGeom h = halo_geom(d, s, P->mode);
@@ -421,7 +520,8 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.m_order = pos[0] < pos[2] ? 0 : 1;
   prm.k_outer = pos[1] == 0 ? 1 : 0;
   prm.m_block = s.m_block;
-  prm.tap_dw = 1;
+  prm.tap_dw = P->fold ? P->fold_g : 1;
+  prm.tap_phases = P->fold ? P->fold_phases : 1;
   prm.ksteps = Cb * R * S;
   prm.kps = s.kps;
   prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
@@ -524,9 +624,27 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     validate_desc(d);
     Recipe r;
     Schedule s;
+    conv_desc kd = d;
+    int fold = 0, fold_g = 1, fold_phases = 1;
     if (recipe && *recipe) {
       r = Recipe::parse(recipe);
-      s = resolve_schedule(d, r, mode);
+      if (r.fold) {
+        // (c,s) fold: one 16-channel block holding C real channels, G taps per block
+        fold = r.fold;
+        fold_g = 16 / fold;
+        if (d.nIfm != 16 || d.gemm_block != 16 || fold_g < 2 || d.kw < 2)
+          throw ConfigError("fold:C needs nIfm = gemm_block = 16, C <= 8 and kw > 1");
+        kd.kw = (d.kw + fold_g - 1) / fold_g;
+        // the folded copy carries the left padding. (Splitting it into stride_w
+        // column-phase planes read at unit stride is supported by the kernel --
+        // tap_dw / tap_phases -- but measured slower on the stem: 848 vs 639 us
+        // for the conv, 728 vs 637 us for the fold; TMA element strides fetch
+        // only the used 64-B rows, so there is no waste to remove.)
+        fold_phases = 1;
+        kd.ifw = d.ifw + d.pad_w;
+        kd.pad_w = 0;
+      }
+      s = resolve_schedule(kd, r, mode);
     } else {
       const auto cands = candidate_schedules(d, mode);
       if (cands.empty()) throw ConfigError("no GPU schedule for this descriptor");
@@ -553,17 +671,26 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     P->device = device;
     P->num_sms = prop.multiProcessorCount;
     P->sched = s;
+    P->kd = kd;
+    P->fold = fold;
+    P->fold_g = fold_g;
+    P->fold_phases = fold_phases;
     // 128-B filter rows pair channel blocks inside a stage: needs even kps dividing Cb
     P->b128 = s.kps % 2 == 0 && (d.nIfm / 16) % s.kps == 0 && std::getenv("PSCONV_NO_B128") == nullptr;
-    P->flt_elems = d.nOfm * d.nIfm * d.kh * d.kw;
+    P->flt_elems = kd.nOfm * kd.nIfm * kd.kh * kd.kw;
     {
       int prev = 0;
       cudaGetDevice(&prev);
       cudaSetDevice(device);
       const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
-      const cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
+      cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
+      if (e == cudaSuccess && fold) e = cudaMalloc(&P->wfold, P->flt_elems * sizeof(float));
+      if (e == cudaSuccess && fold)
+        e = cudaMalloc(&P->xfold, size_t(kd.nImg) * fold_phases * kd.ifh * kd.ifw * 16 * sizeof(float));
       cudaSetDevice(prev);
       if (e != cudaSuccess) {
+        cudaFree(P->flt_pack);
+        cudaFree(P->wfold);
         delete P;
         throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
       }
@@ -600,6 +727,8 @@ void conv_plan_destroy(conv_plan* p) {
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
     cudaFree(p->flt_pack);
+    cudaFree(p->wfold);
+    cudaFree(p->xfold);
     cudaSetDevice(prev);
   }
   delete p;

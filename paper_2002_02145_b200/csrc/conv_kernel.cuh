@@ -83,8 +83,11 @@ struct ConvParams {
   int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
   int chunk_stages;               // stages per TMEM accumulation chunk
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
-  int tap_dw;                     // input columns between consecutive ki taps (1; 5 for the
-                                  // (c,s)-folded stem, conv_fwd.cu fold)
+  int tap_dw;                     // input columns between consecutive ki taps (1; G for the
+                                  // (c,s)-folded input, conv_fwd.cu fold)
+  int tap_phases;                 // folded input split into this many column-phase planes
+                                  // (the A map's channel-block dim): tap ki reads plane
+                                  // (ki*tap_dw) % phases at column (ki*tap_dw) / phases
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -521,13 +524,21 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
           const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
           const int rs = r * p.S + s;
+          int tw = s, tc_ = 0;  // tap column offset / phase plane
+          if (p.tap_phases > 1) {
+            tw = (s * p.tap_dw) / p.tap_phases;
+            tc_ = (s * p.tap_dw) % p.tap_phases;
+          } else if (p.tap_dw > 1) {
+            tw = s * p.tap_dw;
+          }
           if (issuer) {
             uint8_t* sa = sb + j * p.a_boxes * p.a_pitch;
             uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes;
             if (!PAIR) {
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + s * p.tap_dw, hp + r, n0, cb + i);
+                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0,
+                                   cb + i + tc_);
               ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb >> p.b128);
               if (SPLIT3)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
@@ -536,7 +547,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               const uint32_t fb = full_leader + 8u * stage;
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + s * p.tap_dw, hp + r, n0, cb + i);
+                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + tw, hp + r, n0, cb + i + tc_);
               ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
             }
           }

@@ -55,6 +55,7 @@ struct Recipe {
   int kg = 0;                                                 // k-steps per stage, 0 = auto
   int halo = 0;                                               // 1: halo mode (stride-1 R x S)
   int gm = -1;                                                // grouped raster block, -1 = auto
+  int fold = 0;                                               // (c,s) fold: C real channels
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;

@@ -100,6 +100,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
           if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
+        } else if (key == "fold") {
+          r.fold = static_cast<int>(parse_int(val, "gpu fold channels"));
+          if (r.fold < 1 || r.fold > 8) throw ConfigError("gpu fold must be in [1, 8] (real input channels)");
         } else if (key == "gm") {
           r.gm = static_cast<int>(parse_int(val, "gpu raster group"));
           if (r.gm < 0) throw ConfigError("gpu gm must be >= 0");
@@ -135,6 +138,7 @@ std::string Recipe::id() const {
     if (cs) s += ",cl:" + std::to_string(cs);
     if (halo) s += ",halo:1";
     if (gm >= 0) s += ",gm:" + std::to_string(gm);
+    if (fold) s += ",fold:" + std::to_string(fold);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -291,6 +295,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.box_p = s.pb;
   canon.box_n = s.nb;
   canon.halo = s.halo;
+  canon.fold = r.fold;
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)

@@ -19,7 +19,7 @@ from .timing import L2Flush
 CACHE_ENV = "PSCONV_PLAN_CACHE"
 
 
-def _variants(preset: ConvPreset, mode: str, k: int) -> list[str]:
+def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list[str]:
     ranked = [r for r, _ in select_topk(preset, mode, k)]
     out = list(ranked)
     base = ranked[0]
@@ -35,6 +35,15 @@ def _variants(preset: ConvPreset, mode: str, k: int) -> list[str]:
             if mode == "3xtf32":
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
+    # (c,s) fold when the caller knows only c_logical <= 8 of the 16 input channels are
+    # real (the stem): the same top candidates over the folded input
+    if 0 < c_logical <= 8 and preset.nIfm == 16 and preset.kw > 1:
+        for rid in ranked[:2]:
+            h2, g2 = rid.split(";gpu=")
+            kv2 = dict(item.split(":") for item in g2.split(","))
+            kv2.pop("box", None)  # the folded layer has its own box candidates
+            kv2.pop("ch", None)
+            alts.append({**kv2, "fold": str(c_logical)})
     for a in alts:
         rid = head + ";gpu=" + ",".join(f"{key}:{val}" for key, val in a.items())
         if rid not in out:
@@ -85,7 +94,7 @@ def autotune(preset: ConvPreset, mode: str = "3xtf32", k: int = 4, device: int =
     fill_filter(preset, seeds[1], w, c_logical=c_logical)
     flush = L2Flush(dev)
     rows = []
-    for rid in _variants(preset, mode, k):
+    for rid in _variants(preset, mode, k, c_logical):
         try:
             ms = time_recipe(preset, mode, rid, x, w, y, flush, stream)
         except ConfigRejectedError:

@@ -262,3 +262,22 @@ def test_grouped_raster(recipe):
     the partial last block."""
     mode = "tf32" if "cl:2" in recipe else "3xtf32"
     _check("gm", BASELINE["cfg5"][0], 256, 5, mode, 23, recipe)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    # the ResNet-50 stem (7x7/s2/p3, C = 3 of 16): 5 taps per folded block, 2 tap groups
+    ("conv:2,64,16,112,112,7,7,2,2,16,3,3,224,224", 3, "gpu=bn:64,fold:3"),
+    ("conv:2,64,16,20,20,7,7,2,2,16,3,3,40,40", 3, "gpu=bn:32,box:20x6x1,fold:3"),
+    # 3x3 stride 1 with C = 5 (G = 3: one tap group), and C = 8 (G = 2) 5x5 unpadded
+    ("conv:3,32,16,17,19,3,3,1,1,16,1,1,17,19", 5, "gpu=bn:32,fold:5"),
+    ("conv:2,32,16,12,12,5,5,1,1,16,0,0,16,16", 8, "gpu=bn:32,fold:8"),
+])
+def test_cs_fold(conv, c_log, recipe, mode):
+    """(c,s)-folded input (SURVEY §8d stem note): G = 16 / C kw taps share one 16-channel
+    block; same result as the unfolded conv on inputs whose channels >= C are zero."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("fold", conv, c_log, 14, mode, n, recipe)
+    if mode == "tf32":
+        _check("fold-pair", conv, c_log, 14, mode, n, recipe + ",cl:2")
