@@ -197,9 +197,13 @@ class ConvPlan:
             img_count = self.preset.nImg - img_begin
         flags = ((FLAG_ACCUMULATE if accumulate else 0) | (FLAG_PREPACKED if prepacked else 0)
                  | (FLAG_RELU if relu else 0))
-        _check(lib.conv_fwd_ex(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
-                               0 if bias is None else _ptr(bias), img_begin, img_count,
-                               _stream_ptr(stream), flags))
+        if bias is None and not relu:
+            _check(lib.conv_fwd(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
+                                img_begin, img_count, _stream_ptr(stream), flags))
+        else:
+            _check(lib.conv_fwd_ex(self._h, _ptr(inp), 0 if flt is None else _ptr(flt), _ptr(out),
+                                   0 if bias is None else _ptr(bias), img_begin, img_count,
+                                   _stream_ptr(stream), flags))
 
     __call__ = forward
 

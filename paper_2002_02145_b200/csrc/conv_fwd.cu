@@ -344,7 +344,7 @@ int grid_for(int64_t n) {
 }
 
 // ---------------------------------------------------------------- launch
-template <int BN, bool SPLIT3, int CS>
+template <int BN, bool SPLIT3, int CS, bool FUSED>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2)) {
@@ -355,7 +355,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR>,
+      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, FUSED>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     CUDA_OK(attr_err);
@@ -376,19 +376,19 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     cfg.numAttrs = force_cl >= 0 ? force_cl : (CS > 1 ? 1 : 0);
     static const bool full_smem = std::getenv("PSCONV_FULL_SMEM") != nullptr;
     if (full_smem) cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR>, prm, a, b, blo, o));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, FUSED>, prm, a, b, blo, o));
   }
 }
 
-template <bool SPLIT3, int CS>
+template <bool SPLIT3, int CS, bool FUSED>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_conv<16, SPLIT3, CS>(P, prm, a, b, blo, o, st);
-    case 32: return launch_conv<32, SPLIT3, CS>(P, prm, a, b, blo, o, st);
-    case 64: return launch_conv<64, SPLIT3, CS>(P, prm, a, b, blo, o, st);
-    case 128: return launch_conv<128, SPLIT3, CS>(P, prm, a, b, blo, o, st);
-    case 256: return launch_conv<256, SPLIT3, CS>(P, prm, a, b, blo, o, st);
+    case 16: return launch_conv<16, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
+    case 32: return launch_conv<32, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
+    case 64: return launch_conv<64, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
+    case 128: return launch_conv<128, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
+    case 256: return launch_conv<256, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported bn");
   }
 }
@@ -397,8 +397,12 @@ template <bool SPLIT3>
 void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (cs) {
-    case 1: return dispatch_bn<SPLIT3, 1>(bn, P, prm, a, b, blo, o, st);
-    case 2: return dispatch_bn<SPLIT3, 2>(bn, P, prm, a, b, blo, o, st);
+    case 1:
+      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 1, true>(bn, P, prm, a, b, blo, o, st)
+                                  : dispatch_bn<SPLIT3, 1, false>(bn, P, prm, a, b, blo, o, st);
+    case 2:
+      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 2, true>(bn, P, prm, a, b, blo, o, st)
+                                  : dispatch_bn<SPLIT3, 2, false>(bn, P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported cluster size");
   }
 }
@@ -521,7 +525,6 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.k_outer = pos[1] == 0 ? 1 : 0;
   prm.m_block = s.m_block;
   prm.tap_dw = P->fold ? P->fold_g : 1;
-  prm.tap_phases = P->fold ? P->fold_phases : 1;
   prm.ksteps = Cb * R * S;
   prm.kps = s.kps;
   prm.cb_group = Cb % s.kps == 0 ? 1 : 0;
@@ -636,10 +639,9 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
           throw ConfigError("fold:C needs nIfm = gemm_block = 16, C <= 8 and kw > 1");
         kd.kw = (d.kw + fold_g - 1) / fold_g;
         // the folded copy carries the left padding. (Splitting it into stride_w
-        // column-phase planes read at unit stride is supported by the kernel --
-        // tap_dw / tap_phases -- but measured slower on the stem: 848 vs 639 us
-        // for the conv, 728 vs 637 us for the fold; TMA element strides fetch
-        // only the used 64-B rows, so there is no waste to remove.)
+        // column-phase planes read at unit stride measured slower on the stem --
+        // 848 vs 639 us for the conv: TMA element strides fetch only the used
+        // 64-B rows, so there is no waste to remove; fold_phases stays 1.)
         fold_phases = 1;
         kd.ifw = d.ifw + d.pad_w;
         kd.pad_w = 0;

@@ -85,9 +85,6 @@ struct ConvParams {
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
-  int tap_phases;                 // folded input split into this many column-phase planes
-                                  // (the A map's channel-block dim): tap ki reads plane
-                                  // (ki*tap_dw) % phases at column (ki*tap_dw) / phases
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -398,7 +395,9 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
   }
 }
 
-template <int BN, bool SPLIT3, bool PAIR>
+// FUSED: bias / ReLU epilogue compiled in (a separate instantiation: the runtime
+// checks alone cost 5% on epilogue-heavy layers, measured on l1 1x1 64->256)
+template <int BN, bool SPLIT3, bool PAIR, bool FUSED>
 __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
@@ -497,6 +496,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // cb_group: one coordinate step per stage, boxes span kps channel blocks;
     // otherwise kps coordinate steps per stage (the last stage may be partial)
     const int nsub = p.cb_group ? 1 : p.kps;
+    const int tap_dw = p.tap_dw;
     const int cb_mul = p.cb_group ? p.kps : 1;
     const int d0 = p.kord[0], d1 = p.kord[1], d2 = p.kord[2];
     const int e1 = d1 == 0 ? p.cbg : (d1 == 1 ? p.R : p.S);
@@ -524,21 +524,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           const int r = d0 == 1 ? v0 : (d1 == 1 ? v1 : v2);
           const int s = d0 == 2 ? v0 : (d1 == 2 ? v1 : v2);
           const int rs = r * p.S + s;
-          int tw = s, tc_ = 0;  // tap column offset / phase plane
-          if (p.tap_phases > 1) {
-            tw = (s * p.tap_dw) / p.tap_phases;
-            tc_ = (s * p.tap_dw) % p.tap_phases;
-          } else if (p.tap_dw > 1) {
-            tw = s * p.tap_dw;
-          }
+          const int tw = s * tap_dw;  // input column of tap ki (tap dilation of the fold)
           if (issuer) {
             uint8_t* sa = sb + j * p.a_boxes * p.a_pitch;
             uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes;
             if (!PAIR) {
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0,
-                                   cb + i + tc_);
+                  ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0, cb + i);
               ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb >> p.b128);
               if (SPLIT3)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
@@ -547,7 +540,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               const uint32_t fb = full_leader + 8u * stage;
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
-                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + tw, hp + r, n0, cb + i + tc_);
+                  ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + tw, hp + r, n0, cb + i);
               ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
             }
           }
@@ -728,6 +721,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           } else if (tc.live) {
             // fused epilogue on the finished sum: + bias[k], ReLU (the same
             // value for all lanes: broadcast loads through L1)
+            if constexpr (FUSED) {
             if (p.bias != nullptr) {
               const float* bj = p.bias + tc.tk * BN + j * DW;
 #pragma unroll
@@ -736,6 +730,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             if (p.relu) {
 #pragma unroll
               for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(fmaxf(__uint_as_float(v[i]), 0.f));
+            }
             }
 #pragma unroll
             for (int blk = 0; blk < DW / 16; ++blk) {
