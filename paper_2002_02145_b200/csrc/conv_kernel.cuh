@@ -112,7 +112,8 @@ constexpr int kHaloB = 8;  // halo mode: B-ring barriers follow 8 A-ring slots
 // PSCONV_DEBUG=7 on cfg1), which exceeded the 64-cycle MMA time of a BN=64
 // k-step; grouping amortises it over kps k-steps.
 constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
-constexpr int kStageBudget = 227 * 1024 - 2 * kOutStageBytes - 2048 - 1024;
+constexpr int kOutStages = 4;             // staging blocks: two rounds of 32 channels in flight
+constexpr int kStageBudget = 227 * 1024 - kOutStages * kOutStageBytes - 2048 - 1024;
 constexpr int kMaxStages = 16;
 
 template <int BN, bool SPLIT3, bool PAIR>
@@ -134,8 +135,10 @@ struct KernelCfg {
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
-      kStageBudget + 2 * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
-  static constexpr int smem_bytes(int ring_bytes) { return ring_bytes + 2 * kOutStageBytes + kBarBytes + 1024; }
+      kStageBudget + kOutStages * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
+  static constexpr int smem_bytes(int ring_bytes) {
+    return ring_bytes + kOutStages * kOutStageBytes + kBarBytes + 1024;
+  }
   static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
@@ -419,8 +422,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   auto stage_base = [&](int s) { return smem + s * p.stage_bytes; };
 
-  uint8_t* out_stage = smem + p.ring_bytes;  // 2 x 8 KB (1024-B aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.ring_bytes + 2 * Cfg::kOutStageBytes);
+  uint8_t* out_stage = smem + p.ring_bytes;  // kOutStages x 8 KB (1024-B aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.ring_bytes + kOutStages * Cfg::kOutStageBytes);
   uint64_t* full = bars;                         // own TMA landed (1 arrive + tx)
   uint64_t* split_full = bars + kMaxStages;      // own splitter done (count 128)
   uint64_t* empty = bars + 2 * kMaxStages;       // MMA consumed the stage (commit, pair: both CTAs)
@@ -732,32 +735,40 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(fmaxf(__uint_as_float(v[i]), 0.f));
             }
             }
+            // one staging round = the DW/16 blocks of this TMEM load: one
+            // barrier pair and one bulk group per round, kOutStages/(DW/16)
+            // rounds in flight
+            constexpr int kBlk = DW / 16;
+            constexpr int kRounds = kOutStages / kBlk;
+            uint8_t* st = out_stage + ostage * (kBlk * Cfg::kOutStageBytes);
+            if (store_thread) ptx::bulk_wait_read<kRounds - 1>();  // this round's buffers read out
+            ptx::named_bar(1, 128);
+            if (row_valid) {
 #pragma unroll
-            for (int blk = 0; blk < DW / 16; ++blk) {
-              uint8_t* st = out_stage + ostage * Cfg::kOutStageBytes;
-              // staging buffer free? (the store issued two blocks ago has read it)
-              if (store_thread) ptx::bulk_wait_read<1>();
-              ptx::named_bar(1, 128);
-              if (row_valid) {
+              for (int blk = 0; blk < kBlk; ++blk) {
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
                   const int b = blk * 16 + 4 * c4;
                   const uint32_t off = row_off + ((static_cast<uint32_t>(c4) ^ row_swz) << 4);
-                  *reinterpret_cast<uint4*>(st + off) = make_uint4(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
+                  *reinterpret_cast<uint4*>(st + blk * Cfg::kOutStageBytes + off) =
+                      make_uint4(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
                 }
               }
-              ptx::fence_proxy_async_smem();
-              ptx::named_bar(1, 128);
-              if (store_thread && !(p.debug & 4)) {
-                const int kb = kb0 + j * (DW / 16) + blk;
-                if (p.accumulate)
-                  ptx::tma_reduce_add_5d(&tmap_out, st, 0, q0, p0, kb, n0);
-                else
-                  ptx::tma_store_5d(&tmap_out, st, 0, q0, p0, kb, n0);
-                ptx::bulk_commit();
-              }
-              ostage ^= 1;
             }
+            ptx::fence_proxy_async_smem();
+            ptx::named_bar(1, 128);
+            if (store_thread && !(p.debug & 4)) {
+#pragma unroll
+              for (int blk = 0; blk < kBlk; ++blk) {
+                const int kb = kb0 + j * kBlk + blk;
+                if (p.accumulate)
+                  ptx::tma_reduce_add_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
+                else
+                  ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
+              }
+              ptx::bulk_commit();
+            }
+            ostage = ostage + 1 == kRounds ? 0 : ostage + 1;
           }
         }
         if (!last) ptx::tmem_wait_st();

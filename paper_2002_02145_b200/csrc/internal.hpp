@@ -86,7 +86,7 @@ struct Schedule {
 Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gpu = true);
 
 // Shared-memory pipeline geometry (conv_kernel.cuh): k-steps per stage and ring depth.
-constexpr int kSmemStageBudget = 227 * 1024 - 2 * 128 * 64 - 2048 - 1024;
+constexpr int kSmemStageBudget = 227 * 1024 - 4 * 128 * 64 - 2048 - 1024;  // == conv_kernel.cuh kStageBudget
 constexpr int kSmemMaxStages = 16;
 int stage_bytes(const Schedule& s, int mode);  // bytes of one stage of s.kps k-steps
 void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg);  // throws ConfigError
