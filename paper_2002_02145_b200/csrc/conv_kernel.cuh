@@ -712,11 +712,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             if constexpr (DW == 32) ptx::tmem_ld32(tsum + j * 32, sacc);
             else ptx::tmem_ld16(tsum + j * 16, sacc);
             ptx::tmem_wait_ld();
+            ptx::reg_fence(v);
+            ptx::reg_fence(sacc);
 #pragma unroll
             for (int i = 0; i < DW; ++i)
               v[i] = __float_as_uint(__uint_as_float(sacc[i]) + __uint_as_float(v[i]));
           } else {
             ptx::tmem_wait_ld();
+            ptx::reg_fence(v);
           }
           if (!last) {
             if constexpr (DW == 32) ptx::tmem_st32(tsum + j * 32, v);
