@@ -107,6 +107,7 @@ __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __re
                                       float* __restrict__ lo, int K, int CRS, int RS, int split,
                                       int b128) {
   __shared__ float tile[16][17];
+  ptx::griddep_launch_dependents();  // the conv kernel may start its prologue now
   const int blk = blockIdx.x;  // = kb * CRS + crs, crs = cb * RS + rs
   const int kb = blk / CRS, crs = blk % CRS;
   const int t = threadIdx.x;
@@ -270,6 +271,7 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
 // one 16-B load per tap (C <= 4) or two (C <= 8).
 __global__ void fold_input_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n_px,
                                   int H, int W, int Wq, int phases, int pw, int C, int G) {
+  ptx::griddep_launch_dependents();
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_px;
        e += int64_t(gridDim.x) * blockDim.x) {
     int64_t t = e;
@@ -366,16 +368,25 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     cfg.blockDim = dim3(Cfg::kThreads);
     cfg.dynamicSmemBytes = Cfg::smem_bytes(prm.ring_bytes);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    // programmatic stream serialization (PDL): the prologue overlaps the
+    // preceding kernel; the producer's griddepcontrol.wait orders the operands
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    static const bool no_pdl = std::getenv("PSCONV_NO_PDL") != nullptr;
+    if (!no_pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (CS > 1) {  // plain launch for single-CTA clusters
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = CS;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    static const int force_cl = std::getenv("PSCONV_CL_ATTR") ? std::atoi(std::getenv("PSCONV_CL_ATTR")) : -1;
-    cfg.numAttrs = force_cl >= 0 ? force_cl : (CS > 1 ? 1 : 0);
-    static const bool full_smem = std::getenv("PSCONV_FULL_SMEM") != nullptr;
-    if (full_smem) cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.numAttrs = na;
     CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, FUSED>, prm, a, b, blo, o));
   }
 }

@@ -481,6 +481,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       ptx::prefetch_tmap(&tmap_flt);
       if (SPLIT3) ptx::prefetch_tmap(&tmap_flt_lo);
     }
+    // all global-memory operands come from earlier kernels in the stream (PDL)
+    ptx::griddep_wait();
     __syncwarp();
     if (p.halo) {
       halo_producer<BN, SPLIT3, PAIR>(p, smem, full, empty, cluster, nclusters, rank, leader,
