@@ -180,7 +180,7 @@ def cpu_leg(workload, conv, c_logical, sx, sw, reps, warmup):
     what = ("reference emitted Fig.5 driver (oracle/_ref, emit.hpp:60-134) + plain-C band microkernel"
             if kind == "reference" else "oracle port (oracle/oracle.c Fig.5 restatement)")
     return {"value": round(flops / mean / 1e9, 3), "unit": "GFLOP/s", "cores": oracle.threads(),
-            "kind": kind, "best_value": round(flops / best / 1e9, 3),
+            "kind": kind, "best_value": round(flops / best / 1e9, 3), "ms_per_rep": round(mean * 1e3, 3),
             "sample": f"{n} of {p_full.nImg} images of {workload} ({flops / 1e9:.2f} GFLOP), "
                       f"{reps} reps after {warmup} warm-up, gcc -O3 OpenMP over img; {what}",
             "cpu_model": _cpu_model()}
@@ -442,7 +442,8 @@ def run_reference(args, rank, world):
     v = leg["value"]
     return {
         "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": leg["ms_per_rep"], "higher_is_better": True,
+        "scaling": "strong", "step": "one rep of the bounded CPU sample (see cpu_baseline.sample)",
         "vs_baseline": None, "dtype": "f32", "impl": "reference",
         "data": "synthetic: seeded uniform[-1,1) by logical NCHW/KCRS index (BASELINE configs)",
         "config": {"workload": f"{args.workload} {conv}", "mode": "fp32 CPU"},
