@@ -552,8 +552,14 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.a_boxes = (prm.cb_group && a_packed) ? 1 : (prm.cb_group ? s.kps : 1);
     prm.a_pitch = (prm.cb_group && a_packed) ? rows * 64 : 8192;
     prm.a_lo_off = s.kps * 8192;
-    prm.b_off = s.kps * 8192 * mult;
+    prm.b_off = s.kps * 8192 * (s.tmem_a ? 1 : mult);
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
+    prm.tmem_a = s.tmem_a;
+    if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
+      prm.a_slot_col = (3 * s.bn + 31) / 32 * 32;
+      prm.a_slots = std::min(kMaxStages, (512 - prm.a_slot_col) / 32);
+      if (prm.a_slots < s.kps) throw RuntimeError("internal: TMEM A ring smaller than a stage");
+    }
     prm.ring_bytes = (prm.stages * prm.stage_bytes + 1023) / 1024 * 1024;
     if (s.halo) {
       const HaloGeom h = halo_geom(d, s, P->mode);

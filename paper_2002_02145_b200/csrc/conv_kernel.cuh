@@ -65,6 +65,11 @@ struct ConvParams {
   int ring_bytes;                 // stages * stage_bytes rounded up to 1 KB
   int a_pitch;                    // bytes between the kps A tiles of a stage
   int b128;                       // filter rows hold 2 channel blocks (128 B, SWIZZLE_128B)
+  int tmem_a;                     // 3xTF32, BN <= 128: A_hi / A_lo live in TMEM (the splitter
+                                  // writes them with tcgen05.st, the MMAs read A from TMEM):
+                                  // no A_lo round trip through smem, no smem reads of A by
+                                  // the three MMAs per K-half
+  int a_slots, a_slot_col;        // TMEM A ring: slots of 32 columns (hi 16 | lo 16) from col
   // halo mode (stride-1 R x S > 1): the M tile is Pb whole output rows of one
   // image laid out at the padded input pitch hw = Q + S - 1 (columns q >= Q
   // are junk rows); one TMA box loads the input halo (hr = Pb + R - 1 rows of
@@ -127,7 +132,9 @@ struct KernelCfg {
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
   static constexpr int kSumCol = kAccBufs * BN;
   static constexpr int kColsNeeded = kAccBufs * BN + (SPLIT3 ? BN : 0);
-  static constexpr int kTmemCols = kColsNeeded <= 32    ? 32
+  // 3xTF32 at BN <= 128 takes all 512 columns: the rest hold the TMEM A ring
+  static constexpr int kTmemCols = (SPLIT3 && BN <= 128) ? 512
+                                   : kColsNeeded <= 32    ? 32
                                    : kColsNeeded <= 64  ? 64
                                    : kColsNeeded <= 128 ? 128
                                    : kColsNeeded <= 256 ? 256
@@ -144,7 +151,7 @@ struct KernelCfg {
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
   static_assert(2 * (kABytes + kBBytes) * (SPLIT3 ? 2 : 1) <= kStageBudget, "two stages of one k-step");
   static_assert(kSmemBytes <= 227 * 1024, "smem");
-  static_assert(4 * kMaxStages * 8 + 4 * 8 + 4 <= kBarBytes, "barriers");
+  static_assert(4 * kMaxStages * 8 + 4 * 8 + 4 <= kBarBytes, "barriers");  // full/split/empty/aslot + acc
   static_assert(kColsNeeded <= 512, "TMEM");
   // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
   // a cluster-scope release per k-step (MEMBAR.GPU, measured ~3x slower).
@@ -429,7 +436,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   uint64_t* empty = bars + 2 * kMaxStages;       // MMA consumed the stage (commit, pair: both CTAs)
   uint64_t* acc_full = bars + 3 * kMaxStages;    // chunk accumulator ready   [kAccBufs]
   uint64_t* acc_empty = acc_full + 2;            // chunk accumulator drained [kAccBufs] (4 warps x CS)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* aslot_empty = acc_empty + 2;         // TMEM A slot consumed by the MMA [kMaxStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aslot_empty + kMaxStages);
 
   const int warp = threadIdx.x >> 5;
   const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
@@ -453,6 +461,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       ptx::mbar_init(&acc_full[a], 1);
       ptx::mbar_init(&acc_empty[a], 4 * CS);
     }
+    for (int a = 0; a < (p.tmem_a ? p.a_slots : 0); ++a) ptx::mbar_init(&aslot_empty[a], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
@@ -589,6 +598,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const int kps = p.kps;
     const bool skip_mma = (p.debug & 2) != 0;
     int stage = 0, gs = 0;
+    int aslot = 0;  // TMEM A ring position (3xTF32 tmem_a)
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
     for (int g = cluster; g < p.groups; g += nclusters) {
@@ -610,12 +620,36 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
           ptx::tc_fence_after();
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
+          const int nk = min(kps, p.ksteps - it * kps);  // partial last stage (cb_group = 0)
           if (ptx::elect_one()) {
             uint64_t da = desc0 + static_cast<uint64_t>(stage) * stage_desc;
             uint64_t db = bdesc0 + static_cast<uint64_t>(stage) * stage_desc + b_off;
             uint32_t acc_in = it == it0 ? 0u : 1u;
-            const int nk = min(kps, p.ksteps - it * kps);  // partial last stage (cb_group = 0)
-            for (int j = 0; j < nk && !skip_mma; ++j) {
+            int aslot_j = aslot;  // (state lives outside the elected lane: any lane may be elected)
+            for (int j = 0; j < nk && (!skip_mma || p.tmem_a); ++j) {
+              if constexpr (SPLIT3 && BN <= 128) {
+                if (p.tmem_a) {  // A_hi / A_lo from the TMEM slot of this k-step
+                  const uint32_t ah = tmem_base + static_cast<uint32_t>(p.a_slot_col + aslot_j * 32);
+                  const uint64_t db_lo = db - b_off + blo_off;
+#ifdef PSCONV_DBG_PRINT
+                  if (blockIdx.x == 0)
+                    printf("mma it=%d j=%d stage=%d aslot=%d ah=%u db=%llx dblo=%llx acc_in=%u d=%u\n", it, j, stage, aslot_j,
+                           ah, (unsigned long long)db, (unsigned long long)db_lo, acc_in, d_tmem);
+#endif
+#pragma unroll
+                  for (int h = 0; h < 2 && !skip_mma; ++h) {
+                    ptx::mma_tf32_ts(d_tmem, ah + 16 + h * 8, db + h * 2, kIdesc, acc_in);  // small terms first
+                    ptx::mma_tf32_ts(d_tmem, ah + h * 8, db_lo + h * 2, kIdesc, 1u);
+                    ptx::mma_tf32_ts(d_tmem, ah + h * 8, db + h * 2, kIdesc, 1u);
+                    acc_in = 1u;
+                  }
+                  ptx::mma_commit(&aslot_empty[aslot_j]);
+                  if (++aslot_j == p.a_slots) aslot_j = 0;
+                  da += a_step;
+                  db += (j & 1) ? b_odd : b_even;
+                  continue;
+                }
+              }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 if (SPLIT3) {
@@ -640,6 +674,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               ptx::mma_commit(&empty[stage]);
           }
           __syncwarp();
+          if (SPLIT3 && p.tmem_a) aslot = (aslot + nk) % p.a_slots;  // warp-uniform ring position
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 2] = clock64();
           ++gs;
           if (++stage == kStages) {
@@ -812,6 +847,61 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             phase ^= 1;
           }
         }
+    } else if (SPLIT3 && BN <= 128 && p.tmem_a) {
+      // TMEM A: each thread owns one pixel row (TMEM lane = warp quadrant x 32 +
+      // lane), reads its 16 channels from the swizzled smem tile and writes
+      // hi = x (the MMA truncates) and lo = x - trunc(x) into a 32-column slot
+      const int lane = threadIdx.x & 31;
+      const int quad = (threadIdx.x >> 5) & 3;
+      const int row = quad * 32 + lane;
+      const uint32_t row_off = static_cast<uint32_t>(row) * 64u;
+      const uint32_t row_swz = (static_cast<uint32_t>(row) >> 1) & 3u;
+      const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+      int slot = 0;
+      uint32_t sph = 0;
+      for (int g = cluster; g < p.groups; g += nclusters) {
+        for (int it = 0; it < nst; ++it) {
+          ptx::mbar_wait(&full[stage], phase);
+          const int nk = min(p.kps, p.ksteps - it * p.kps);
+          for (int j = 0; j < nk; ++j) {
+            ptx::mbar_wait(&aslot_empty[slot], sph ^ 1);  // the MMAs of slot's last use retired
+            ptx::tc_fence_after();
+            const uint8_t* a = stage_base(stage) + j * p.a_pitch + row_off;
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint4 x = *reinterpret_cast<const uint4*>(a + ((static_cast<uint32_t>(c4) ^ row_swz) << 4));
+              const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[c4 * 4 + e] = xs[e];
+                lo[c4 * 4 + e] = __float_as_uint(__uint_as_float(xs[e]) -
+                                                 __uint_as_float(xs[e] & 0xFFFFE000u));
+              }
+            }
+            const uint32_t col = lane_base + static_cast<uint32_t>(p.a_slot_col + slot * 32);
+#ifdef PSCONV_DBG_PRINT
+            if (blockIdx.x == 0 && (row == 0 || row == 1))
+              printf("split it=%d j=%d stage=%d slot=%d row=%d col=%u a0=%f a1=%f lo0=%e sb_off=%d\n", it, j, stage, slot, row,
+                     col, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(lo[0]),
+                     int(stage_base(stage) - smem));
+#endif
+            ptx::tmem_st16(col, hi);
+            ptx::tmem_st16(col + 16, lo);
+            if (++slot == p.a_slots) {
+              slot = 0;
+              sph ^= 1;
+            }
+          }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&split_full[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     } else
     for (int g = cluster; g < p.groups; g += nclusters) {
       for (int it = 0; it < nst; ++it) {

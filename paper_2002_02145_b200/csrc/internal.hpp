@@ -56,6 +56,7 @@ struct Recipe {
   int halo = 0;                                               // 1: halo mode (stride-1 R x S)
   int gm = -1;                                                // grouped raster block, -1 = auto
   int fold = 0;                                               // (c,s) fold: C real channels
+  int ta = -1;                                                // TMEM-resident A: -1 auto, 0/1
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -76,6 +77,8 @@ struct Schedule {
   int halo = 0;        // halo mode: Pb whole output rows, input halo loaded once per block
   int m_block = 0;     // grouped raster block (M groups); 0 = the recipe's loop order
   int hb_stages = 0;   // halo: B-ring stages
+  int tmem_a = 0;      // 3xTF32, bn <= 128, not halo: A_hi/A_lo in TMEM (no A_lo smem region)
+  int ta = -1;         // recipe request for tmem_a (-1 auto)
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;

@@ -16,6 +16,7 @@
 //   * tile=oj:T  -> T output rows per 128-pixel tile (box P extent);
 //     tile=img:T -> T images per tile; tile=ofm_tile:T -> BN = 16*T channels.
 #include <algorithm>
+#include <cstdlib>
 #include <cctype>
 #include <map>
 #include <set>
@@ -100,6 +101,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
           if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
+        } else if (key == "ta") {
+          r.ta = static_cast<int>(parse_int(val, "gpu TMEM-resident A"));
+          if (r.ta != 0 && r.ta != 1) throw ConfigError("gpu ta must be 0 or 1");
         } else if (key == "fold") {
           r.fold = static_cast<int>(parse_int(val, "gpu fold channels"));
           if (r.fold < 1 || r.fold > 8) throw ConfigError("gpu fold must be in [1, 8] (real input channels)");
@@ -139,6 +143,7 @@ std::string Recipe::id() const {
     if (halo) s += ",halo:1";
     if (gm >= 0) s += ",gm:" + std::to_string(gm);
     if (fold) s += ",fold:" + std::to_string(fold);
+    if (ta >= 0) s += ",ta:" + std::to_string(ta);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -296,6 +301,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.box_n = s.nb;
   canon.halo = s.halo;
   canon.fold = r.fold;
+  canon.ta = r.ta;
+  s.ta = r.ta;
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
@@ -345,6 +352,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
 
 int stage_bytes(const Schedule& s, int mode) {
   const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
+  // TMEM-A stages hold A once (its lo part lives in TMEM) and B hi + lo
+  if (s.tmem_a) return s.kps * (128 * 64 + (s.bn / s.cs) * 64 * 2);
   return s.kps * (128 * 64 + (s.bn / s.cs) * 64) * mult;
 }
 
@@ -377,6 +386,15 @@ HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode) {
 
 void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   const int Cb = static_cast<int>(d.nIfm / 16);
+  // TMEM-resident A (3xTF32, bn <= 128, not halo): default at bn <= 64, where the
+  // three MMAs per K-half are smem-read bound (cfg1 69.6 -> 56.8 us, l1 3x3 499 ->
+  // 390 us); at bn 128 only 4 slots fit beside the accumulators (l2 3x3 312 ->
+  // 339 us), so it is a tuner option there (recipe ta:1)
+  {
+    const bool ok = mode == PSCONV_MODE_3XTF32 && s.bn <= 128 && !s.halo;
+    const bool want = s.ta == 1 || (s.ta < 0 && s.bn <= 64);
+    s.tmem_a = (ok && want && std::getenv("PSCONV_NO_TMEMA") == nullptr) ? 1 : 0;
+  }
   if (s.halo) {
     // A ring of 2 halo stages, the rest B stages (<= 8 each); largest kps in
     // {4, 2, 1} dividing Cb that leaves >= 3 B stages

@@ -125,9 +125,12 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const bool b128 = s.kps % 2 == 0 && g.Cb % std::max(1, s.kps) == 0;
   const double rows = double(s.qb) * s.pb * s.nb + b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0);
   const double del_cyc = rows / m.row_requests_per_cycle;
-  const double tc_reads = 2.0 * mult * (4096.0 + b_rows * 32.0);
+  // operand reads per k-step: 2 K-halves x (A 4 KB + B rows x 32 B) per MMA; with
+  // TMEM-resident A (3xTF32) the MMAs read only B and the splitter reads A once
+  const double tc_reads = 2.0 * mult * ((s.tmem_a ? 0.0 : 4096.0) + b_rows * 32.0);
+  const double split_b = mult > 1 ? (s.tmem_a ? 8192.0 * 0.5 : 4096.0) : 0.0;
   // (the splitter's LSU traffic only partly competes with the async-proxy traffic)
-  const double smem_cyc = 0.94 * (tc_reads + deliver_b + (mult > 1 ? 4096.0 : 0.0)) / 128.0;
+  const double smem_cyc = 0.94 * (tc_reads + deliver_b + split_b) / 128.0;
   const double busy = std::max(mma_cyc, smem_cyc);
   const double other = std::min(mma_cyc, smem_cyc);
   double kstep_cyc = busy * std::pow(1.0 + std::pow(other / busy, 4.0), 0.25);

@@ -29,6 +29,8 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     if mode == "tf32":
         alts.append({**kv, "cl": "1" if kv.get("cl") == "2" else "2"})
     bn = int(kv["bn"])
+    if mode == "3xtf32" and bn == 128:  # TMEM-resident A is opt-in at bn 128
+        alts.append({**kv, "ta": "1"})
     for nb in (bn * 2, bn // 2):
         if 16 <= nb <= 256 and preset.nOfm % nb == 0:
             alt = {**kv, "bn": str(nb)}

@@ -281,3 +281,19 @@ def test_cs_fold(conv, c_log, recipe, mode):
     _check("fold", conv, c_log, 14, mode, n, recipe)
     if mode == "tf32":
         _check("fold-pair", conv, c_log, 14, mode, n, recipe + ",cl:2")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,kg:1,ta:1"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:7x3x2,kg:4,ta:1"),
+    ("conv:2,128,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:128,box:2x4x16,ta:1"),
+    ("conv:2,128,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:128,box:2x4x16,ta:0"),
+    ("conv:2,32,48,9,9,3,3,1,1,16,1,1,9,9", 48, "gpu=bn:16,box:9x9x1,kg:4,ta:1"),
+    ("conv:300,64,32,8,16,1,1,1,1,16,0,0,8,16", 32, "gpu=bn:64,box:16x8x1,ta:1,ch:1"),
+])
+def test_tmem_resident_a(conv, c_log, recipe):
+    """3xTF32 with A_hi / A_lo in TMEM (splitter tcgen05.st, MMAs read A from TMEM): slot
+    ring wrap-around, partial stages, unaligned boxes, many tiles, chunked sums."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("tmem-a", conv, c_log, 15, "3xtf32", n, recipe)
