@@ -117,7 +117,10 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const double a_box = double(s.qb) * s.pb * s.nb * 64.0;
   const double b_rows = double(s.bn) / cs;
   const double deliver_b = a_box + b_rows * 64.0 * (mult > 1 ? 2 : 1);
-  const double mma_cyc = s.bn * mult;
+  // MMA: two K=8 MMAs per k-step (x3 for 3xTF32) of max(BN/2, 46) cycles each --
+  // an M=128 tf32 MMA takes >= ~46 cycles whatever N (tools/probe_mma_rate.cu:
+  // N=64 48, N=128 64, N=256 128 cycles)
+  const double mma_cyc = 2.0 * mult * std::max(s.bn / 2.0, 46.0);
   // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows
   // per cycle per SM with every SM loading, for 64-B and 128-B rows alike
   // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows

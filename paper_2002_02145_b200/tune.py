@@ -31,9 +31,11 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     bn = int(kv["bn"])
     if mode == "3xtf32" and bn == 128:  # TMEM-resident A is opt-in at bn 128
         alts.append({**kv, "ta": "1"})
-    for nb in (bn * 2, bn // 2):
+    widest = max(c for c in (16, 32, 64, 128, 256) if preset.nOfm % c == 0)
+    for nb in (bn * 2, bn // 2, widest):
         if 16 <= nb <= 256 and preset.nOfm % nb == 0:
             alt = {**kv, "bn": str(nb)}
+            alt.pop("ta", None)
             if mode == "3xtf32":
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
