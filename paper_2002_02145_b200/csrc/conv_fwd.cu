@@ -833,7 +833,9 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     if (!P->pipe) {  // ~32 MB of input per chunk, double buffered
       auto* h = new conv_plan::HostPipe();
       P->pipe = h;
-      h->chunk = std::max<int64_t>(1, std::min<int64_t>(d.nImg, (int64_t(32) << 20) / (in_img * 4)));
+      int64_t chunk_mb = 32;
+      if (const char* e = std::getenv("PSCONV_HOST_CHUNK_MB")) chunk_mb = std::max(1, std::atoi(e));
+      h->chunk = std::max<int64_t>(1, std::min<int64_t>(d.nImg, (chunk_mb << 20) / (in_img * 4)));
       for (int i = 0; i < 2; ++i) {
         CUDA_OK(cudaMalloc(&h->din[i], h->chunk * in_img * sizeof(float)));
         CUDA_OK(cudaMalloc(&h->dout[i], h->chunk * out_img * sizeof(float)));
