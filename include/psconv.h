@@ -131,6 +131,18 @@ typedef struct conv_plan conv_plan;
 
 int conv_plan_create(const conv_desc* d, int mode, int device, const char* recipe_or_null,
                      conv_plan** out);
+
+/* Backward-data plan (neighbouring ops): for the FORWARD
+ * descriptor d (stride 1), a plan whose conv_fwd / conv_fwd_host computes
+ * dX = dL/dInput from dY = dL/dOutput and the forward filter:
+ *   in  = dY  [N][nOfm/16][ofh][ofw][16]   (NKPQ16k of the forward output)
+ *   flt = W   KCRS16c16k of the forward layer (transposed and flipped inside)
+ *   out = dX  [N][nIfm/16][ifh][ifw][16]   (NCHW16c of the forward input)
+ * i.e. the transposed convolution conv(dY, W^T flipped, pad = k - 1 - pad) on the
+ * same kernel; conv_plan_recipe reports the transposed layer's schedule.
+ * Returns 0 / 2 (stride > 1) / 1. */
+int conv_plan_create_bwd_data(const conv_desc* d, int mode, int device, const char* recipe_or_null,
+                              conv_plan** out);
 void conv_plan_destroy(conv_plan* p);
 
 /* The plan's recipe id in the reference's grammar plus the gpu clause. */

@@ -156,16 +156,20 @@ class ConvPlan:
     """One conv layer bound to a device, a mode and a schedule (recipe)."""
 
     def __init__(self, preset: ConvPreset, mode="3xtf32", device: int = 0,
-                 recipe: str | None = None):
+                 recipe: str | None = None, bwd_data: bool = False):
+        """bwd_data=True: the backward-data plan of the (stride-1) forward layer `preset`;
+        forward(dy, w, dx) then computes dX from dY (NKPQ16k) and the forward filter."""
         if isinstance(mode, str):
             mode = _MODES[mode.lower()]
         self.preset = ConvPreset(**{f.name: getattr(preset, f.name) for f in fields(preset)}).validate()
         self.mode = mode
         self.device = device
+        self.bwd_data = bwd_data
         self._d = self.preset.to_c()
         h = ctypes.c_void_p()
-        _check(lib.conv_plan_create(ctypes.byref(self._d), mode, device,
-                                    recipe.encode() if recipe else None, ctypes.byref(h)))
+        create = lib.conv_plan_create_bwd_data if bwd_data else lib.conv_plan_create
+        _check(create(ctypes.byref(self._d), mode, device, recipe.encode() if recipe else None,
+                      ctypes.byref(h)))
         self._h = h
 
     @property

@@ -49,6 +49,8 @@ _sigs = {
                                         _P(c_vp)]),
     "conv_plan_destroy": (None, [c_vp]),
     "conv_plan_recipe": (ctypes.c_char_p, [c_vp]),
+    "conv_plan_create_bwd_data": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                                  ctypes.POINTER(c_vp)]),
     "conv_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, ctypes.c_uint]),
     "conv_model_stats": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_char_p,
                                          ctypes.POINTER(ctypes.c_double)]),

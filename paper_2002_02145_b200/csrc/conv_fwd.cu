@@ -36,6 +36,12 @@ struct conv_plan {
   conv_desc kd{};                 // kernel descriptor (== d unless folded)
   float* xfold = nullptr;         // [nImg][phases][H][Wq][16]
   float* wfold = nullptr;         // folded filter, KCRS16c16k of kd
+  // backward-data plan (conv_plan_create_bwd_data): d is the TRANSPOSED stride-1
+  // convolution dX = conv(dY, W^T flipped); the forward filter is transformed
+  // into wtrans before the repack
+  bool bwd_data = false;
+  conv_desc fwd{};                // the forward layer's descriptor
+  float* wtrans = nullptr;
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
   // conv_fwd_host staging (lazily created): double-buffered device chunks,
@@ -248,7 +254,13 @@ __global__ void unpack_output_kernel(const float* __restrict__ in16, float* __re
 void launch_fold_filter(const conv_plan* P, const float* flt, cudaStream_t st);
 int grid_for(int64_t n);
 
+void launch_bwd_filter(const conv_plan* P, const float* flt, cudaStream_t st);
+
 void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
+  if (P->bwd_data) {
+    launch_bwd_filter(P, flt, st);
+    flt = P->wtrans;
+  }
   if (P->fold) {
     launch_fold_filter(P, flt, st);
     flt = P->wfold;
@@ -329,6 +341,35 @@ __global__ void fold_filter_kernel(const float* __restrict__ flt, float* __restr
     if (sp < G && sx < S) v = flt[((kb * R + r) * S + sx) * 256 + c * 16 + k16];
     out[e] = v;
   }
+}
+
+// Backward data: the forward filter KCRS16c16k [Kb][Cb][R][S][16c][16k] becomes the
+// filter of the transposed conv, [Cb][Kb][R][S][16k][16c] with the taps flipped:
+// W'[c][k][r][s] = W[k][c][R-1-r][S-1-s].
+__global__ void bwd_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int64_t n_elems,
+                                  int Kb, int Cb, int R, int S) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int c16 = int(t & 15);  // output channel of the transposed conv (forward input c)
+    t >>= 4;
+    const int k16 = int(t & 15);  // its input channel (forward output k)
+    t >>= 4;
+    const int s = int(t % S);
+    t /= S;
+    const int r = int(t % R);
+    t /= R;
+    const int kb = int(t % Kb);
+    const int cb = int(t / Kb);
+    out[e] = w[((((int64_t(kb) * Cb + cb) * R + (R - 1 - r)) * S + (S - 1 - s)) * 16 + c16) * 16 + k16];
+  }
+}
+
+void launch_bwd_filter(const conv_plan* P, const float* flt, cudaStream_t st) {
+  const int64_t n = P->fwd.nOfm * P->fwd.nIfm * P->fwd.kh * P->fwd.kw;
+  bwd_filter_kernel<<<grid_for(n), 256, 0, st>>>(flt, P->wtrans, n, int(P->fwd.nOfm / 16),
+                                                 int(P->fwd.nIfm / 16), int(P->fwd.kh), int(P->fwd.kw));
+  CUDA_OK(cudaGetLastError());
 }
 
 void launch_fold_filter(const conv_plan* P, const float* flt, cudaStream_t st) {
@@ -718,6 +759,55 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
   });
 }
 
+int conv_plan_create_bwd_data(const conv_desc* d_in, int mode, int device, const char* recipe,
+                              conv_plan** out) {
+  return guarded([&] {
+    if (!d_in || !out) throw ConfigError("null argument");
+    *out = nullptr;
+    conv_desc f = *d_in;
+    validate_desc(f);
+    if (f.stride_h != 1 || f.stride_w != 1)
+      throw ConfigError("backward data: only stride-1 layers are supported (stride " +
+                        std::to_string(f.stride_h) + "x" + std::to_string(f.stride_w) + ")");
+    if (f.kh - 1 - f.pad_h < 0 || f.kw - 1 - f.pad_w < 0)
+      throw ConfigError("backward data: padding larger than kernel - 1");
+    // dX = conv(dY, W^T flipped): images stay, channels swap, the output is the
+    // forward input extent, padding kernel - 1 - pad
+    conv_desc t{};
+    t.nImg = f.nImg;
+    t.nOfm = f.nIfm;
+    t.nIfm = f.nOfm;
+    t.ofh = f.ifh;
+    t.ofw = f.ifw;
+    t.kh = f.kh;
+    t.kw = f.kw;
+    t.stride_h = t.stride_w = 1;
+    t.gemm_block = f.gemm_block;
+    t.pad_h = f.kh - 1 - f.pad_h;
+    t.pad_w = f.kw - 1 - f.pad_w;
+    t.ifh = f.ofh;
+    t.ifw = f.ofw;
+    conv_plan* P = nullptr;
+    const int rc = conv_plan_create(&t, mode, device, recipe, &P);
+    if (rc != PSCONV_OK) {
+      if (rc == PSCONV_ERR_CONFIG) throw ConfigError(conv_last_error());
+      throw RuntimeError(conv_last_error());
+    }
+    P->bwd_data = true;
+    P->fwd = f;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    const cudaError_t e = cudaMalloc(&P->wtrans, size_t(f.nOfm) * f.nIfm * f.kh * f.kw * sizeof(float));
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      conv_plan_destroy(P);
+      throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    *out = P;
+  });
+}
+
 void conv_plan_destroy(conv_plan* p) {
   if (!p) return;
   if (p->pipe) {
@@ -748,6 +838,7 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->flt_pack);
     cudaFree(p->wfold);
     cudaFree(p->xfold);
+    cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }
   delete p;

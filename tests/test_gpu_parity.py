@@ -297,3 +297,49 @@ def test_tmem_resident_a(conv, c_log, recipe):
     ring wrap-around, partial stages, unaligned boxes, many tiles, chunked sums."""
     n = ps.ConvPreset.parse(conv).nImg
     _check("tmem-a", conv, c_log, 15, "3xtf32", n, recipe)
+
+
+def _bwd_data_ref(p, dy, w):
+    """dX[n][c][h][w] = sum_{k,r,s} dY[n][k][h+p-r][w+p-s] W[k][c][r][s] (float64, NCHW16c)."""
+    N, K, C = p.nImg, p.nOfm, p.nIfm
+    P, Q, R, S, H, W_ = p.ofh, p.ofw, p.kh, p.kw, p.ifh, p.ifw
+    dyl = dy.reshape(N, K // 16, P, Q, 16).transpose(0, 1, 4, 2, 3).reshape(N, K, P, Q).astype(np.float64)
+    wl = w.reshape(K // 16, C // 16, R, S, 16, 16).transpose(0, 5, 1, 4, 2, 3).reshape(K, C, R, S)
+    dx = np.zeros((N, C, H, W_))
+    for r in range(R):
+        for s in range(S):
+            for h in range(H):
+                pp = h + p.pad_h - r
+                if not 0 <= pp < P:
+                    continue
+                # columns: q = w + pad - s
+                ws = [x for x in range(W_) if 0 <= x + p.pad_w - s < Q]
+                qs = [x + p.pad_w - s for x in ws]
+                dx[:, :, h, ws] += np.einsum("nkq,kc->ncq", dyl[:, :, pp, qs], wl[:, :, r, s])
+    return dx.reshape(N, C // 16, 16, H, W_).transpose(0, 1, 3, 4, 2).ravel()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv", ["conv:2,64,32,12,12,3,3,1,1,16,1,1,12,12",
+                                  "conv:2,32,48,9,11,5,5,1,1,16,2,2,9,11",
+                                  "conv:3,128,64,7,7,1,1,1,1,16"])
+def test_backward_data(conv, mode):
+    """§8f row f4: dX of a stride-1 layer as the transposed conv on the same kernel."""
+    p = ps.ConvPreset.parse(conv)
+    rng = np.random.default_rng(3)
+    dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
+    w = rng.uniform(-1, 1, p.filter_elems()).astype(np.float32)
+    plan = ps.ConvPlan(p, mode=mode, device=0, bwd_data=True)
+    dx = torch.full((p.input_elems(),), float("nan"), device="cuda:0")
+    plan.forward(torch.from_numpy(dy).cuda(), torch.from_numpy(w).cuda(), dx)
+    torch.cuda.synchronize()
+    ref = _bwd_data_ref(p, dy, w)
+    err = oracle.rel_l2(dx.cpu().numpy(), ref)
+    assert err <= TOL[mode], f"bwd-data relL2 {err:.3e} ({plan.recipe})"
+
+
+@pytest.mark.gpu
+def test_backward_data_rejects_strided():
+    with pytest.raises(ps.ConfigRejectedError):
+        ps.ConvPlan(ps.ConvPreset.parse(BASELINE["cfg3"][0]), bwd_data=True)
