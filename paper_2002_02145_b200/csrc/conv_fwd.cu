@@ -624,6 +624,12 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   }
   const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
   prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
+  // split-K units (not with a fused epilogue: ReLU needs the whole sum)
+  prm.ksplit = (bias || (flags & PSCONV_FLAG_RELU) || s.halo) ? 1 : std::max(1, s.ksplit);
+  prm.split_stages = (prm.nst + prm.ksplit - 1) / prm.ksplit;
+  prm.ksplit = (prm.nst + prm.split_stages - 1) / prm.split_stages;  // no empty units
+  if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE))
+    CUDA_OK(cudaMemsetAsync(out, 0, size_t(img_count) * Kb * Pp * Q * 16 * sizeof(float), st));
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
   prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
   prm.bias = bias;

@@ -87,6 +87,10 @@ struct ConvParams {
   int nst;                        // stages per tile = ceil(ksteps / kps)
   int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
   int chunk_stages;               // stages per TMEM accumulation chunk
+  int ksplit;                     // split-K: work units per tile (reduction split into ksplit
+                                  // stage ranges of split_stages, partial sums reduce-added
+                                  // into the pre-zeroed output); 1 = whole tiles
+  int split_stages;
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
@@ -233,6 +237,19 @@ __device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, i
 // Halo-mode producer (warp 0; warp-uniform loop, one elected lane issues).
 // Per M tile and input-channel group: one halo box into the A ring, then one
 // filter box per (kj, ki) tap into the B ring.
+// split-K work unit u -> (tile group, stage range [ib, ie))
+struct Unit {
+  int g, ib, ie;
+};
+__device__ __forceinline__ Unit decode_unit(const ConvParams& p, int u) {
+  Unit w;
+  w.g = u / p.ksplit;
+  const int sp = u - w.g * p.ksplit;
+  w.ib = sp * p.split_stages;
+  w.ie = min(p.nst, w.ib + p.split_stages);
+  return w;
+}
+
 template <int BN, bool SPLIT3, bool PAIR>
 __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem, uint64_t* full,
                                               uint64_t* empty, int cluster, int nclusters, int rank,
@@ -445,7 +462,6 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   const int cluster = blockIdx.x / CS;
   const int nclusters = gridDim.x / CS;
   const int nst = p.nst;  // pipeline stages per tile
-  const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -517,14 +533,22 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const int e2 = d2 == 0 ? p.cbg : (d2 == 1 ? p.R : p.S);
     int stage = 0, gs = 0;
     uint32_t phase = 0;
-    for (int g = cluster; g < p.groups; g += nclusters) {
-      const TileCoord tc = decode_group(p, g, rank, CS);
+    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+      const Unit un = decode_unit(p, u);
+      const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int wq = tc.tq * p.Qb * p.sw - p.pw;
       const int hp = tc.tp * p.Pb * p.sh - p.ph;
       const int n0 = tc.tn * p.Nb;
       const int k0 = tc.tk * BN + rank * Cfg::kBRows;
-      int v0 = 0, v1 = 0, v2 = 0;  // reduction-loop counters, outer -> inner
-      for (int it = 0; it < p.nst; ++it) {
+      // reduction-loop counters (outer -> inner) at the unit's first coordinate step
+      int v0, v1, v2;
+      {
+        const int t0 = p.cb_group ? un.ib : un.ib * p.kps;
+        v2 = t0 % e2;
+        v1 = (t0 / e2) % e1;
+        v0 = t0 / (e2 * e1);
+      }
+      for (int it = un.ib; it < un.ie; ++it) {
         const int nk = min(p.kps, p.ksteps - it * p.kps);
         const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[gs * 4 + 0] = clock64();
@@ -601,8 +625,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int aslot = 0;  // TMEM A ring position (3xTF32 tmem_a)
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
-    for (int g = cluster; g < p.groups; g += nclusters) {
-      for (int c = 0; c < nchunks; ++c, ++cit) {
+    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+      const Unit un = decode_unit(p, u);
+      const int unchunks = (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+      for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
         if (PAIR)
@@ -611,8 +637,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
-        const int it0 = c * p.chunk_stages;
-        const int it_end = min(nst, it0 + p.chunk_stages);
+        const int it0 = un.ib + c * p.chunk_stages;
+        const int it_end = min(un.ie, it0 + p.chunk_stages);
         for (int it = it0; it < it_end; ++it) {
           const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
@@ -722,14 +748,16 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int ostage = 0;                                                  // staging buffer toggle
     if (store_thread) ptx::prefetch_tmap(&tmap_out);
     int cit = 0;
-    for (int g = cluster; g < p.groups; g += nclusters) {
-      const TileCoord tc = decode_group(p, g, rank, CS);
+    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+      const Unit un = decode_unit(p, u);
+      const int unchunks = (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+      const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
       const int kb0 = tc.tk * (BN / 16);
-      for (int c = 0; c < nchunks; ++c, ++cit) {
+      for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
-        const bool last = c == nchunks - 1;
+        const bool last = c == unchunks - 1;
 #ifdef PSCONV_EPI_SLEEP
         ptx::mbar_wait_sleep(&acc_full[buf], acc_phase);
 #else
@@ -801,7 +829,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
 #pragma unroll
               for (int blk = 0; blk < kBlk; ++blk) {
                 const int kb = kb0 + j * kBlk + blk;
-                if (p.accumulate)
+                if (p.accumulate || p.ksplit > 1)  // split-K partials add into the zeroed output
                   ptx::tma_reduce_add_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
                 else
                   ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
@@ -859,8 +887,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       int slot = 0;
       uint32_t sph = 0;
-      for (int g = cluster; g < p.groups; g += nclusters) {
-        for (int it = 0; it < nst; ++it) {
+      for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+        const Unit un = decode_unit(p, u);
+        for (int it = un.ib; it < un.ie; ++it) {
           ptx::mbar_wait(&full[stage], phase);
           const int nk = min(p.kps, p.ksteps - it * p.kps);
           for (int j = 0; j < nk; ++j) {
@@ -903,8 +932,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         }
       }
     } else
-    for (int g = cluster; g < p.groups; g += nclusters) {
-      for (int it = 0; it < nst; ++it) {
+    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+      const Unit un = decode_unit(p, u);
+      for (int it = un.ib; it < un.ie; ++it) {
         ptx::mbar_wait(&full[stage], phase);
         // A tiles of the stage: kps x a_pitch bytes (packed box image, or 8 KB
         // tiles); the lo region mirrors it (offsets are multiples of 512 B, so

@@ -16,6 +16,7 @@
 //   * tile=oj:T  -> T output rows per 128-pixel tile (box P extent);
 //     tile=img:T -> T images per tile; tile=ofm_tile:T -> BN = 16*T channels.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cctype>
 #include <map>
@@ -101,6 +102,9 @@ Recipe Recipe::parse(const std::string& text) {
           r.kg = static_cast<int>(parse_int(val, "gpu k-steps per stage"));
           if (r.kg != 1 && r.kg != 2 && r.kg != 4 && r.kg != 8)
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
+        } else if (key == "ks") {
+          r.ks = static_cast<int>(parse_int(val, "gpu split-K"));
+          if (r.ks < 1 || r.ks > 16) throw ConfigError("gpu ks must be in [1, 16]");
         } else if (key == "ta") {
           r.ta = static_cast<int>(parse_int(val, "gpu TMEM-resident A"));
           if (r.ta != 0 && r.ta != 1) throw ConfigError("gpu ta must be 0 or 1");
@@ -144,6 +148,7 @@ std::string Recipe::id() const {
     if (gm >= 0) s += ",gm:" + std::to_string(gm);
     if (fold) s += ",fold:" + std::to_string(fold);
     if (ta >= 0) s += ",ta:" + std::to_string(ta);
+    if (ks) s += ",ks:" + std::to_string(ks);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -327,6 +332,35 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
+  // Split-K (wave quantisation): when a layer has only a few waves of tiles, the
+  // reduction of each tile is split into ks stage ranges run as separate work
+  // units whose partials are reduce-added into the zeroed output. Auto: the ks in
+  // 1..8 (>= 4 stages each) maximising the last-wave fill minus 2% per extra unit.
+  {
+    const int ksteps_all = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
+    const int nst = (ksteps_all + s.kps - 1) / s.kps;
+    const int64_t tq = (d.ofw + s.qb - 1) / s.qb, tp = (d.ofh + s.pb - 1) / s.pb,
+                  tn = (d.nImg + s.nb - 1) / s.nb;
+    const int cs = std::max(1, s.cs);
+    const int64_t tiles = (tq * tp * tn + cs - 1) / cs * (d.nOfm / s.bn);
+    const double slots = 148.0 / cs;
+    int best = 1;
+    if (r.ks) {
+      best = std::min(r.ks, nst);
+    } else if (!s.halo && tiles < 4 * slots) {
+      double best_v = -1;
+      for (int k = 1; k <= 8 && nst / k >= 4; ++k) {
+        const double units = double(tiles) * k;
+        const double v = units / (std::ceil(units / slots) * slots) - 0.02 * (k - 1);
+        if (v > best_v + 1e-9) {
+          best_v = v;
+          best = k;
+        }
+      }
+    }
+    s.ksplit = s.halo ? 1 : best;
+    canon.ks = r.ks ? s.ksplit : 0;
+  }
   // Grouped raster (auto): when both the activation rows and the filter of all
   // tiles exceed the L2 share, a wave of 148 concurrent tiles should cover a
   // ~12 x 12 block of (M group, N tile) so A rows and B columns are reused in

@@ -149,11 +149,14 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // accumulator (bn 256)
   const double drain_cyc = (s.bn / 32.0) * m.drain_round_trip_cyc;
   const bool drain_exposed = mult > 1 && s.bn == 256;
-  const double tile_cyc = ksteps * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
+  // split-K: each tile is ks work units of ksteps / ks, each with its own drain
+  const int ks = std::max(1, s.ksplit);
+  const double tile_cyc = double(ksteps) / ks * kstep_cyc +
+                          (drain_exposed ? nchunks / ks * drain_cyc : drain_cyc);
   // a CTA pair works on 2 pixel tiles at once: tiles per SM are still tiles/148
-  const double groups_per_cluster = std::ceil(double(tiles) / m.sms);
+  const double groups_per_cluster = std::ceil(double(tiles) * ks / m.sms);
   b.us_tensor = groups_per_cluster * tile_cyc / (m.clock_ghz * 1e3);
-  const double to_us = groups_per_cluster * ksteps / (m.clock_ghz * 1e3);
+  const double to_us = groups_per_cluster * double(ksteps) / ks / (m.clock_ghz * 1e3);
   b.us_mma = mma_cyc * to_us;
   b.us_smem_traffic = smem_cyc * to_us;
   b.us_rows = del_cyc * to_us;

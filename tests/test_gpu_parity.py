@@ -343,3 +343,32 @@ def test_backward_data(conv, mode):
 def test_backward_data_rejects_strided():
     with pytest.raises(ps.ConfigRejectedError):
         ps.ConvPlan(ps.ConvPreset.parse(BASELINE["cfg3"][0]), bwd_data=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:256,box:7x1x18,ks:2"),
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:128,box:1x7x18,ks:5"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,kg:4,ks:3"),
+    ("conv:2,32,48,9,9,3,3,1,1,16,1,1,9,9", 48, "gpu=bn:32,box:9x9x1,kg:4,ks:2"),
+])
+def test_split_k(conv, c_log, recipe, mode):
+    """Split-K work units: each tile's reduction in ks stage ranges, partials reduce-added
+    into the zeroed output (also with the pair, TMEM-A and partial-stage paths)."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("ks", conv, c_log, 16, mode, n, recipe)
+    if mode == "tf32":
+        _check("ks-pair", conv, c_log, 16, mode, n, recipe + ",cl:2")
+
+
+@pytest.mark.gpu
+def test_split_k_accumulate():
+    """+= with split-K: no zeroing, every unit adds into the existing output."""
+    p = ps.ConvPreset.parse("conv:4,256,256,7,7,3,3,1,1,16,1,1,7,7")
+    sx, sw = seeds(17)
+    base = np.random.default_rng(1).standard_normal(p.output_elems()).astype(np.float32)
+    xg, wg, yg, rec = _run_gpu(p, 256, sx, sw, "3xtf32", recipe="gpu=bn:128,box:7x1x18,ks:3",
+                               accumulate=True, out_init=base)
+    ref = base + oracle.conv(p, oracle.fill_input(p, sx, 256), oracle.fill_filter(p, sw, 256)).ravel()
+    assert oracle.rel_l2(yg, ref) <= 1e-5, rec
