@@ -628,6 +628,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.ksplit = (bias || (flags & PSCONV_FLAG_RELU) || s.halo) ? 1 : std::max(1, s.ksplit);
   prm.split_stages = (prm.nst + prm.ksplit - 1) / prm.ksplit;
   prm.ksplit = (prm.nst + prm.split_stages - 1) / prm.split_stages;  // no empty units
+  prm.tile_chunks = (prm.nst + prm.chunk_stages - 1) / prm.chunk_stages;
   if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE))
     CUDA_OK(cudaMemsetAsync(out, 0, size_t(img_count) * Kb * Pp * Q * 16 * sizeof(float), st));
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];

@@ -91,6 +91,7 @@ struct ConvParams {
                                   // stage ranges of split_stages, partial sums reduce-added
                                   // into the pre-zeroed output); 1 = whole tiles
   int split_stages;
+  int tile_chunks;                // accumulation chunks of a whole tile (ksplit == 1)
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
@@ -243,6 +244,12 @@ struct Unit {
 };
 __device__ __forceinline__ Unit decode_unit(const ConvParams& p, int u) {
   Unit w;
+  if (p.ksplit == 1) {  // whole tiles: no divisions on the producer's per-tile path
+    w.g = u;
+    w.ib = 0;
+    w.ie = p.nst;
+    return w;
+  }
   w.g = u / p.ksplit;
   const int sp = u - w.g * p.ksplit;
   w.ib = sp * p.split_stages;
@@ -541,8 +548,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const int n0 = tc.tn * p.Nb;
       const int k0 = tc.tk * BN + rank * Cfg::kBRows;
       // reduction-loop counters (outer -> inner) at the unit's first coordinate step
-      int v0, v1, v2;
-      {
+      int v0 = 0, v1 = 0, v2 = 0;
+      if (un.ib > 0) {
         const int t0 = p.cb_group ? un.ib : un.ib * p.kps;
         v2 = t0 % e2;
         v1 = (t0 / e2) % e1;
@@ -627,7 +634,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
     for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
       const Unit un = decode_unit(p, u);
-      const int unchunks = (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+      const int unchunks =
+          p.ksplit == 1 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -750,7 +758,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int cit = 0;
     for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
       const Unit un = decode_unit(p, u);
-      const int unchunks = (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+      const int unchunks =
+          p.ksplit == 1 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
       const int kb0 = tc.tk * (BN / 16);

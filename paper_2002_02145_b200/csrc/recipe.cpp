@@ -335,7 +335,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   // Split-K (wave quantisation): when a layer has only a few waves of tiles, the
   // reduction of each tile is split into ks stage ranges run as separate work
   // units whose partials are reduce-added into the zeroed output. Auto: the ks in
-  // 1..8 (>= 4 stages each) maximising the last-wave fill minus 2% per extra unit.
+  // 1..8 (>= 4 stages each) with the lowest modelled time, which charges the
+  // extra output traffic (select.cpp) -- output-heavy layers stay unsplit.
   {
     const int ksteps_all = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
     const int nst = (ksteps_all + s.kps - 1) / s.kps;
@@ -348,12 +349,13 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
     if (r.ks) {
       best = std::min(r.ks, nst);
     } else if (!s.halo && tiles < 4 * slots) {
-      double best_v = -1;
+      double best_us = 1e300;
       for (int k = 1; k <= 8 && nst / k >= 4; ++k) {
-        const double units = double(tiles) * k;
-        const double v = units / (std::ceil(units / slots) * slots) - 0.02 * (k - 1);
-        if (v > best_v + 1e-9) {
-          best_v = v;
+        Schedule t = s;
+        t.ksplit = k;
+        const double us = model_schedule(d, t, mode).us_total;
+        if (us < best_us * 0.98) {  // a split must win by 2%
+          best_us = us;
           best = k;
         }
       }

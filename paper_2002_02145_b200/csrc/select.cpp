@@ -174,6 +174,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   double in_reads = 1.0;
   if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
+  // split-K: the output is zeroed first and every extra unit's partial is
+  // reduce-added (in L2 while the tile's lines stay resident, partly in HBM)
+  if (ks > 1) b.hbm_bytes += out_b * (1.0 + 0.5 * (ks - 1));
   b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain
