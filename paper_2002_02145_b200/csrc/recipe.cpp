@@ -354,14 +354,14 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
         Schedule t = s;
         t.ksplit = k;
         const double us = model_schedule(d, t, mode).us_total;
-        if (us < best_us * 0.98) {  // a split must win by 2%
+        if (us < best_us * 0.95) {  // a split must win by 5%
           best_us = us;
           best = k;
         }
       }
     }
     s.ksplit = s.halo ? 1 : best;
-    canon.ks = r.ks ? s.ksplit : 0;
+    canon.ks = (r.ks || s.ksplit > 1) ? s.ksplit : 0;  // shown when it splits
   }
   // Grouped raster (auto): when both the activation rows and the filter of all
   // tiles exceed the L2 share, a wave of 148 concurrent tiles should cover a

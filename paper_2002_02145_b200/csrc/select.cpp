@@ -151,8 +151,10 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const bool drain_exposed = mult > 1 && s.bn == 256;
   // split-K: each tile is ks work units of ksteps / ks, each with its own drain
   const int ks = std::max(1, s.ksplit);
+  // (a split unit also refills the pipeline and drains a whole output tile:
+  // ~1500 cycles, fitted to l3 3x3 / cfg3 / l4 3x3 A/B timings)
   const double tile_cyc = double(ksteps) / ks * kstep_cyc +
-                          (drain_exposed ? nchunks / ks * drain_cyc : drain_cyc);
+                          (drain_exposed ? nchunks / ks * drain_cyc : drain_cyc) + (ks > 1 ? 1500.0 : 0.0);
   // a CTA pair works on 2 pixel tiles at once: tiles per SM are still tiles/148
   const double groups_per_cluster = std::ceil(double(tiles) * ks / m.sms);
   b.us_tensor = groups_per_cluster * tile_cyc / (m.clock_ghz * 1e3);
@@ -176,7 +178,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
   // split-K: the output is zeroed first and every extra unit's partial is
   // reduce-added (in L2 while the tile's lines stay resident, partly in HBM)
-  if (ks > 1) b.hbm_bytes += out_b * (1.0 + 0.5 * (ks - 1));
+  if (ks > 1) b.hbm_bytes += out_b * ks;
   b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain
