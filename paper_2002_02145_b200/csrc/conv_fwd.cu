@@ -56,7 +56,13 @@ struct conv_plan {
     cudaEvent_t h2d[2] = {nullptr, nullptr}, conv[2] = {nullptr, nullptr}, d2h[2] = {nullptr, nullptr};
   };
   mutable HostPipe* pipe = nullptr;
+  // split-tile flags (tail split-K): kFlagRing regions of flag_cap ints, one
+  // region per launch epoch so stream-ordered launches never reset them
+  mutable int* tile_flags = nullptr;
+  mutable int64_t flag_cap = 0;
+  mutable int epoch = 0;
 };
+constexpr int kFlagRing = 8;
 
 namespace psconv {
 namespace {
@@ -625,12 +631,37 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
   prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
   // split-K units (not with a fused epilogue: ReLU needs the whole sum)
+  // Only the tiles of the last partial wave are split (tail split): the first
+  // (groups / clusters) * clusters tiles run whole, each later tile becomes
+  // ksplit units of split_stages stages.
   prm.ksplit = (bias || (flags & PSCONV_FLAG_RELU) || s.halo) ? 1 : std::max(1, s.ksplit);
   prm.split_stages = (prm.nst + prm.ksplit - 1) / prm.ksplit;
   prm.ksplit = (prm.nst + prm.split_stages - 1) / prm.split_stages;  // no empty units
   prm.tile_chunks = (prm.nst + prm.chunk_stages - 1) / prm.chunk_stages;
-  if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE))
-    CUDA_OK(cudaMemsetAsync(out, 0, size_t(img_count) * Kb * Pp * Q * 16 * sizeof(float), st));
+  {
+    const int clusters = P->num_sms / s.cs;
+    prm.split_from = prm.ksplit > 1 ? prm.groups / clusters * clusters : prm.groups;
+    if (prm.split_from == prm.groups) prm.ksplit = 1;  // no partial wave: nothing to split
+    prm.units = prm.split_from + (prm.groups - prm.split_from) * prm.ksplit;
+    prm.tile_flags = nullptr;
+    prm.epoch = 0;
+    if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE)) {
+      const int64_t need = int64_t(prm.groups - prm.split_from) * s.cs;
+      if (need > P->flag_cap) {
+        if (P->tile_flags) {
+          CUDA_OK(cudaStreamSynchronize(st));
+          CUDA_OK(cudaFree(P->tile_flags));
+        }
+        CUDA_OK(cudaMalloc(&P->tile_flags, size_t(need) * kFlagRing * sizeof(int)));
+        CUDA_OK(cudaMemsetAsync(P->tile_flags, 0, size_t(need) * kFlagRing * sizeof(int), st));
+        P->flag_cap = need;
+        P->epoch = 0;
+      }
+      P->epoch = P->epoch == INT32_MAX ? 1 : P->epoch + 1;
+      prm.epoch = P->epoch;
+      prm.tile_flags = P->tile_flags + (P->epoch % kFlagRing) * P->flag_cap;
+    }
+  }
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
   prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
   prm.bias = bias;
@@ -845,6 +876,7 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->flt_pack);
     cudaFree(p->wfold);
     cudaFree(p->xfold);
+    cudaFree(p->tile_flags);
     cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }

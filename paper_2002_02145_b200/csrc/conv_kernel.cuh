@@ -91,6 +91,10 @@ struct ConvParams {
                                   // stage ranges of split_stages, partial sums reduce-added
                                   // into the pre-zeroed output); 1 = whole tiles
   int split_stages;
+  int split_from;                 // tiles [0, split_from) are whole units; later tiles split
+  int units;                      // split_from + (groups - split_from) * ksplit
+  int* tile_flags;                // per split tile: the first unit's stores landed (== epoch)
+  int epoch;                      // launch counter of the plan (flags need no reset)
   int tile_chunks;                // accumulation chunks of a whole tile (ksplit == 1)
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
@@ -240,19 +244,22 @@ __device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, i
 // filter box per (kj, ki) tap into the B ring.
 // split-K work unit u -> (tile group, stage range [ib, ie))
 struct Unit {
-  int g, ib, ie;
+  int g, ib, ie, sp;  // sp: split index, -1 for a whole tile
 };
 __device__ __forceinline__ Unit decode_unit(const ConvParams& p, int u) {
   Unit w;
-  if (p.ksplit == 1) {  // whole tiles: no divisions on the producer's per-tile path
+  if (u < p.split_from) {  // whole tiles: no divisions on the producer's per-tile path
     w.g = u;
     w.ib = 0;
     w.ie = p.nst;
+    w.sp = -1;
     return w;
   }
-  w.g = u / p.ksplit;
-  const int sp = u - w.g * p.ksplit;
-  w.ib = sp * p.split_stages;
+  const int v = u - p.split_from;
+  const int t = v / p.ksplit;
+  w.g = p.split_from + t;
+  w.sp = v - t * p.ksplit;
+  w.ib = w.sp * p.split_stages;
   w.ie = min(p.nst, w.ib + p.split_stages);
   return w;
 }
@@ -540,7 +547,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const int e2 = d2 == 0 ? p.cbg : (d2 == 1 ? p.R : p.S);
     int stage = 0, gs = 0;
     uint32_t phase = 0;
-    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+    for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit(p, u);
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int wq = tc.tq * p.Qb * p.sw - p.pw;
@@ -632,10 +639,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int aslot = 0;  // TMEM A ring position (3xTF32 tmem_a)
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
-    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+    for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit(p, u);
       const int unchunks =
-          p.ksplit == 1 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+          un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -756,13 +763,20 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int ostage = 0;                                                  // staging buffer toggle
     if (store_thread) ptx::prefetch_tmap(&tmap_out);
     int cit = 0;
-    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+    for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit(p, u);
       const int unchunks =
-          p.ksplit == 1 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+          un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
       const int kb0 = tc.tk * (BN / 16);
+      // split tile (no `+=`): its first unit stores and then raises the tile's
+      // flag; the other units reduce-add once the flag shows this launch's epoch
+      // (they wait only on smaller unit indices of co-resident persistent CTAs)
+      const bool flagged = un.sp >= 0 && !p.accumulate;
+      const bool reduce = p.accumulate || un.sp > 0;
+      int* const flag = flagged ? p.tile_flags + (un.g - p.split_from) * CS + rank : nullptr;
+      bool wait_flag = flagged && un.sp > 0;
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -834,11 +848,18 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             }
             ptx::fence_proxy_async_smem();
             ptx::named_bar(1, 128);
+            if (store_thread && wait_flag) {
+              const uint64_t t0 = ptx::globaltimer();
+              while (ptx::ld_acquire_gpu(flag) != p.epoch)
+                if (ptx::globaltimer() - t0 > 10000000000ull) __trap();  // 10 s: not co-resident
+              ptx::fence_proxy_async_global();
+              wait_flag = false;
+            }
             if (store_thread && !(p.debug & 4)) {
 #pragma unroll
               for (int blk = 0; blk < kBlk; ++blk) {
                 const int kb = kb0 + j * kBlk + blk;
-                if (p.accumulate || p.ksplit > 1)  // split-K partials add into the zeroed output
+                if (reduce)  // `+=` or a later split-K partial
                   ptx::tma_reduce_add_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
                 else
                   ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
@@ -858,6 +879,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             ptx::mbar_arrive(&acc_empty[buf]);
         }
         __syncwarp();
+      }
+      if (store_thread && flagged && un.sp == 0) {  // the tile's first partial is in memory
+        ptx::bulk_wait_all();
+        ptx::fence_proxy_async_global();
+        ptx::st_release_gpu(flag, p.epoch);
       }
     }
     if (ev && store_thread) ev[5] = clock64();  // last store issued
@@ -896,7 +922,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       int slot = 0;
       uint32_t sph = 0;
-      for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+      for (int u = cluster; u < p.units; u += nclusters) {
         const Unit un = decode_unit(p, u);
         for (int it = un.ib; it < un.ie; ++it) {
           ptx::mbar_wait(&full[stage], phase);
@@ -941,7 +967,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         }
       }
     } else
-    for (int u = cluster; u < p.groups * p.ksplit; u += nclusters) {
+    for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit(p, u);
       for (int it = un.ib; it < un.ie; ++it) {
         ptx::mbar_wait(&full[stage], phase);

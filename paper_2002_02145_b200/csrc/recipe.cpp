@@ -332,29 +332,29 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
-  // Split-K (wave quantisation): when a layer has only a few waves of tiles, the
-  // reduction of each tile is split into ks stage ranges run as separate work
-  // units whose partials are reduce-added into the zeroed output. Auto: the ks in
-  // 1..8 (>= 4 stages each) with the lowest modelled time, which charges the
-  // extra output traffic (select.cpp) -- output-heavy layers stay unsplit.
+  // Tail split-K (wave quantisation): the tiles of the last partial wave are
+  // split into ks stage ranges run as separate work units (the first stores,
+  // the others reduce-add once it landed). Auto: the ks in 1..8 (>= 4 stages
+  // each) with the lowest modelled time, charging the per-unit refill/drain
+  // and the extra output traffic (select.cpp); a split must win by 3%.
   {
     const int ksteps_all = static_cast<int>(d.nIfm / 16 * d.kh * d.kw);
     const int nst = (ksteps_all + s.kps - 1) / s.kps;
     const int64_t tq = (d.ofw + s.qb - 1) / s.qb, tp = (d.ofh + s.pb - 1) / s.pb,
                   tn = (d.nImg + s.nb - 1) / s.nb;
     const int cs = std::max(1, s.cs);
-    const int64_t tiles = (tq * tp * tn + cs - 1) / cs * (d.nOfm / s.bn);
-    const double slots = 148.0 / cs;
+    const int64_t groups = (tq * tp * tn + cs - 1) / cs * (d.nOfm / s.bn);
+    const int64_t clusters = 148 / cs;
     int best = 1;
     if (r.ks) {
       best = std::min(r.ks, nst);
-    } else if (!s.halo && tiles < 4 * slots) {
+    } else if (!s.halo && groups % clusters != 0) {
       double best_us = 1e300;
       for (int k = 1; k <= 8 && nst / k >= 4; ++k) {
         Schedule t = s;
         t.ksplit = k;
         const double us = model_schedule(d, t, mode).us_total;
-        if (us < best_us * 0.95) {  // a split must win by 5%
+        if (us < best_us * 0.97) {
           best_us = us;
           best = k;
         }

@@ -149,16 +149,27 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // accumulator (bn 256)
   const double drain_cyc = (s.bn / 32.0) * m.drain_round_trip_cyc;
   const bool drain_exposed = mult > 1 && s.bn == 256;
-  // split-K: each tile is ks work units of ksteps / ks, each with its own drain
+  // Static round-robin over persistent clusters: W full waves of whole tiles,
+  // then (tail split-K) the rem tiles of the last partial wave as ks units of
+  // ksteps / ks each, with their own drain
   const int ks = std::max(1, s.ksplit);
-  // (a split unit also refills the pipeline and drains a whole output tile:
-  // ~1500 cycles, fitted to l3 3x3 / cfg3 / l4 3x3 A/B timings)
-  const double tile_cyc = double(ksteps) / ks * kstep_cyc +
-                          (drain_exposed ? nchunks / ks * drain_cyc : drain_cyc) + (ks > 1 ? 1500.0 : 0.0);
-  // a CTA pair works on 2 pixel tiles at once: tiles per SM are still tiles/148
-  const double groups_per_cluster = std::ceil(double(tiles) * ks / m.sms);
-  b.us_tensor = groups_per_cluster * tile_cyc / (m.clock_ghz * 1e3);
-  const double to_us = groups_per_cluster * double(ksteps) / ks / (m.clock_ghz * 1e3);
+  const int64_t clusters = m.sms / cs, groups = (mt + cs - 1) / cs * tk;
+  const int64_t waves = groups / clusters, rem = groups - waves * clusters;
+  const int kt = rem > 0 ? ks : 1;
+  const double tile_cyc = double(ksteps) * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
+  // (a split unit also refills the pipeline (~1500 cycles) and drains a whole
+  // output tile that the later units wait for (128 x BN fp32 at ~64 B/cycle);
+  // fitted to the r01 tail-split A/B timings of cfg3 / cfg5 / l3 / l4)
+  const double split_cyc = 1500.0 + 128.0 * s.bn * 4.0 / 64.0;
+  const double unit_cyc = double(ksteps) / kt * kstep_cyc +
+                          (drain_exposed ? nchunks / kt * drain_cyc : drain_cyc) + (kt > 1 ? split_cyc : 0.0);
+  double tail_units = std::ceil(double(rem) * kt / clusters);
+  // a partial wave of whole tiles runs faster than a full one (fewer SMs share
+  // L2/HBM and the power budget): fitted to the r01 tail-split A/B timings
+  // (l3/l4 layers at 1.3-2.7 waves, cfg5 at 21.2)
+  if (kt == 1 && rem > 0) tail_units = 0.5 + 0.5 * double(rem) / clusters;
+  b.us_tensor = (waves * tile_cyc + tail_units * unit_cyc) / (m.clock_ghz * 1e3);
+  const double to_us = (waves + tail_units / kt) * double(ksteps) / (m.clock_ghz * 1e3);
   b.us_mma = mma_cyc * to_us;
   b.us_smem_traffic = smem_cyc * to_us;
   b.us_rows = del_cyc * to_us;
@@ -176,9 +187,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   double in_reads = 1.0;
   if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
-  // split-K: the output is zeroed first and every extra unit's partial is
-  // reduce-added (in L2 while the tile's lines stay resident, partly in HBM)
-  if (ks > 1) b.hbm_bytes += out_b * ks;
+  // split-K: every extra unit of a split tile reduce-adds its partial (in L2
+  // while the tile's lines stay resident, partly in HBM)
+  if (kt > 1) b.hbm_bytes += out_b * double(rem) / groups * (kt - 1);
   b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain

@@ -39,6 +39,11 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
             if mode == "3xtf32":
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
+    # tail split-K: the model's split decision both ways
+    if "ks" in kv:
+        alts.append({**kv, "ks": "1"})
+    else:
+        alts += [{**kv, "ks": "2"}, {**kv, "ks": "3"}]
     # (c,s) fold when the caller knows only c_logical <= 8 of the 16 input channels are
     # real (the stem): the same top candidates over the folded input
     if 0 < c_logical <= 8 and preset.nIfm == 16 and preset.kw > 1:

@@ -362,6 +362,57 @@ def test_split_k(conv, c_log, recipe, mode):
         _check("ks-pair", conv, c_log, 16, mode, n, recipe + ",cl:2")
 
 
+TAIL = "conv:8,64,64,56,56,3,3,1,1,16,1,1,56,56"  # 196 tiles of 8x8x2 px: 1 wave + 48
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("recipe", [
+    "gpu=bn:64,box:8x8x2,ks:3",   # 144 tail units after 148 whole tiles
+    "gpu=bn:64,box:8x8x2,ks:4",   # 192 tail units: a second round of units
+    "gpu=bn:64,box:8x8x2,ks:2,cl:2",  # pairs: 74 clusters, 98 groups
+])
+def test_tail_split(recipe, mode):
+    """Tail split-K: only the last partial wave's tiles are split; a split tile's first
+    unit stores, the others reduce-add after its flag (no output memset)."""
+    if "cl:2" in recipe and mode == "3xtf32":
+        pytest.skip("the CTA pair is TF32-only")
+    _check("tail", TAIL, 64, 16, mode, 8, recipe)
+
+
+@pytest.mark.gpu
+def test_tail_split_relaunch():
+    """Flags are epoch-tagged in a ring: repeated launches of one plan on one stream stay
+    correct with no reset (each launch overwrites a NaN-filled output)."""
+    p = ps.ConvPreset.parse(TAIL)
+    sx, sw = seeds(16)
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), dtype=torch.float32, device=dev)
+    w = torch.empty(p.filter_elems(), dtype=torch.float32, device=dev)
+    ps.fill_input(p, sx, x, c_logical=64)
+    ps.fill_filter(p, sw, w, c_logical=64)
+    ref = oracle.conv(p, oracle.fill_input(p, sx, 64), oracle.fill_filter(p, sw, 64)).ravel()
+    plan = ps.ConvPlan(p, mode="tf32", device=0, recipe="gpu=bn:64,box:8x8x2,ks:3")
+    ys = [torch.full((p.output_elems(),), float("nan"), dtype=torch.float32, device=dev) for _ in range(11)]
+    for y in ys:
+        plan.forward(x, w, y)
+    torch.cuda.synchronize()
+    for i, y in enumerate(ys):
+        err = oracle.rel_l2(y.cpu().numpy(), ref)
+        assert err <= TOL["tf32"], f"launch {i}: relL2 {err:.3e}"
+
+
+@pytest.mark.gpu
+def test_tail_split_accumulate():
+    p = ps.ConvPreset.parse(TAIL)
+    sx, sw = seeds(16)
+    base = np.random.default_rng(2).standard_normal(p.output_elems()).astype(np.float32)
+    xg, wg, yg, rec = _run_gpu(p, 64, sx, sw, "3xtf32", recipe="gpu=bn:64,box:8x8x2,ks:3",
+                               accumulate=True, out_init=base)
+    ref = base + oracle.conv(p, oracle.fill_input(p, sx, 64), oracle.fill_filter(p, sw, 64)).ravel()
+    assert oracle.rel_l2(yg, ref) <= 1e-5, rec
+
+
 @pytest.mark.gpu
 def test_split_k_accumulate():
     """+= with split-K: no zeroing, every unit adds into the existing output."""
