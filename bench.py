@@ -323,9 +323,13 @@ def run_ours(args, rank, world, local_rank):
 
         e2e_ms = max_over_ranks(statistics.mean(timed(e2e_step, args.steps, max(1, args.warmup))))
         torch.cuda.synchronize()
-        # the host path's last image must equal the device path's (same kernel, same inputs)
-        e2e_match = bool(torch.equal(hy[(n_local - 1) * out_elems_img:],
-                                     y[(b1 - 1) * out_elems_img:b1 * out_elems_img].cpu()))
+        # the host path's last image must match the device path's (same kernel, same
+        # inputs; the chunked launches may split tail tiles differently, so the fp32
+        # summation order -- not the result -- can differ: relative L2 <= 1e-6)
+        a = hy[(n_local - 1) * out_elems_img:].double()
+        b = y[(b1 - 1) * out_elems_img:b1 * out_elems_img].cpu().double()
+        e2e_diff = float((a - b).norm() / b.norm().clamp_min(1e-30))
+        e2e_match = e2e_diff <= 1e-6
     clocks = clk.summary()
 
     # ---- verification (untimed): gather output shards to rank 0 over NCCL, check sampled images
@@ -364,6 +368,10 @@ def run_ours(args, rank, world, local_rank):
             "peak_source": f"{peak_src}: bf16 {bf16_tflops} TFLOP/s /2 (tf32 rate)"
                            + (" /3 (3xTF32: three tf32 MMAs per MAC)" if args.mode == "3xtf32" else "")
                            + f"; HBM {hbm_gbs} GB/s",
+            # context: the nominal dense tf32 rate (1.1 PFLOP/s, B200_PROFILING.md) -- the
+            # measured bf16/2 denominator sits below it because cuBLAS bf16 runs power-capped
+            "frac_of_nominal": round(achieved_tflops / (1100.0 / (3 if args.mode == "3xtf32" else 1)), 4)
+                               if bound == "tensor" else None,
             "algorithmic": f"{f_alg / 1e9:.3f} GFLOP and {b_comp / 1e6:.1f} MB compulsory per launch "
                            f"({n_local} images x 2*K*C*P*Q*R*S)"})
         bi = 4 * (n_local * in_elems_img + p.filter_elems())
@@ -389,7 +397,7 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roof,
             "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": bi,
                     "d2h_bytes_per_step": bo, "ms_per_step": round(e2e_ms, 3),
-                    "matches_device_path": e2e_match,
+                    "matches_device_path": e2e_match, "rel_l2_vs_device_path": float(f"{e2e_diff:.3g}"),
                     "path": "ConvPlan.forward_host (C ABI conv_fwd_host): pinned host -> device -> pinned host, chunked and overlapped"},
             "gpu_launches": args.steps * plan.launches,
             "clocks": clocks,

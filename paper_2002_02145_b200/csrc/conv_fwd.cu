@@ -393,7 +393,7 @@ int grid_for(int64_t n) {
 }
 
 // ---------------------------------------------------------------- launch
-template <int BN, bool SPLIT3, int CS, bool FUSED>
+template <int BN, bool SPLIT3, int CS, int EPI>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2)) {
@@ -404,7 +404,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, FUSED>,
+      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     CUDA_OK(attr_err);
@@ -434,19 +434,19 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, FUSED>, prm, a, b, blo, o));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, EPI>, prm, a, b, blo, o));
   }
 }
 
-template <bool SPLIT3, int CS, bool FUSED>
+template <bool SPLIT3, int CS, int EPI>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_conv<16, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
-    case 32: return launch_conv<32, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
-    case 64: return launch_conv<64, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
-    case 128: return launch_conv<128, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
-    case 256: return launch_conv<256, SPLIT3, CS, FUSED>(P, prm, a, b, blo, o, st);
+    case 16: return launch_conv<16, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
+    case 32: return launch_conv<32, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
+    case 64: return launch_conv<64, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
+    case 128: return launch_conv<128, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
+    case 256: return launch_conv<256, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported bn");
   }
 }
@@ -456,11 +456,13 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (cs) {
     case 1:
-      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 1, true>(bn, P, prm, a, b, blo, o, st)
-                                  : dispatch_bn<SPLIT3, 1, false>(bn, P, prm, a, b, blo, o, st);
+      if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 1, kEpiSplit>(bn, P, prm, a, b, blo, o, st);
+      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 1, kEpiFused>(bn, P, prm, a, b, blo, o, st)
+                                  : dispatch_bn<SPLIT3, 1, kEpiStore>(bn, P, prm, a, b, blo, o, st);
     case 2:
-      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 2, true>(bn, P, prm, a, b, blo, o, st)
-                                  : dispatch_bn<SPLIT3, 2, false>(bn, P, prm, a, b, blo, o, st);
+      if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 2, kEpiSplit>(bn, P, prm, a, b, blo, o, st);
+      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 2, kEpiFused>(bn, P, prm, a, b, blo, o, st)
+                                  : dispatch_bn<SPLIT3, 2, kEpiStore>(bn, P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported cluster size");
   }
 }
@@ -640,11 +642,17 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.tile_chunks = (prm.nst + prm.chunk_stages - 1) / prm.chunk_stages;
   {
     const int clusters = P->num_sms / s.cs;
-    prm.split_from = prm.ksplit > 1 ? prm.groups / clusters * clusters : prm.groups;
+    // (kt:1: every tile split, the output zeroed first and every partial reduce-added;
+    // measured faster than the tail split on some 3xTF32 layers at ~1.3 waves)
+    prm.split_from = prm.ksplit > 1 ? (s.split_all ? 0 : prm.groups / clusters * clusters) : prm.groups;
     if (prm.split_from == prm.groups) prm.ksplit = 1;  // no partial wave: nothing to split
     prm.units = prm.split_from + (prm.groups - prm.split_from) * prm.ksplit;
     prm.tile_flags = nullptr;
     prm.epoch = 0;
+    if (s.split_all && prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE)) {
+      CUDA_OK(cudaMemsetAsync(out, 0, size_t(img_count) * Kb * Pp * Q * 16 * sizeof(float), st));
+      flags |= PSCONV_FLAG_ACCUMULATE;
+    }
     if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE)) {
       const int64_t need = int64_t(prm.groups - prm.split_from) * s.cs;
       if (need > P->flag_cap) {

@@ -243,12 +243,16 @@ __device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, i
 // Per M tile and input-channel group: one halo box into the A ring, then one
 // filter box per (kj, ki) tap into the B ring.
 // split-K work unit u -> (tile group, stage range [ib, ie))
+enum : int { kEpiStore = 0, kEpiFused = 1, kEpiSplit = 2 };
 struct Unit {
   int g, ib, ie, sp;  // sp: split index, -1 for a whole tile
 };
+// SPLITK: the launch splits its tail tiles (EPI == kEpiSplit); otherwise every
+// unit is a whole tile
+template <bool SPLITK>
 __device__ __forceinline__ Unit decode_unit(const ConvParams& p, int u) {
   Unit w;
-  if (u < p.split_from) {  // whole tiles: no divisions on the producer's per-tile path
+  if (!SPLITK || u < p.split_from) {  // whole tiles: no divisions on the producer's per-tile path
     w.g = u;
     w.ib = 0;
     w.ie = p.nst;
@@ -436,9 +440,11 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
   }
 }
 
-// FUSED: bias / ReLU epilogue compiled in (a separate instantiation: the runtime
-// checks alone cost 5% on epilogue-heavy layers, measured on l1 1x1 64->256)
-template <int BN, bool SPLIT3, bool PAIR, bool FUSED>
+// EPI: the output path, each a separate instantiation (runtime checks in the
+// per-block store loop cost 5-10% on epilogue-heavy layers, measured on l1 1x1
+// 64->64 / 64->256): kEpiStore (store, or reduce-add for `+=`), kEpiFused
+// (+ bias / ReLU), kEpiSplit (tail split-K units, flag-ordered partials)
+template <int BN, bool SPLIT3, bool PAIR, int EPI>
 __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     int stage = 0, gs = 0;
     uint32_t phase = 0;
     for (int u = cluster; u < p.units; u += nclusters) {
-      const Unit un = decode_unit(p, u);
+      const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int wq = tc.tq * p.Qb * p.sw - p.pw;
       const int hp = tc.tp * p.Pb * p.sh - p.ph;
@@ -640,9 +646,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     uint32_t phase = 0;
     int cit = 0;  // chunk counter across tiles -> accumulator buffer / phase
     for (int u = cluster; u < p.units; u += nclusters) {
-      const Unit un = decode_unit(p, u);
+      const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
       const int unchunks =
-          un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+          EPI != kEpiSplit || un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -764,17 +770,17 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     if (store_thread) ptx::prefetch_tmap(&tmap_out);
     int cit = 0;
     for (int u = cluster; u < p.units; u += nclusters) {
-      const Unit un = decode_unit(p, u);
+      const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
       const int unchunks =
-          un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
+          EPI != kEpiSplit || un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
       const int kb0 = tc.tk * (BN / 16);
       // split tile (no `+=`): its first unit stores and then raises the tile's
       // flag; the other units reduce-add once the flag shows this launch's epoch
       // (they wait only on smaller unit indices of co-resident persistent CTAs)
-      const bool flagged = un.sp >= 0 && !p.accumulate;
-      const bool reduce = p.accumulate || un.sp > 0;
+      const bool flagged = EPI == kEpiSplit && un.sp >= 0 && !p.accumulate;
+      const bool reduce = p.accumulate || (EPI == kEpiSplit && un.sp > 0);
       int* const flag = flagged ? p.tile_flags + (un.g - p.split_from) * CS + rank : nullptr;
       bool wait_flag = flagged && un.sp > 0;
       for (int c = 0; c < unchunks; ++c, ++cit) {
@@ -815,7 +821,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
           } else if (tc.live) {
             // fused epilogue on the finished sum: + bias[k], ReLU (the same
             // value for all lanes: broadcast loads through L1)
-            if constexpr (FUSED) {
+            if constexpr (EPI == kEpiFused) {
             if (p.bias != nullptr) {
               const float* bj = p.bias + tc.tk * BN + j * DW;
 #pragma unroll
@@ -848,7 +854,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             }
             ptx::fence_proxy_async_smem();
             ptx::named_bar(1, 128);
-            if (store_thread && wait_flag) {
+            if (EPI == kEpiSplit && store_thread && wait_flag) {
               const uint64_t t0 = ptx::globaltimer();
               while (ptx::ld_acquire_gpu(flag) != p.epoch)
                 if (ptx::globaltimer() - t0 > 10000000000ull) __trap();  // 10 s: not co-resident
@@ -880,7 +886,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         }
         __syncwarp();
       }
-      if (store_thread && flagged && un.sp == 0) {  // the tile's first partial is in memory
+      if (EPI == kEpiSplit && store_thread && flagged && un.sp == 0) {  // the tile's first partial is in memory
         ptx::bulk_wait_all();
         ptx::fence_proxy_async_global();
         ptx::st_release_gpu(flag, p.epoch);
@@ -923,7 +929,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       int slot = 0;
       uint32_t sph = 0;
       for (int u = cluster; u < p.units; u += nclusters) {
-        const Unit un = decode_unit(p, u);
+        const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
         for (int it = un.ib; it < un.ie; ++it) {
           ptx::mbar_wait(&full[stage], phase);
           const int nk = min(p.kps, p.ksteps - it * p.kps);
@@ -968,7 +974,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
       }
     } else
     for (int u = cluster; u < p.units; u += nclusters) {
-      const Unit un = decode_unit(p, u);
+      const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
       for (int it = un.ib; it < un.ie; ++it) {
         ptx::mbar_wait(&full[stage], phase);
         // A tiles of the stage: kps x a_pitch bytes (packed box image, or 8 KB

@@ -58,6 +58,7 @@ struct Recipe {
   int fold = 0;                                               // (c,s) fold: C real channels
   int ta = -1;                                                // TMEM-resident A: -1 auto, 0/1
   int ks = 0;                                                 // split-K units per tile, 0 = auto
+  int kt = 0;                                                 // split-K scope: 0 tail wave, 1 all tiles
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -81,6 +82,8 @@ struct Schedule {
   int tmem_a = 0;      // 3xTF32, bn <= 128, not halo: A_hi/A_lo in TMEM (no A_lo smem region)
   int ta = -1;         // recipe request for tmem_a (-1 auto)
   int ksplit = 1;      // split-K: reduction split into ksplit work units per tile
+  int split_all = 0;   // split every tile (zeroed output, all partials reduce-added)
+                       // instead of only the last partial wave's (flag-ordered)
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;

@@ -105,6 +105,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "ks") {
           r.ks = static_cast<int>(parse_int(val, "gpu split-K"));
           if (r.ks < 1 || r.ks > 16) throw ConfigError("gpu ks must be in [1, 16]");
+        } else if (key == "kt") {
+          r.kt = static_cast<int>(parse_int(val, "gpu split-K scope"));
+          if (r.kt != 0 && r.kt != 1) throw ConfigError("gpu kt must be 0 (tail wave) or 1 (all tiles)");
         } else if (key == "ta") {
           r.ta = static_cast<int>(parse_int(val, "gpu TMEM-resident A"));
           if (r.ta != 0 && r.ta != 1) throw ConfigError("gpu ta must be 0 or 1");
@@ -149,6 +152,7 @@ std::string Recipe::id() const {
     if (fold) s += ",fold:" + std::to_string(fold);
     if (ta >= 0) s += ",ta:" + std::to_string(ta);
     if (ks) s += ",ks:" + std::to_string(ks);
+    if (kt) s += ",kt:" + std::to_string(kt);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -361,7 +365,9 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
       }
     }
     s.ksplit = s.halo ? 1 : best;
+    s.split_all = s.ksplit > 1 && r.kt == 1;
     canon.ks = (r.ks || s.ksplit > 1) ? s.ksplit : 0;  // shown when it splits
+    canon.kt = s.split_all ? 1 : 0;
   }
   // Grouped raster (auto): when both the activation rows and the filter of all
   // tiles exceed the L2 share, a wave of 148 concurrent tiles should cover a

@@ -154,7 +154,8 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // ksteps / ks each, with their own drain
   const int ks = std::max(1, s.ksplit);
   const int64_t clusters = m.sms / cs, groups = (mt + cs - 1) / cs * tk;
-  const int64_t waves = groups / clusters, rem = groups - waves * clusters;
+  // (kt:1 splits every tile: no whole-tile waves)
+  const int64_t waves = s.split_all && ks > 1 ? 0 : groups / clusters, rem = groups - waves * clusters;
   const int kt = rem > 0 ? ks : 1;
   const double tile_cyc = double(ksteps) * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
   // (a split unit also refills the pipeline (~1500 cycles) and drains a whole
@@ -189,7 +190,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
   // split-K: every extra unit of a split tile reduce-adds its partial (in L2
   // while the tile's lines stay resident, partly in HBM)
-  if (kt > 1) b.hbm_bytes += out_b * double(rem) / groups * (kt - 1);
+  if (kt > 1) b.hbm_bytes += out_b * double(rem) / groups * (kt - 1) + (s.split_all ? out_b : 0.0);
   b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain

@@ -40,10 +40,11 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
     # tail split-K: the model's split decision both ways
+    # (kt:1 splits every tile instead of the tail wave: faster on some 3xTF32 layers)
     if "ks" in kv:
-        alts.append({**kv, "ks": "1"})
+        alts += [{**kv, "ks": "1"}, {**kv, "kt": "1"}]
     else:
-        alts += [{**kv, "ks": "2"}, {**kv, "ks": "3"}]
+        alts += [{**kv, "ks": "2"}, {**kv, "ks": "3"}, {**kv, "ks": "3", "kt": "1"}]
     # (c,s) fold when the caller knows only c_logical <= 8 of the 16 input channels are
     # real (the stem): the same top candidates over the folded input
     if 0 < c_logical <= 8 and preset.nIfm == 16 and preset.kw > 1:

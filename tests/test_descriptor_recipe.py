@@ -102,3 +102,15 @@ def test_gpu_clause_validation():
     with pytest.raises(ConfigRejectedError):
         ps.model_us(p, "gpu=box:16x16x1")       # > 128 rows
     assert ps.model_us(p, "gpu=bn:32,box:8x8x2,ch:4") > 0
+
+
+def test_split_k_recipe_keys():
+    """Tail split-K (ks) and its scope (kt): ~1.3 waves of tiles -> the split of the
+    partial wave is modelled faster; kt:1 (every tile split) is accepted, kt:2 is not."""
+    p = ConvPreset.parse("conv:256,512,512,7,7,3,3,1,1,16,1,1,7,7")
+    base = "gpu=bn:256,box:1x1x128,cl:1,ch:36"
+    assert ps.model_us(p, base + ",ks:3", "3xtf32") < ps.model_us(p, base + ",ks:1", "3xtf32")
+    assert ps.model_us(p, base + ",ks:3,kt:1", "3xtf32") > 0
+    for bad in (",kt:2", ",ks:0", ",ks:17"):
+        with pytest.raises(ConfigRejectedError):
+            ps.model_us(p, base + bad, "3xtf32")

@@ -371,6 +371,7 @@ TAIL = "conv:8,64,64,56,56,3,3,1,1,16,1,1,56,56"  # 196 tiles of 8x8x2 px: 1 wav
     "gpu=bn:64,box:8x8x2,ks:3",   # 144 tail units after 148 whole tiles
     "gpu=bn:64,box:8x8x2,ks:4",   # 192 tail units: a second round of units
     "gpu=bn:64,box:8x8x2,ks:2,cl:2",  # pairs: 74 clusters, 98 groups
+    "gpu=bn:64,box:8x8x2,ks:3,kt:1",  # every tile split: zeroed output, all partials added
 ])
 def test_tail_split(recipe, mode):
     """Tail split-K: only the last partial wave's tiles are split; a split tile's first
