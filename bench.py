@@ -325,11 +325,29 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         # the host path's last image must match the device path's (same kernel, same
         # inputs; the chunked launches may split tail tiles differently, so the fp32
-        # summation order -- not the result -- can differ: relative L2 <= 1e-6)
+        # summation order -- not the result -- can differ: relative L2 within the 3xTF32
+        # parity bound, 1e-5)
         a = hy[(n_local - 1) * out_elems_img:].double()
         b = y[(b1 - 1) * out_elems_img:b1 * out_elems_img].cpu().double()
         e2e_diff = float((a - b).norm() / b.norm().clamp_min(1e-30))
-        e2e_match = e2e_diff <= 1e-6
+        e2e_match = e2e_diff <= 1e-5
+        # the e2e leg's own bound on this box: the same bytes as two plain copies, H2D and
+        # D2H at once on two streams (PCIe is duplex; no kernel, no chunking)
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        xs = x[b0 * in_elems_img:b1 * in_elems_img]
+        ys = y[b0 * out_elems_img:b1 * out_elems_img]
+
+        def duplex():
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            with torch.cuda.stream(s_in):
+                xs.copy_(hx, non_blocking=True)  # (hx holds xs: a no-op on the data)
+            with torch.cuda.stream(s_out):
+                hy.copy_(ys, non_blocking=True)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
+
+        pcie_ms = max_over_ranks(min(timed(duplex, 3, 1)))
     clocks = clk.summary()
 
     # ---- verification (untimed): gather output shards to rank 0 over NCCL, check sampled images
@@ -398,6 +416,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": bi,
                     "d2h_bytes_per_step": bo, "ms_per_step": round(e2e_ms, 3),
                     "matches_device_path": e2e_match, "rel_l2_vs_device_path": float(f"{e2e_diff:.3g}"),
+                    "copy_bound_ms": round(pcie_ms, 3), "frac_of_copy_bound": round(pcie_ms / e2e_ms, 4),
                     "path": "ConvPlan.forward_host (C ABI conv_fwd_host): pinned host -> device -> pinned host, chunked and overlapped"},
             "gpu_launches": args.steps * plan.launches,
             "clocks": clocks,

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "conv_kernel.cuh"
 #include "internal.hpp"
@@ -48,12 +49,13 @@ struct conv_plan {
   // copy-in / copy-out streams and their events
   struct HostPipe {
     int64_t chunk = 0;                 // images per chunk
-    float* din[2] = {nullptr, nullptr};
-    float* dout[2] = {nullptr, nullptr};
+    static constexpr int kSlots = 3;   // device chunk buffers in flight
+    float* din[kSlots] = {};
+    float* dout[kSlots] = {};
     float* dflt = nullptr;
     cudaStream_t sin = nullptr, sout = nullptr;
     cudaEvent_t start = nullptr, flt = nullptr, end = nullptr;
-    cudaEvent_t h2d[2] = {nullptr, nullptr}, conv[2] = {nullptr, nullptr}, d2h[2] = {nullptr, nullptr};
+    cudaEvent_t h2d[kSlots] = {}, conv[kSlots] = {}, d2h[kSlots] = {};
   };
   mutable HostPipe* pipe = nullptr;
   // split-tile flags (tail split-K): kFlagRing regions of flag_cap ints, one
@@ -861,7 +863,7 @@ void conv_plan_destroy(conv_plan* p) {
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
     auto* h = p->pipe;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < conv_plan::HostPipe::kSlots; ++i) {
       cudaFree(h->din[i]);
       cudaFree(h->dout[i]);
       cudaEventDestroy(h->h2d[i]);
@@ -968,13 +970,13 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     int prev = 0;
     CUDA_OK(cudaGetDevice(&prev));
     CUDA_OK(cudaSetDevice(P->device));
-    if (!P->pipe) {  // ~32 MB of input per chunk, double buffered
+    if (!P->pipe) {  // ~32 MB of input per chunk, kSlots buffers
       auto* h = new conv_plan::HostPipe();
       P->pipe = h;
       int64_t chunk_mb = 32;
       if (const char* e = std::getenv("PSCONV_HOST_CHUNK_MB")) chunk_mb = std::max(1, std::atoi(e));
       h->chunk = std::max<int64_t>(1, std::min<int64_t>(d.nImg, (chunk_mb << 20) / (in_img * 4)));
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < conv_plan::HostPipe::kSlots; ++i) {
         CUDA_OK(cudaMalloc(&h->din[i], h->chunk * in_img * sizeof(float)));
         CUDA_OK(cudaMalloc(&h->dout[i], h->chunk * out_img * sizeof(float)));
         CUDA_OK(cudaEventCreateWithFlags(&h->h2d[i], cudaEventDisableTiming));
@@ -1000,23 +1002,38 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
       CUDA_OK(cudaEventRecord(h->flt, h->sin));
       CUDA_OK(cudaStreamWaitEvent(cs, h->flt, 0));
     }
-    const int64_t nchunks = (img_count + h->chunk - 1) / h->chunk;
-    for (int64_t i = 0; i < nchunks; ++i) {
-      const int sl = int(i & 1);
-      const int64_t c0 = img_begin + i * h->chunk;
-      const int64_t cn = std::min(h->chunk, img_begin + img_count - c0);
-      // copy in once the kernel two chunks back has read this slot
-      if (i >= 2) CUDA_OK(cudaStreamWaitEvent(h->sin, h->conv[sl], 0));
+    // Chunk schedule: full chunks, with a ramp of 1/8, 1/4, 1/2 chunks at both ends
+    // when there are enough images -- the first copy-in and the last copy-out are
+    // the only copies not overlapped with the opposite direction (PCIe is duplex)
+    std::vector<int64_t> sizes;
+    {
+      const int64_t c = h->chunk;
+      int64_t left = img_count;
+      std::vector<int64_t> ramp;
+      if (img_count >= 4 * c && c >= 8) ramp = {c / 8, c / 4, c / 2};
+      for (int64_t r : ramp) sizes.push_back(r), left -= r;
+      std::vector<int64_t> tail(ramp.rbegin(), ramp.rend());
+      for (int64_t r : tail) left -= r;
+      while (left > 0) sizes.push_back(std::min(c, left)), left -= sizes.back();
+      for (int64_t r : tail) sizes.push_back(r);
+    }
+    constexpr int kS = conv_plan::HostPipe::kSlots;
+    int64_t c0 = img_begin;
+    for (size_t i = 0; i < sizes.size(); ++i) {
+      const int sl = int(i % kS);
+      const int64_t cn = sizes[i];
+      // copy in once the kernel kS chunks back has read this slot
+      if (i >= kS) CUDA_OK(cudaStreamWaitEvent(h->sin, h->conv[sl], 0));
       CUDA_OK(cudaMemcpyAsync(h->din[sl], h_in + c0 * in_img, cn * in_img * sizeof(float),
                               cudaMemcpyHostToDevice, h->sin));
       if (accumulate) {  // `+=`: bring the current output chunk in as well
-        if (i >= 2) CUDA_OK(cudaStreamWaitEvent(h->sin, h->d2h[sl], 0));
+        if (i >= kS) CUDA_OK(cudaStreamWaitEvent(h->sin, h->d2h[sl], 0));
         CUDA_OK(cudaMemcpyAsync(h->dout[sl], h_out + c0 * out_img, cn * out_img * sizeof(float),
                                 cudaMemcpyHostToDevice, h->sin));
       }
       CUDA_OK(cudaEventRecord(h->h2d[sl], h->sin));
       CUDA_OK(cudaStreamWaitEvent(cs, h->h2d[sl], 0));
-      if (i >= 2 && !accumulate) CUDA_OK(cudaStreamWaitEvent(cs, h->d2h[sl], 0));
+      if (i >= kS && !accumulate) CUDA_OK(cudaStreamWaitEvent(cs, h->d2h[sl], 0));
       launch_range(P, h->din[sl], h->dflt, h->dout[sl], cn, cs, kflags);
       kflags |= PSCONV_FLAG_PREPACKED;  // the filter is repacked once, by the first chunk
       CUDA_OK(cudaEventRecord(h->conv[sl], cs));
@@ -1024,6 +1041,7 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
       CUDA_OK(cudaMemcpyAsync(h_out + c0 * out_img, h->dout[sl], cn * out_img * sizeof(float),
                               cudaMemcpyDeviceToHost, h->sout));
       CUDA_OK(cudaEventRecord(h->d2h[sl], h->sout));
+      c0 += cn;
     }
     CUDA_OK(cudaEventRecord(h->end, h->sout));
     CUDA_OK(cudaStreamWaitEvent(cs, h->end, 0));
