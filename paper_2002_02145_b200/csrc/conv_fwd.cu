@@ -622,11 +622,12 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
       prm.a_lo_off = h.a_lo_off;
       prm.hb_stages = s.hb_stages;
       prm.hb_stage_bytes = h.b_stage;
+      prm.b_res = s.b_res;
       prm.b_lo_off = h.b_lo_off;
       prm.hb_ring_off = prm.stages * h.a_stage;
-      prm.ring_bytes = prm.hb_ring_off + prm.hb_stages * h.b_stage;
+      prm.ring_bytes = prm.hb_ring_off + (s.b_res ? int(R * S) * prm.cbg : prm.hb_stages) * h.b_stage;
       prm.nst = prm.cbg * R * S;  // taps per tile (B stages)
-      if (prm.stages > kHaloB || prm.hb_stages < 2 || prm.hb_stages > kMaxStages - kHaloB)
+      if (prm.stages > kHaloB || prm.hb_stages < (s.b_res ? 1 : 2) || prm.hb_stages > kMaxStages - kHaloB)
         throw RuntimeError("internal: bad halo stage plan");
     }
     if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)

@@ -80,6 +80,9 @@ struct ConvParams {
   // (one (kj, ki) filter box over the kps blocks) at hb_ring_off.
   int halo, hw, hr, a_tile;
   int hb_stages, hb_stage_bytes, hb_ring_off;
+  int b_res;                      // halo: the CTA's whole filter slice (R*S*cbg boxes of
+                                  // hb_stage_bytes at hb_ring_off) loaded once and kept
+                                  // resident (one N tile); no B ring
   int cb_group;                   // 1: a stage = kps channel blocks at one (kj, ki), one B box
                                   // spanning them; 0: kps consecutive k-steps, one box each
   int a_boxes;                    // A boxes per coordinate step: 1 (spans the step's blocks;
@@ -282,6 +285,26 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   const int taps = p.R * p.S;
   int as = 0, bs = 0, gs = 0;
   uint32_t aph = 0, bph = 0;
+  if (p.b_res) {
+    // resident filter slice: every (channel group, tap) box once, one barrier
+    // (PAIR: each CTA loads its BN/2 rows, completing on the leader's barrier)
+    const int k0 = rank * Cfg::kBRows;  // single N tile (tiles_k == 1)
+    if (ptx::elect_one()) {
+      if (!PAIR || leader) ptx::mbar_expect_tx(&full[kHaloB], b_tx * p.cbg * taps);
+      for (int cg = 0; cg < p.cbg; ++cg)
+        for (int t = 0; t < taps; ++t) {
+          uint8_t* sb = smem + p.hb_ring_off + (cg * taps + t) * p.hb_stage_bytes;
+          const int cb = cg * p.kps;
+          if (!PAIR) {
+            ptx::tma_load_4d(sb, tmap_flt, &full[kHaloB], 0, k0, t, cb >> p.b128);
+            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[kHaloB], 0, k0, t, cb >> p.b128);
+          } else {
+            ptx::tma_load_4d_cb(sb, tmap_flt, full_leader + 8u * kHaloB, 0, k0, t, cb >> p.b128);
+          }
+        }
+    }
+    __syncwarp();
+  }
   for (int g = cluster; g < p.groups; g += nclusters) {
     const TileCoord tc = decode_group(p, g, rank, CS);
     const int hp = tc.tp * p.Pb - p.ph;
@@ -305,7 +328,7 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
         as = 0;
         aph ^= 1;
       }
-      for (int t = 0; t < taps; ++t) {
+      for (int t = 0; t < taps && !p.b_res; ++t) {
         const int bi = kHaloB + bs;
         const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[gs * 4 + 0] = clock64();
@@ -334,6 +357,93 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   }
 }
 
+// Halo-mode MMA issuer with the filter resident (b_res), 3x3 taps, one
+// accumulation chunk per tile: per (tile, channel group) one elected thread
+// issues all 9 x KPS x 2 (x3 in 3xTF32) MMAs with compile-time tap offsets
+// (A: kj*hw + ki rows into the halo tile; B: box t of the group). The generic
+// issuer's per-tap bookkeeping (~200-400 cycles per tap, measured with the
+// clock trace) starves the tensor core at N = 64 (48-cycle MMAs).
+template <int BN, bool SPLIT3, bool PAIR, int KPS>
+__device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem, uint64_t* full,
+                                             uint64_t* split_full, uint64_t* empty, uint64_t* acc_full,
+                                             uint64_t* acc_empty, uint32_t tmem_base, int cluster,
+                                             int nclusters, uint32_t idesc) {
+  using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+  constexpr int kAccBufs = Cfg::kAccBufs;
+  const uint64_t adesc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
+  const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : adesc0;
+  const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);
+  const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
+  const uint32_t a_tile = static_cast<uint32_t>(p.a_tile) >> 4;
+  const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
+  const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
+  const uint32_t hw4 = static_cast<uint32_t>(p.hw) * 4u;  // one row = 64 B = 4 desc units
+  const uint32_t bstep = static_cast<uint32_t>(p.hb_stage_bytes) >> 4;
+  const uint32_t bres = static_cast<uint32_t>(p.hb_ring_off) >> 4;
+  const uint32_t astage = static_cast<uint32_t>(p.stage_bytes) >> 4;
+  const bool skip_mma = (p.debug & 2) != 0;
+  ptx::mbar_wait(&full[kHaloB], 0);  // resident filter slice landed (both CTAs')
+  ptx::tc_fence_after();
+  int as = 0, cit = 0;
+  uint32_t aph = 0;
+  for (int g = cluster; g < p.groups; g += nclusters, ++cit) {
+    const int buf = kAccBufs == 1 ? 0 : (cit & 1);
+    const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
+    if (PAIR)
+      ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
+    else
+      ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
+    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+    for (int cg = 0; cg < p.cbg; ++cg) {
+      ptx::mbar_wait(&full[as], aph);  // PAIR: both CTAs' halos landed
+      if (SPLIT3) ptx::mbar_wait(&split_full[as], aph);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        const uint64_t a0 = adesc0 + static_cast<uint32_t>(as) * astage;
+        const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(cg * 9) * bstep;
+        uint32_t acc_in = cg == 0 ? 0u : 1u;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          uint64_t da = a0 + static_cast<uint32_t>(t / 3) * hw4 + static_cast<uint32_t>(t % 3) * 4u;
+          uint64_t db = b0 + static_cast<uint32_t>(t) * bstep;
+#pragma unroll
+          for (int j = 0; j < KPS; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (!skip_mma) {
+                if (SPLIT3) {
+                  ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, acc_in);
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + blo_off + h * 2, idesc, 1u);
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, 1u);
+                } else if (PAIR) {
+                  ptx::mma_tf32_pair(d_tmem, da + h * 2, db + h * 2, idesc, acc_in);
+                } else {
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, acc_in);
+                }
+              }
+              acc_in = 1u;
+            }
+            da += a_tile;
+            db += (j & 1) ? b_odd : b_even;
+          }
+        }
+        if (PAIR) {
+          ptx::mma_commit_pair(&empty[as]);
+          if (cg == p.cbg - 1) ptx::mma_commit_pair(&acc_full[buf]);
+        } else {
+          ptx::mma_commit(&empty[as]);
+          if (cg == p.cbg - 1) ptx::mma_commit(&acc_full[buf]);
+        }
+      }
+      __syncwarp();
+      if (++as == p.stages) {
+        as = 0;
+        aph ^= 1;
+      }
+    }
+  }
+}
+
 // Halo-mode MMA issuer (warp 1 of the single CTA / pair leader). Walks the same
 // (channel group, tap) sequence; accumulation chunks are counted in taps.
 template <int BN, bool SPLIT3, bool PAIR>
@@ -355,6 +465,10 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
   const bool skip_mma = (p.debug & 2) != 0;
   int as = 0, bs = 0, cit = 0, gs = 0;
   uint32_t aph = 0, bph = 0;
+  if (p.b_res) {
+    ptx::mbar_wait(&full[kHaloB], 0);  // resident filter slice landed (both CTAs')
+    ptx::tc_fence_after();
+  }
   for (int g = cluster; g < p.groups; g += nclusters) {
     int tg = 0;  // tap index within the tile's reduction
     int cc = 0;  // taps into the current accumulation chunk
@@ -379,13 +493,16 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
         const int bi = kHaloB + bs;
         const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
         if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
-        ptx::mbar_wait(&full[bi], bph);
-        ptx::tc_fence_after();
+        if (!p.b_res) {
+          ptx::mbar_wait(&full[bi], bph);
+          ptx::tc_fence_after();
+        }
         if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
         if (ptx::elect_one()) {
           uint64_t da = adesc0 + ((static_cast<uint32_t>(as * p.stage_bytes) +
                                    static_cast<uint32_t>(r * p.hw + sx) * 64u) >> 4);
-          uint64_t db = bdesc0 + ((static_cast<uint32_t>(p.hb_ring_off + bs * p.hb_stage_bytes)) >> 4);
+          const int bslot = p.b_res ? cg * taps + t : bs;
+          uint64_t db = bdesc0 + ((static_cast<uint32_t>(p.hb_ring_off + bslot * p.hb_stage_bytes)) >> 4);
           uint32_t acc_in = chunk_start ? 0u : 1u;
           for (int j = 0; j < kps && !skip_mma; ++j) {
 #pragma unroll
@@ -405,11 +522,11 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
             db += (j & 1) ? b_odd : b_even;
           }
           if (PAIR) {
-            ptx::mma_commit_pair(&empty[bi]);
+            if (!p.b_res) ptx::mma_commit_pair(&empty[bi]);
             if (t == taps - 1) ptx::mma_commit_pair(&empty[as]);
             if (chunk_end) ptx::mma_commit_pair(&acc_full[buf]);
           } else {
-            ptx::mma_commit(&empty[bi]);
+            if (!p.b_res) ptx::mma_commit(&empty[bi]);
             if (t == taps - 1) ptx::mma_commit(&empty[as]);
             if (chunk_end) ptx::mma_commit(&acc_full[buf]);
           }
@@ -621,8 +738,20 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     }
     }  // !halo
   } else if (warp == 1 && leader && p.halo) {
-    halo_mma<BN, SPLIT3, PAIR>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
-                               cluster, nclusters, kIdesc);
+    // resident filter, 3x3, one chunk per tile: the lean issuer
+    const bool res_fast = p.b_res && p.R == 3 && p.S == 3 && p.chunk_stages >= p.nst;
+    if (res_fast && p.kps == 4)
+      halo_mma_res<BN, SPLIT3, PAIR, 4>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
+                                        cluster, nclusters, kIdesc);
+    else if (res_fast && p.kps == 2)
+      halo_mma_res<BN, SPLIT3, PAIR, 2>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
+                                        cluster, nclusters, kIdesc);
+    else if (res_fast && p.kps == 1)
+      halo_mma_res<BN, SPLIT3, PAIR, 1>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
+                                        cluster, nclusters, kIdesc);
+    else
+      halo_mma<BN, SPLIT3, PAIR>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
+                                 cluster, nclusters, kIdesc);
   } else if (warp == 1 && leader) {
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues tcgen05.mma / commit.

@@ -59,6 +59,7 @@ struct Recipe {
   int ta = -1;                                                // TMEM-resident A: -1 auto, 0/1
   int ks = 0;                                                 // split-K units per tile, 0 = auto
   int kt = 0;                                                 // split-K scope: 0 tail wave, 1 all tiles
+  int br = -1;                                                // halo: resident filter, -1 auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
@@ -79,6 +80,8 @@ struct Schedule {
   int halo = 0;        // halo mode: Pb whole output rows, input halo loaded once per block
   int m_block = 0;     // grouped raster block (M groups); 0 = the recipe's loop order
   int hb_stages = 0;   // halo: B-ring stages
+  int b_res = 0;       // halo: whole filter slice resident in smem (one N tile), no B ring
+  int br = -1;         // recipe request for b_res (-1 auto)
   int tmem_a = 0;      // 3xTF32, bn <= 128, not halo: A_hi/A_lo in TMEM (no A_lo smem region)
   int ta = -1;         // recipe request for tmem_a (-1 auto)
   int ksplit = 1;      // split-K: reduction split into ksplit work units per tile

@@ -105,6 +105,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "ks") {
           r.ks = static_cast<int>(parse_int(val, "gpu split-K"));
           if (r.ks < 1 || r.ks > 16) throw ConfigError("gpu ks must be in [1, 16]");
+        } else if (key == "br") {
+          r.br = static_cast<int>(parse_int(val, "gpu resident filter"));
+          if (r.br != 0 && r.br != 1) throw ConfigError("gpu br must be 0 or 1");
         } else if (key == "kt") {
           r.kt = static_cast<int>(parse_int(val, "gpu split-K scope"));
           if (r.kt != 0 && r.kt != 1) throw ConfigError("gpu kt must be 0 (tail wave) or 1 (all tiles)");
@@ -153,6 +156,7 @@ std::string Recipe::id() const {
     if (ta >= 0) s += ",ta:" + std::to_string(ta);
     if (ks) s += ",ks:" + std::to_string(ks);
     if (kt) s += ",kt:" + std::to_string(kt);
+    if (br >= 0) s += ",br:" + std::to_string(br);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -312,6 +316,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.fold = r.fold;
   canon.ta = r.ta;
   s.ta = r.ta;
+  s.br = r.br;
+  canon.br = r.br;
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
@@ -437,6 +443,32 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
     const bool want = s.ta == 1 || (s.ta < 0 && s.bn <= 64);
     s.tmem_a = (ok && want && std::getenv("PSCONV_NO_TMEMA") == nullptr) ? 1 : 0;
   }
+  if (s.halo && s.br != 0 && d.nOfm == s.bn) {
+    // resident filter (one N tile): the CTA's whole filter slice -- R*S*Cb/kps boxes
+    // -- loaded once; the rest of the budget is A halo stages (>= 2, <= 8). The B
+    // ring's per-tap round trip (<= 8 stages in flight over ~1-2 us of L2
+    // latency) bounds the ringed halo mode; auto whenever it fits.
+    for (int k : {4, 2, 1}) {
+      if (kg && k != kg) continue;
+      if (Cb % k) continue;
+      Schedule t = s;
+      t.kps = k;
+      const HaloGeom h = halo_geom(d, t, mode);
+      const int64_t bres = int64_t(d.kh * d.kw) * (Cb / k) * h.b_stage;
+      const int64_t left = kSmemStageBudget - bres;
+      const int a = left > 0 ? static_cast<int>(std::min<int64_t>(8, left / h.a_stage)) : 0;
+      if (a >= 2) {
+        s.kps = k;
+        s.stages = a;
+        s.hb_stages = 1;
+        s.b_res = 1;
+        return;
+      }
+    }
+    if (s.br == 1) throw ConfigError("GPU tile: resident filter (br:1) does not fit in shared memory");
+  }
+  if (s.br == 1 && !(s.halo && d.nOfm == s.bn))
+    throw ConfigError("GPU tile: br:1 needs halo mode and a single N tile (bn == nOfm)");
   if (s.halo) {
     // A ring of 2 halo stages, the rest B stages (<= 8 each); largest kps in
     // {4, 2, 1} dividing Cb that leaves >= 3 B stages

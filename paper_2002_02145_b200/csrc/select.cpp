@@ -116,7 +116,6 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const int cs = std::max(1, s.cs);
   const double a_box = double(s.qb) * s.pb * s.nb * 64.0;
   const double b_rows = double(s.bn) / cs;
-  const double deliver_b = a_box + b_rows * 64.0 * (mult > 1 ? 2 : 1);
   // MMA: two K=8 MMAs per k-step (x3 for 3xTF32) of max(BN/2, 46) cycles each --
   // an M=128 tf32 MMA takes >= ~46 cycles whatever N (tools/probe_mma_rate.cu:
   // N=64 48, N=128 64, N=256 128 cycles)
@@ -126,7 +125,17 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows
   // are 128 B when a stage pairs channel blocks (b128), halving their count.
   const bool b128 = s.kps % 2 == 0 && g.Cb % std::max(1, s.kps) == 0;
-  const double rows = double(s.qb) * s.pb * s.nb + b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0);
+  double rows = double(s.qb) * s.pb * s.nb + b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0);
+  double a_bytes = a_box;  // TMA writes of A per k-step
+  if (s.halo) {
+    // halo mode: the (Pb + R - 1) x (Q + S - 1) halo of a channel block is loaded
+    // once for its R*S taps; the filter is resident (b_res: loaded once per CTA)
+    // or streamed per tap through the B ring
+    const double halo_rows = double(s.pb + g.R - 1) * (g.Q + g.S - 1) / (double(g.R) * g.S);
+    rows = halo_rows + (s.b_res ? 0.0 : b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0));
+    a_bytes = halo_rows * 64.0;
+  }
+  const double deliver_b = a_bytes + (s.halo && s.b_res ? 0.0 : b_rows * 64.0 * (mult > 1 ? 2 : 1));
   const double del_cyc = rows / m.row_requests_per_cycle;
   // operand reads per k-step: 2 K-halves x (A 4 KB + B rows x 32 B) per MMA; with
   // TMEM-resident A (3xTF32) the MMAs read only B and the splitter reads A once
@@ -140,7 +149,14 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // + per-stage issue cost (barrier round trip, TMA issue ~45 cycles each, MMA
   // commit) amortised over the stage's kps k-steps
   const double boxes = s.kps > 1 && g.Cb % s.kps == 0 ? 2.0 : 2.0 * std::max(1, s.kps);
-  const double stage_cyc = m.kstep_sync_cyc * 4 + 45.0 * boxes;
+  double stage_cyc = m.kstep_sync_cyc * 4 + 45.0 * boxes;
+  if (s.halo) {
+    // halo issuers (clock trace, l1 3x3 TF32): the generic one spends ~300 cycles
+    // of bookkeeping per tap (kps k-steps); the resident-filter 3x3 one issues a
+    // whole channel group (9 taps) per ~300 cycles
+    const bool fast = s.b_res && g.R == 3 && g.S == 3 && (s.chunk <= 0 || s.chunk >= ksteps);
+    stage_cyc = fast ? 300.0 / 9.0 : 300.0;
+  }
   kstep_cyc = std::max(kstep_cyc, del_cyc) + stage_cyc / std::max(1, s.kps);
   const int chunk = s.chunk > 0 ? s.chunk : static_cast<int>(ksteps);
   const double nchunks = std::ceil(double(ksteps) / chunk);
@@ -174,7 +190,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.us_mma = mma_cyc * to_us;
   b.us_smem_traffic = smem_cyc * to_us;
   b.us_rows = del_cyc * to_us;
-  b.l2_bytes = ksteps * (a_box + s.bn * 64.0 * (mult > 1 ? 2 : 1) / std::max(1, s.cs)) * tiles;
+  b.l2_bytes = ksteps * (a_bytes + (s.halo && s.b_res ? 0.0 : s.bn * 64.0 * (mult > 1 ? 2 : 1) / cs)) * tiles;
   b.us_l2 = b.l2_bytes / (m.l2_gbs * 1e9) * 1e6;
   (void)per_sm;
 
@@ -228,6 +244,21 @@ std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
         r.box_n = n;
         Schedule s = resolve_schedule(d, r, mode);
         if (seen.insert(s.recipe_id).second) out.push_back(s);
+      }
+  // halo mode (stride-1 R x S > 1): its own tile shape (whole padded rows)
+  if (halo_eligible(d))
+    for (const char* perm : kPerms)
+      for (int bn : bns) {
+        Recipe r = Recipe::parse(std::string("perm=") + perm);
+        r.has_gpu = true;
+        r.bn = bn;
+        r.halo = 1;
+        try {
+          Schedule s = resolve_schedule(d, r, mode);
+          if (seen.insert(s.recipe_id).second) out.push_back(s);
+        } catch (const ConfigError&) {
+          // the halo tile does not fit at this bn
+        }
       }
   return out;
 }

@@ -127,11 +127,27 @@ def test_stage_geometry(conv, c_log, recipe, mode):
 ])
 def test_halo_mode(conv, c_log, recipe, mode):
     """Halo mode: whole output rows at the padded pitch, the input halo loaded once per
-    channel block and the R*S shifted operands addressed in place."""
+    channel block and the R*S shifted operands addressed in place; with the filter slice
+    resident in smem (auto when bn == nOfm and it fits) and with the B ring (br:0)."""
     n = ps.ConvPreset.parse(conv).nImg
-    _check("halo", conv, c_log, 9, mode, n, recipe + (",cl:1" if mode == "tf32" else ""))
-    if mode == "tf32":
-        _check("halo-pair", conv, c_log, 9, mode, n, recipe + ",cl:2")
+    for br in ("", ",br:0"):
+        _check("halo" + br, conv, c_log, 9, mode, n, recipe + br + (",cl:1" if mode == "tf32" else ""))
+        if mode == "tf32":
+            _check("halo-pair" + br, conv, c_log, 9, mode, n, recipe + br + ",cl:2")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,recipe", [
+    ("tf32", "gpu=bn:64,halo:1,br:1,cl:1"),
+    ("tf32", "gpu=bn:64,halo:1,br:1,cl:2"),
+    ("tf32", "gpu=bn:64,halo:1,br:1,kg:2"),
+    ("3xtf32", "gpu=bn:32,halo:1,br:1"),
+])
+def test_halo_resident_filter(mode, recipe):
+    """br:1 -- the whole filter slice resident in shared memory, only halo tiles stream."""
+    conv = "conv:2,64,64,56,56,3,3,1,1,16,1,1,56,56" if "bn:64" in recipe else \
+        "conv:3,32,32,20,20,3,3,1,1,16,1,1,20,20"
+    _check("halo-br", conv, int(conv.split(",")[1]), 9, mode, ps.ConvPreset.parse(conv).nImg, recipe)
 
 
 @pytest.mark.gpu
