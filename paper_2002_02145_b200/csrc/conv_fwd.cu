@@ -685,7 +685,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.debug = debug_env;
   static unsigned long long* trace_buf = nullptr;
   if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, (8 * kTraceStages + 8) * 8));
-  prm.debug = debug_env & 7;
+  prm.debug = debug_env & ~8;  // 1 2 4: skip loads / MMAs / stores; 16: generic halo issuer
   prm.trace = (debug_env & 8) ? trace_buf : nullptr;
   prm.out = out;
   prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;

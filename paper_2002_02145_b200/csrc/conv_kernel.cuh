@@ -357,14 +357,15 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   }
 }
 
-// Halo-mode MMA issuer with the filter resident (b_res), 3x3 taps, one
-// accumulation chunk per tile: per (tile, channel group) one elected thread
-// issues all 9 x KPS x 2 (x3 in 3xTF32) MMAs with compile-time tap offsets
-// (A: kj*hw + ki rows into the halo tile; B: box t of the group). The generic
-// issuer's per-tap bookkeeping (~200-400 cycles per tap, measured with the
-// clock trace) starves the tensor core at N = 64 (48-cycle MMAs).
-template <int BN, bool SPLIT3, bool PAIR, int KPS>
-__device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem, uint64_t* full,
+// Lean halo-mode MMA issuer for 3x3 taps with one accumulation chunk per tile:
+// per (tile, channel group) one elected thread issues all 9 x KPS x 2 (x3 in
+// 3xTF32) MMAs with compile-time tap offsets (A: kj*hw + ki rows into the halo
+// tile). BRES: the filter is resident (box t of the group); otherwise the
+// thread waits for each tap's B-ring stage and releases it by a commit. The
+// generic issuer's per-tap bookkeeping (~200-400 cycles per tap, measured with
+// the clock trace) starves the tensor core at N = 64 (48-cycle MMAs).
+template <int BN, bool SPLIT3, bool PAIR, int KPS, bool BRES>
+__device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem, uint64_t* full,
                                              uint64_t* split_full, uint64_t* empty, uint64_t* acc_full,
                                              uint64_t* acc_empty, uint32_t tmem_base, int cluster,
                                              int nclusters, uint32_t idesc) {
@@ -382,10 +383,12 @@ __device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem,
   const uint32_t bres = static_cast<uint32_t>(p.hb_ring_off) >> 4;
   const uint32_t astage = static_cast<uint32_t>(p.stage_bytes) >> 4;
   const bool skip_mma = (p.debug & 2) != 0;
-  ptx::mbar_wait(&full[kHaloB], 0);  // resident filter slice landed (both CTAs')
-  ptx::tc_fence_after();
-  int as = 0, cit = 0;
-  uint32_t aph = 0;
+  if (BRES) {
+    ptx::mbar_wait(&full[kHaloB], 0);  // resident filter slice landed (both CTAs')
+    ptx::tc_fence_after();
+  }
+  int as = 0, cit = 0, bs = 0;
+  uint32_t aph = 0, bph = 0;
   for (int g = cluster; g < p.groups; g += nclusters, ++cit) {
     const int buf = kAccBufs == 1 ? 0 : (cit & 1);
     const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -400,12 +403,18 @@ __device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem,
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
         const uint64_t a0 = adesc0 + static_cast<uint32_t>(as) * astage;
-        const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(cg * 9) * bstep;
+        const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(BRES ? cg * 9 : 0) * bstep;
         uint32_t acc_in = cg == 0 ? 0u : 1u;
+        int ts = bs;
+        uint32_t tph = bph;
 #pragma unroll
         for (int t = 0; t < 9; ++t) {
           uint64_t da = a0 + static_cast<uint32_t>(t / 3) * hw4 + static_cast<uint32_t>(t % 3) * 4u;
-          uint64_t db = b0 + static_cast<uint32_t>(t) * bstep;
+          uint64_t db = b0 + static_cast<uint32_t>(BRES ? t : ts) * bstep;
+          if (!BRES) {
+            ptx::mbar_wait(&full[kHaloB + ts], tph);  // this tap's filter box landed
+            ptx::tc_fence_after();
+          }
 #pragma unroll
           for (int j = 0; j < KPS; ++j) {
 #pragma unroll
@@ -426,6 +435,16 @@ __device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem,
             da += a_tile;
             db += (j & 1) ? b_odd : b_even;
           }
+          if (!BRES) {  // release the tap's B stage once its MMAs completed
+            if (PAIR)
+              ptx::mma_commit_pair(&empty[kHaloB + ts]);
+            else
+              ptx::mma_commit(&empty[kHaloB + ts]);
+            if (++ts == p.hb_stages) {
+              ts = 0;
+              tph ^= 1;
+            }
+          }
         }
         if (PAIR) {
           ptx::mma_commit_pair(&empty[as]);
@@ -436,6 +455,12 @@ __device__ __forceinline__ void halo_mma_res(const ConvParams& p, uint8_t* smem,
         }
       }
       __syncwarp();
+      if (!BRES)
+        for (int t = 0; t < 9; ++t)  // warp-uniform copy of the B-ring position
+          if (++bs == p.hb_stages) {
+            bs = 0;
+            bph ^= 1;
+          }
       if (++as == p.stages) {
         as = 0;
         aph ^= 1;
@@ -738,17 +763,18 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     }
     }  // !halo
   } else if (warp == 1 && leader && p.halo) {
-    // resident filter, 3x3, one chunk per tile: the lean issuer
-    const bool res_fast = p.b_res && p.R == 3 && p.S == 3 && p.chunk_stages >= p.nst;
-    if (res_fast && p.kps == 4)
-      halo_mma_res<BN, SPLIT3, PAIR, 4>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
-                                        cluster, nclusters, kIdesc);
-    else if (res_fast && p.kps == 2)
-      halo_mma_res<BN, SPLIT3, PAIR, 2>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
-                                        cluster, nclusters, kIdesc);
-    else if (res_fast && p.kps == 1)
-      halo_mma_res<BN, SPLIT3, PAIR, 1>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
-                                        cluster, nclusters, kIdesc);
+    // 3x3, one chunk per tile: the lean issuer (resident filter or B ring)
+    const bool fast = p.R == 3 && p.S == 3 && p.chunk_stages >= p.nst && (p.debug & 16) == 0;
+#define PSCONV_HALO_FAST(K, R)                                                                         \
+  halo_mma_fast<BN, SPLIT3, PAIR, K, R>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base, \
+                                        cluster, nclusters, kIdesc)
+    if (fast && p.b_res && p.kps == 4) PSCONV_HALO_FAST(4, true);
+    else if (fast && p.b_res && p.kps == 2) PSCONV_HALO_FAST(2, true);
+    else if (fast && p.b_res && p.kps == 1) PSCONV_HALO_FAST(1, true);
+    else if (fast && p.kps == 4) PSCONV_HALO_FAST(4, false);
+    else if (fast && p.kps == 2) PSCONV_HALO_FAST(2, false);
+    else if (fast && p.kps == 1) PSCONV_HALO_FAST(1, false);
+#undef PSCONV_HALO_FAST
     else
       halo_mma<BN, SPLIT3, PAIR>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
                                  cluster, nclusters, kIdesc);

@@ -152,10 +152,11 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   double stage_cyc = m.kstep_sync_cyc * 4 + 45.0 * boxes;
   if (s.halo) {
     // halo issuers (clock trace, l1 3x3 TF32): the generic one spends ~300 cycles
-    // of bookkeeping per tap (kps k-steps); the resident-filter 3x3 one issues a
-    // whole channel group (9 taps) per ~300 cycles
-    const bool fast = s.b_res && g.R == 3 && g.S == 3 && (s.chunk <= 0 || s.chunk >= ksteps);
-    stage_cyc = fast ? 300.0 / 9.0 : 300.0;
+    // of bookkeeping per tap (kps k-steps); the lean 3x3 one (one chunk per tile)
+    // issues a whole channel group (9 taps) per ~300 cycles, + a B-ring wait per
+    // tap when the filter is not resident
+    const bool fast = g.R == 3 && g.S == 3 && (s.chunk <= 0 || s.chunk >= ksteps);
+    stage_cyc = fast ? (s.b_res ? 300.0 / 9.0 : 60.0) : 300.0;
   }
   kstep_cyc = std::max(kstep_cyc, del_cyc) + stage_cyc / std::max(1, s.kps);
   const int chunk = s.chunk > 0 ? s.chunk : static_cast<int>(ksteps);

@@ -15,10 +15,10 @@ using namespace psconv;
 constexpr int N = 256, Cb = 4, H = 56, W = 56;
 
 __global__ void k_load(const __grid_constant__ CUtensorMap m, int loads, int stages, int w0, int bw, int bh,
-                       int bn, uint32_t box_bytes, int stride_bytes, long long* out) {
+                       int bn, uint32_t box_bytes, int stride_bytes, int nmax, long long* out) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar[16];
+  __shared__ uint64_t bar[16];  // <= 16 stages
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) ptx::mbar_init(&bar[s], 1);
     ptx::fence_mbar_init();
@@ -26,24 +26,23 @@ __global__ void k_load(const __grid_constant__ CUtensorMap m, int loads, int sta
   __syncthreads();
   if (threadIdx.x != 0) return;
   ptx::prefetch_tmap(&m);
-  const int tiles_h = H / bh, tiles_n = N / bn;
   long long t0 = clock64();
-  uint32_t ph[16] = {};
+  uint32_t ph = 0;  // phase bits (a register, not a local array)
   for (int i = 0; i < loads; ++i) {
-    const int s = i % stages;
+    const int s = i & (stages - 1);  // stages: a power of two
     if (i >= stages) {
-      ptx::mbar_wait(&bar[s], ph[s]);
-      ph[s] ^= 1;
+      ptx::mbar_wait(&bar[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
     }
-    const int t = blockIdx.x + i * gridDim.x;  // distinct tiles across the grid
-    const int cb = t % Cb, hp = (t / Cb) % tiles_h, n = (t / Cb / tiles_h) % tiles_n;
+    // (bit ops only: runtime divisions here would cost more than the loads)
+    const int cb = i & 3, hp = (i >> 2) & 7, n = ((i >> 5) + blockIdx.x) & (nmax - 1);
     ptx::mbar_expect_tx(&bar[s], box_bytes);
     ptx::tma_load_5d(sm + s * stride_bytes, &m, &bar[s], 0, w0, hp * bh - (w0 < 0 ? 1 : 0), n * bn, cb);
   }
   for (int i = loads; i < loads + stages; ++i) {
-    const int s = i % stages;
-    ptx::mbar_wait(&bar[s], ph[s]);
-    ph[s] ^= 1;
+    const int s = i & (stages - 1);
+    ptx::mbar_wait(&bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
   }
   long long t1 = clock64();
   if (blockIdx.x == 0) out[0] = t1 - t0;
@@ -67,43 +66,41 @@ int main() {
   cudaFuncSetAttribute(k_load, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   struct Case {
     const char* name;
-    int w0, bw, bh, bn, stages;
-    CUtensorMapL2promotion l2;
+    int w0, bw, bh, bn;
   } cases[] = {
-      {"halo 58x4 (w0=-1)", -1, 58, 4, 1, 3, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-      {"halo 58x4 (w0=-1)", -1, 58, 4, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-      {"halo 58x4 none", -1, 58, 4, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_NONE},
-      {"halo 58x4 256B", -1, 58, 4, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_256B},
-      {"56x4 (w0=0)", 0, 56, 4, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-      {"64x2 (w0=0, right OOB)", 0, 64, 2, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-      {"8x4x4", 0, 8, 4, 4, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-      {"56x2", 0, 56, 2, 1, 8, CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
+      {"halo 58x4 (w0=-1)", -1, 58, 4, 1},
+      {"8x4x4", 0, 8, 4, 4},
+      {"56x2", 0, 56, 2, 1},
   };
-  for (const Case& c : cases) {
-    // [16c][W][H][img][Cb] over NCHW16c = [img][Cb][H][W][16]
-    cuuint64_t dims[5] = {16, W, H, N, Cb};
-    cuuint64_t strides[4] = {64, uint64_t(W) * 64, uint64_t(Cb) * H * W * 64, uint64_t(H) * W * 64};
-    cuuint32_t box[5] = {16, cuuint32_t(c.bw), cuuint32_t(c.bh), cuuint32_t(c.bn), 1};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    CUtensorMap m;
-    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, x, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, c.l2,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      printf("%s: encode failed %d\n", c.name, int(r));
-      continue;
-    }
-    const uint32_t bytes = 64u * c.bw * c.bh * c.bn;
-    const int stride = (bytes + 1023) / 1024 * 1024;
-    const int loads = 64;
-    k_load<<<148, 32, 16 * 1024 + c.stages * stride>>>(m, loads, c.stages, c.w0, c.bw, c.bh, c.bn, bytes,
-                                                         stride, out);
-    k_load<<<148, 32, 16 * 1024 + c.stages * stride>>>(m, loads, c.stages, c.w0, c.bw, c.bh, c.bn, bytes,
-                                                         stride, out);
-    long long h = 0;
-    cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
-    printf("%-24s stages %d: %5u B/box, %7.1f cycles/box, %.2f rows/cycle/SM  (%s)\n", c.name, c.stages, bytes,
-           double(h) / loads, (bytes / 64.0) / (double(h) / loads), cudaGetErrorString(cudaGetLastError()));
+  for (int nmax : {64, 8}) {  // 8 images: the working set stays in L2
+   for (int stages : {2, 4, 8})
+    for (int grid : {1, 148})
+      for (const Case& c : cases) {
+        // [16c][W][H][img][Cb] over NCHW16c = [img][Cb][H][W][16]
+        cuuint64_t dims[5] = {16, W, H, N, Cb};
+        cuuint64_t strides[4] = {64, uint64_t(W) * 64, uint64_t(Cb) * H * W * 64, uint64_t(H) * W * 64};
+        cuuint32_t box[5] = {16, cuuint32_t(c.bw), cuuint32_t(c.bh), cuuint32_t(c.bn), 1};
+        cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        CUtensorMap m;
+        CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, x, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+          printf("%s: encode failed %d\n", c.name, int(r));
+          continue;
+        }
+        const uint32_t bytes = 64u * c.bw * c.bh * c.bn;
+        const int stride = (bytes + 1023) / 1024 * 1024;
+        const int loads = 64;
+        for (int rep = 0; rep < 2; ++rep)
+          k_load<<<grid, 32, 16 * 1024 + stages * stride>>>(m, loads, stages, c.w0, c.bw, c.bh, c.bn, bytes, stride,
+                                                            nmax, out);
+        long long h = 0;
+        cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+        printf("stages %2d imgs %3d grid %3d %-20s: %5u B/box, %7.1f cycles/box, %.2f rows/cycle/SM  (%s)\n", stages, nmax, grid,
+               c.name, bytes, double(h) / loads, (bytes / 64.0) / (double(h) / loads),
+               cudaGetErrorString(cudaGetLastError()));
+      }
   }
   return 0;
 }
