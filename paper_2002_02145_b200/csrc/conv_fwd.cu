@@ -395,18 +395,18 @@ int grid_for(int64_t n) {
 }
 
 // ---------------------------------------------------------------- launch
-template <int BN, bool SPLIT3, int CS, int EPI>
+template <int BN, bool SPLIT3, int CS, int EPI, int EG>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
-  if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2)) {
-    throw RuntimeError("unsupported (bn, cluster, mode) combination");
+  if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2) || (EG == 2 && BN < 64)) {
+    throw RuntimeError("unsupported (bn, cluster, mode, epilogue groups) combination");
   } else {
     constexpr bool PAIR = CS == 2;
-    using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+    using Cfg = KernelCfg<BN, SPLIT3, PAIR, EG>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI>,
+      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     CUDA_OK(attr_err);
@@ -436,21 +436,32 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, EPI>, prm, a, b, blo, o));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG>, prm, a, b, blo, o));
   }
 }
 
+template <bool SPLIT3, int CS, int EPI, int EG>
+void dispatch_bn_eg(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
+                    const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
+  switch (bn) {
+    case 16: return launch_conv<16, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    case 32: return launch_conv<32, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    case 64: return launch_conv<64, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    case 128: return launch_conv<128, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    case 256: return launch_conv<256, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    default: throw RuntimeError("unsupported bn");
+  }
+}
+
+// two epilogue groups (recipe eg:2) for bn >= 64; the fused (bias/ReLU)
+// epilogue always runs one group (fewer instantiations)
 template <bool SPLIT3, int CS, int EPI>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
-  switch (bn) {
-    case 16: return launch_conv<16, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
-    case 32: return launch_conv<32, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
-    case 64: return launch_conv<64, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
-    case 128: return launch_conv<128, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
-    case 256: return launch_conv<256, SPLIT3, CS, EPI>(P, prm, a, b, blo, o, st);
-    default: throw RuntimeError("unsupported bn");
+  if constexpr (EPI != kEpiFused) {
+    if (prm.egroups == 2 && bn >= 64) return dispatch_bn_eg<SPLIT3, CS, EPI, 2>(bn, P, prm, a, b, blo, o, st);
   }
+  return dispatch_bn_eg<SPLIT3, CS, EPI, 1>(bn, P, prm, a, b, blo, o, st);
 }
 
 template <bool SPLIT3>
@@ -606,6 +617,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.b_off = s.kps * 8192 * (s.tmem_a ? 1 : mult);
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
     prm.tmem_a = s.tmem_a;
+    prm.egroups = s.egroups;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
       prm.a_slot_col = (3 * s.bn + 31) / 32 * 32;
       prm.a_slots = std::min(kMaxStages, (512 - prm.a_slot_col) / 32);

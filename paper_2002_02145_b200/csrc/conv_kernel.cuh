@@ -102,6 +102,7 @@ struct ConvParams {
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
+  int egroups;                    // host dispatch: epilogue warp groups (kernel template EG)
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -118,7 +119,8 @@ constexpr bool kTrace = true;
 #else
 constexpr bool kTrace = false;
 #endif
-constexpr int kHaloB = 8;  // halo mode: B-ring barriers follow 8 A-ring slots
+constexpr int kHaloB = 8;
+  // halo mode: B-ring barriers follow 8 A-ring slots
 
 // Shared-memory plan (per CTA, one CTA per SM): a ring of `stages` pipeline
 // stages inside kStageBudget, then two output staging blocks, then barriers.
@@ -133,7 +135,7 @@ constexpr int kOutStages = 4;             // staging blocks: two rounds of 32 ch
 constexpr int kStageBudget = 227 * 1024 - kOutStages * kOutStageBytes - 2048 - 1024;
 constexpr int kMaxStages = 16;
 
-template <int BN, bool SPLIT3, bool PAIR>
+template <int BN, bool SPLIT3, bool PAIR, int EG = 1>
 struct KernelCfg {
   static constexpr int kCS = PAIR ? 2 : 1;
   static constexpr int kBRows = BN / kCS;     // B rows staged per CTA
@@ -151,7 +153,11 @@ struct KernelCfg {
                                    : kColsNeeded <= 128 ? 128
                                    : kColsNeeded <= 256 ? 256
                                                         : 512;
-  static constexpr int kThreads = SPLIT3 ? 320 : 192;
+  // two epilogue warp groups (4 warps each, one per TMEM lane quadrant) drain
+  // alternate 32-column rounds: TF32 warps 2-5 and 6-9; 3xTF32 warps 2-5 and
+  // 10-13 (the splitter is 6-9)
+  static constexpr int kEpiGroups = EG;
+  static constexpr int kThreads = (SPLIT3 ? 320 : 192) + (kEpiGroups - 1) * 128;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
       kStageBudget + kOutStages * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
@@ -586,14 +592,15 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
 // per-block store loop cost 5-10% on epilogue-heavy layers, measured on l1 1x1
 // 64->64 / 64->256): kEpiStore (store, or reduce-add for `+=`), kEpiFused
 // (+ bias / ReLU), kEpiSplit (tail split-K units, flag-ordered partials)
-template <int BN, bool SPLIT3, bool PAIR, int EPI>
-__global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
+// EG: epilogue warp groups (1, or 2 draining alternate 32-channel rounds; recipe eg:)
+template <int BN, bool SPLIT3, bool PAIR, int EPI, int EG>
+__global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
                    const __grid_constant__ CUtensorMap tmap_flt_lo,
                    const __grid_constant__ CUtensorMap tmap_out) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
+  using Cfg = KernelCfg<BN, SPLIT3, PAIR, EG>;
   constexpr int CS = Cfg::kCS;
   const int kStages = p.stages;
   constexpr int kAccBufs = Cfg::kAccBufs;
@@ -637,7 +644,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     }
     for (int a = 0; a < kAccBufs; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
-      ptx::mbar_init(&acc_empty[a], 4 * CS);
+      ptx::mbar_init(&acc_empty[a], 4 * EG * CS);
     }
     for (int a = 0; a < (p.tmem_a ? p.a_slots : 0); ++a) ptx::mbar_init(&aslot_empty[a], 1);
     ptx::fence_mbar_init();
@@ -896,9 +903,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
   } else if (warp == 1) {
     // second CTA of a pair: its loads complete on the leader's barrier and the
     // leader issues the pair MMAs; nothing to do here.
-  } else if (warp < 6) {
+  } else if (warp < 6 || (EG == 2 && warp >= (SPLIT3 ? 10 : 6))) {
     // ------------------------------------------------------------ epilogue
     constexpr int DW = Cfg::kDrainW;
+    constexpr int kGroups = EG;
+    const int egrp = warp < 6 ? 0 : 1;  // rounds j = egrp, egrp + kGroups, ...
     // Output path: each 16-channel block of the 128-pixel tile is staged in
     // shared memory (SWIZZLE_64B image of the TMA box, conflict-free 16-B
     // writes) and written by one TMA tensor store (full lines; pixels outside
@@ -906,7 +915,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
     const int lane = threadIdx.x & 31;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const bool store_thread = threadIdx.x == 64;  // first epilogue thread issues TMA stores
+    // first thread of each group issues its TMA stores (own bulk groups, own
+    // staging blocks, own named barrier)
+    const bool store_thread = threadIdx.x == (egrp == 0 ? 64 : (SPLIT3 ? 320 : 192));
+    const int ebar = 1 + egrp;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
     // staged row of this lane: the tile row itself, or (halo) its pixel
@@ -952,7 +964,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
 #pragma unroll 1
-        for (int j = 0; j < BN / DW; ++j) {
+        for (int j = egrp; j < BN / DW; j += kGroups) {
           uint32_t v[DW];
           if constexpr (DW == 32) ptx::tmem_ld32(tacc + j * 32, v);
           else ptx::tmem_ld16(tacc + j * 16, v);
@@ -991,10 +1003,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
             // barrier pair and one bulk group per round, kOutStages/(DW/16)
             // rounds in flight
             constexpr int kBlk = DW / 16;
-            constexpr int kRounds = kOutStages / kBlk;
-            uint8_t* st = out_stage + ostage * (kBlk * Cfg::kOutStageBytes);
+            constexpr int kRounds = kOutStages / kGroups / kBlk;  // per group
+            uint8_t* st = out_stage + (egrp * kRounds + ostage) * (kBlk * Cfg::kOutStageBytes);
             if (store_thread) ptx::bulk_wait_read<kRounds - 1>();  // this round's buffers read out
-            ptx::named_bar(1, 128);
+            ptx::named_bar(ebar, 128);
             if (row_valid) {
 #pragma unroll
               for (int blk = 0; blk < kBlk; ++blk) {
@@ -1008,7 +1020,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
               }
             }
             ptx::fence_proxy_async_smem();
-            ptx::named_bar(1, 128);
+            ptx::named_bar(ebar, 128);
             if (EPI == kEpiSplit && store_thread && wait_flag) {
               const uint64_t t0 = ptx::globaltimer();
               while (ptx::ld_acquire_gpu(flag) != p.epoch)
@@ -1041,16 +1053,19 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR>::kThreads, 1)
         }
         __syncwarp();
       }
-      if (EPI == kEpiSplit && store_thread && flagged && un.sp == 0) {  // the tile's first partial is in memory
-        ptx::bulk_wait_all();
-        ptx::fence_proxy_async_global();
-        ptx::st_release_gpu(flag, p.epoch);
+      if (EPI == kEpiSplit && flagged && un.sp == 0) {  // the tile's first partial is in memory
+        if (store_thread) {
+          ptx::bulk_wait_all();
+          ptx::fence_proxy_async_global();
+        }
+        if (kGroups > 1) ptx::named_bar(3, 128 * kGroups);  // both groups' stores landed
+        if (threadIdx.x == 64) ptx::st_release_gpu(flag, p.epoch);
       }
     }
     if (ev && store_thread) ev[5] = clock64();  // last store issued
     if (store_thread) ptx::bulk_wait_all();  // stores complete before smem is released
     if (ev && store_thread) ev[6] = clock64();
-  } else if (SPLIT3) {
+  } else if (SPLIT3 && warp < 10) {
     // ------------------------------------------------------------ splitter
     // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
     const int tid = threadIdx.x - 192;

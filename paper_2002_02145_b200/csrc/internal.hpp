@@ -61,6 +61,7 @@ struct Recipe {
   int kt = 0;                                                 // split-K scope: 0 tail wave, 1 all tiles
   int br = -1;                                                // halo: resident filter, -1 auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
+  int eg = 0;                                                 // epilogue warp groups, 0 = auto (1)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
   static Recipe parse(const std::string& text);  // throws ConfigError
@@ -87,6 +88,7 @@ struct Schedule {
   int ksplit = 1;      // split-K: reduction split into ksplit work units per tile
   int split_all = 0;   // split every tile (zeroed output, all partials reduce-added)
                        // instead of only the last partial wave's (flag-ordered)
+  int egroups = 1;     // epilogue warp groups draining alternate 32-channel rounds (1 or 2)
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;

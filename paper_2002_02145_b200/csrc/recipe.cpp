@@ -123,6 +123,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "halo") {
           r.halo = static_cast<int>(parse_int(val, "gpu halo"));
           if (r.halo != 0 && r.halo != 1) throw ConfigError("gpu halo must be 0 or 1");
+        } else if (key == "eg") {
+          r.eg = static_cast<int>(parse_int(val, "gpu epilogue groups"));
+          if (r.eg != 1 && r.eg != 2) throw ConfigError("gpu eg must be 1 or 2");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -158,6 +161,7 @@ std::string Recipe::id() const {
     if (kt) s += ",kt:" + std::to_string(kt);
     if (br >= 0) s += ",br:" + std::to_string(br);
     if (kg) s += ",kg:" + std::to_string(kg);
+    if (eg) s += ",eg:" + std::to_string(eg);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
   return s;
@@ -339,6 +343,9 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
     const int nch = (ksteps + cmax - 1) / cmax;
     chunk_def = (ksteps + nch - 1) / nch;
   }
+  // (TF32 accumulates the whole reduction in one TMEM buffer: the chunk running
+  // sum needs the 3xTF32 TMEM layout, so ch: is a 3xTF32-only key)
+  if (r.chunk && mode != PSCONV_MODE_3XTF32) throw ConfigError("gpu ch (accumulation chunk) is a 3xtf32 option");
   s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
@@ -392,8 +399,10 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
     canon.gm = r.gm >= 0 ? r.gm : -1;
   }
   s.chunk = (s.chunk + s.kps - 1) / s.kps * s.kps;  // chunks hold whole stages
-  canon.chunk = (mode == PSCONV_MODE_3XTF32 || r.chunk) ? s.chunk : 0;
+  canon.chunk = mode == PSCONV_MODE_3XTF32 ? s.chunk : 0;
   canon.kg = r.kg ? s.kps : 0;
+  s.egroups = r.eg ? r.eg : 1;
+  canon.eg = s.egroups == 2 ? 2 : 0;
   s.recipe_id = canon.id();
   return s;
 }

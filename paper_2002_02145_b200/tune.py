@@ -29,6 +29,10 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     if mode == "tf32":
         alts.append({**kv, "cl": "1" if kv.get("cl") == "2" else "2"})
     bn = int(kv["bn"])
+    # two epilogue warp groups (alternate 32-channel rounds): faster on some
+    # epilogue-heavy layers, slower on others
+    if int(kv["bn"]) >= 64:
+        alts.append({**kv, "eg": "2"})
     if mode == "3xtf32" and bn == 128:  # TMEM-resident A is opt-in at bn 128
         alts.append({**kv, "ta": "1"})
     widest = max(c for c in (16, 32, 64, 128, 256) if preset.nOfm % c == 0)

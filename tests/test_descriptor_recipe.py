@@ -114,3 +114,17 @@ def test_split_k_recipe_keys():
     for bad in (",kt:2", ",ks:0", ",ks:17"):
         with pytest.raises(ConfigRejectedError):
             ps.model_us(p, base + bad, "3xtf32")
+
+
+def test_epilogue_groups_recipe_key():
+    """eg:2 (two epilogue warp groups) round-trips through the canonical recipe id;
+    eg:1 is the default and is not shown; other values are rejected."""
+    p = ConvPreset.parse("conv:8,128,64,8,8,3,3,1,1,16,1,1,8,8")
+    top = ps.select_topk(p, "tf32", 1)[0][0]
+    assert "eg:" not in top
+    for bad in ("gpu=bn:64,eg:0", "gpu=bn:64,eg:3"):
+        with pytest.raises(ConfigRejectedError):
+            ps.model_us(p, bad, "tf32")
+    assert ps.model_us(p, "gpu=bn:128,eg:2", "tf32") > 0
+    with pytest.raises(ConfigRejectedError):  # accumulation chunks are 3xTF32-only
+        ps.model_us(p, "gpu=bn:64,ch:4", "tf32")

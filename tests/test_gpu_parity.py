@@ -440,3 +440,38 @@ def test_split_k_accumulate():
                                accumulate=True, out_init=base)
     ref = base + oracle.conv(p, oracle.fill_input(p, sx, 256), oracle.fill_filter(p, sw, 256)).ravel()
     assert oracle.rel_l2(yg, ref) <= 1e-5, rec
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,eg:2"),
+    ("conv:2,256,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:256,box:2x4x16,eg:2,ch:8"),
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:256,box:7x1x18,ks:2,eg:2"),
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:128,box:1x7x18,ks:3,kt:1,eg:2"),
+    ("conv:300,128,32,8,16,1,1,1,1,16,0,0,8,16", 32, "gpu=bn:128,box:16x8x1,eg:2"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,halo:1,eg:2"),
+])
+def test_two_epilogue_groups(conv, c_log, recipe, mode):
+    """Recipe eg:2: two epilogue warp groups drain alternate 32-channel rounds (own staging
+    blocks, bulk groups, named barriers); split-K flag release waits for both groups."""
+    if mode == "tf32":
+        recipe = recipe.replace(",ch:8", "")
+        if "bn:128" in recipe and "ks" not in recipe:
+            recipe += ",cl:2"
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("eg2", conv, c_log, 16, mode, n, recipe)
+
+
+@pytest.mark.gpu
+def test_two_epilogue_groups_accumulate():
+    p = ps.ConvPreset.parse("conv:4,128,64,12,12,3,3,1,1,16,1,1,12,12")
+    sx, sw = seeds(17)
+    init = np.random.default_rng(5).uniform(-1, 1, p.output_elems()).astype(np.float32)
+    x = oracle.fill_input(p, sx, 64)
+    w = oracle.fill_filter(p, sw, 64)
+    ref = oracle.conv(p, x, w).ravel() + init
+    _, _, yg, rec = _run_gpu(p, 64, sx, sw, "3xtf32", recipe="gpu=bn:128,eg:2", accumulate=True,
+                             out_init=init)
+    assert "eg:2" in rec
+    assert oracle.rel_l2(yg, ref) <= TOL["3xtf32"]
