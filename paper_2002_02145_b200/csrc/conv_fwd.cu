@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "conv_kernel.cuh"
+#include "conv_pp.cuh"
 #include "internal.hpp"
 #include "seeded.hpp"
 
@@ -34,6 +35,10 @@ struct conv_plan {
   // are packed into one block, so the kernel runs the descriptor kd (kw' =
   // ceil(kw / G), no w padding, tap dilation G) over the folded copy xfold.
   int fold = 0, fold_g = 1, fold_phases = 1;
+  // few-channel kernel (recipe pp:C, conv_pp.cuh): C <= 4 real channels, tap
+  // pairs over input parity planes; the filter is packed per tap-pair MMA
+  int pp = 0;
+  psconv::PpGeom ppg{};
   conv_desc kd{};                 // kernel descriptor (== d unless folded)
   float* xfold = nullptr;         // [nImg][phases][H][Wq][16]
   float* wfold = nullptr;         // folded filter, KCRS16c16k of kd
@@ -264,7 +269,53 @@ int grid_for(int64_t n);
 
 void launch_bwd_filter(const conv_plan* P, const float* flt, cudaStream_t st);
 
+// Filter pack of the few-channel kernel (conv_pp.cuh): per tap-pair MMA i and
+// N tile, a [kh][bn/8][8 rows][4 channels] block (SWIZZLE_NONE K-major core
+// matrices): kh 0 = tap_a's channels 0..3, kh 1 = tap_b's (zero for the
+// partner of an odd tap, and for channels >= C).
+struct PpTaps {
+  int tap_a[psconv::kPpMaxMma], tap_b[psconv::kPpMaxMma];
+};
+__global__ void pp_pack_filter_kernel(const float* __restrict__ flt, float* __restrict__ hi,
+                                      float* __restrict__ lo, int64_t n_elems, int bn, int nmma, int RS,
+                                      int C, const __grid_constant__ PpTaps taps) {
+  ptx::griddep_launch_dependents();
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int c4 = int(e & 3), nr = int((e >> 2) & 7);
+    const int64_t rest = e >> 5;
+    const int ng = int(rest % (bn / 8)), kh = int((rest / (bn / 8)) & 1);
+    const int64_t blk = rest / (bn / 4);  // tk * nmma + i
+    const int i = int(blk % nmma), tk = int(blk / nmma);
+    const int tap = kh == 0 ? taps.tap_a[i] : taps.tap_b[i];
+    const int64_t n = int64_t(tk) * bn + ng * 8 + nr;
+    float x = 0.f;
+    if (tap >= 0 && c4 < C) x = flt[((n / 16) * RS + tap) * 256 + c4 * 16 + (n & 15)];
+    if (lo) {
+      const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      hi[e] = h;
+      lo[e] = x - h;
+    } else {
+      hi[e] = x;
+    }
+  }
+}
+
 void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
+  if (P->pp) {
+    const psconv::PpGeom& g = P->ppg;
+    PpTaps t{};
+    for (int i = 0; i < g.nmma; ++i) {
+      t.tap_a[i] = g.tap_a[i];
+      t.tap_b[i] = g.tap_b[i];
+    }
+    const int64_t n = int64_t(g.b_bytes) / 4;
+    const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+    pp_pack_filter_kernel<<<int((n + 255) / 256), 256, 0, st>>>(
+        flt, P->flt_pack, split3 ? P->flt_pack + n : nullptr, n, g.bn, g.nmma, int(P->d.kh * P->d.kw), P->pp, t);
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   if (P->bwd_data) {
     launch_bwd_filter(P, flt, st);
     flt = P->wtrans;
@@ -482,9 +533,99 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
 
 // Launches the plan on images [0, img_count) of `in` / `out` (already offset to
 // the first image). Validation is the caller's (conv_fwd / conv_fwd_host).
+template <int BN, bool SPLIT3>
+void launch_pp_kernel(const conv_plan* P, const PpParams& prm, const CUtensorMap& ta, const CUtensorMap& tout,
+                      int smem, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(conv_pp_sm100<BN, SPLIT3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024);
+  });
+  CUDA_OK(attr_err);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(prm.groups, P->num_sms));
+  cfg.blockDim = dim3(PpCfg<BN, SPLIT3>::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = std::getenv("PSCONV_NO_PDL") ? 0 : 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, conv_pp_sm100<BN, SPLIT3>, prm, ta, tout));
+}
+
+// few-channel kernel (recipe pp:C): input parity planes read at 16 B per pixel
+void launch_pp(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
+               cudaStream_t st, unsigned flags) {
+  const conv_desc& d = P->d;
+  const PpGeom& g = P->ppg;
+  if (!(flags & PSCONV_FLAG_PREPACKED)) {
+    launch_prepack(P, flt, st);
+    P->prepacked = false;
+  }
+  const int Kb = int(d.nOfm / 16), H = int(d.ifh), W = int(d.ifw), Pp = int(d.ofh), Q = int(d.ofw);
+  CUtensorMap ta, tout;
+  {
+    const cuuint64_t dims[5] = {16, cuuint64_t(Q), cuuint64_t(Pp), cuuint64_t(Kb), cuuint64_t(img_count)};
+    const cuuint64_t strides[4] = {64, cuuint64_t(Q) * 64, cuuint64_t(Pp) * Q * 64, cuuint64_t(Kb) * Pp * Q * 64};
+    const cuuint32_t box[5] = {16, 8, 16, 1, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    encode(&tout, out, 5, dims, strides, box, estr);
+  }
+  {
+    // channels 0..3 of each pixel (16 B), parity planes via element strides
+    const cuuint64_t dims[5] = {16, cuuint64_t(W), cuuint64_t(H), cuuint64_t(img_count), 1};
+    const cuuint64_t strides[4] = {64, cuuint64_t(W) * 64, cuuint64_t(H) * W * 64, cuuint64_t(H) * W * 64};
+    const cuuint32_t box[5] = {4, cuuint32_t(g.PC * g.s), cuuint32_t(g.PR * g.s), 1, 1};
+    const cuuint32_t estr[5] = {1, cuuint32_t(g.s), cuuint32_t(g.s), 1, 1};
+    encode(&ta, in, 5, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  PpParams prm{};
+  prm.img_count = int(img_count);
+  prm.P = Pp;
+  prm.Q = Q;
+  prm.s = g.s;
+  prm.ph = int(d.pad_h);
+  prm.pw = int(d.pad_w);
+  prm.tiles_q = (Q + 7) / 8;
+  prm.tiles_p = (Pp + 15) / 16;
+  prm.tiles_k = g.tiles_k;
+  const int64_t groups = int64_t(prm.tiles_q) * prm.tiles_p * img_count * g.tiles_k;
+  if (groups >= (int64_t(1) << 31)) throw ConfigError("too many tiles");
+  prm.groups = int(groups);
+  prm.nmma = g.nmma;
+  prm.planes = g.planes;
+  prm.plane_bytes = g.plane_bytes;
+  prm.pitch = g.pitch;
+  prm.box_bytes = g.box_bytes;
+  prm.stage_bytes = g.stage_bytes;
+  prm.lo_off = g.lo_off;
+  prm.stages = g.stages;
+  prm.b_bytes = g.b_bytes;
+  for (int i = 0; i < g.nmma; ++i) {
+    prm.a_off[i] = g.a_off[i];
+    prm.a_lbo[i] = g.a_lbo[i];
+  }
+  prm.bpack = P->flt_pack;
+  prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
+  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+  if (g.bn == 64)
+    split3 ? launch_pp_kernel<64, true>(P, prm, ta, tout, g.smem_bytes, st)
+           : launch_pp_kernel<64, false>(P, prm, ta, tout, g.smem_bytes, st);
+  else
+    split3 ? launch_pp_kernel<128, true>(P, prm, ta, tout, g.smem_bytes, st)
+           : launch_pp_kernel<128, false>(P, prm, ta, tout, g.smem_bytes, st);
+}
+
 void launch_range(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
                   cudaStream_t st, unsigned flags, const float* bias = nullptr) {
   const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
+  if (P->pp) {
+    if (bias || (flags & PSCONV_FLAG_RELU)) throw ConfigError("gpu pp kernel: no fused bias/ReLU epilogue");
+    return launch_pp(P, in, flt, out, img_count, st, flags);
+  }
   const conv_desc& d = P->kd;  // the kernel's descriptor (folded for fold:C plans)
   if (P->fold) {  // planes [img][phase][H][Wq][16], Wq = kd.ifw
     const int64_t n_px = img_count * P->fold_phases * d.ifh * d.ifw;
@@ -750,7 +891,7 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     int fold = 0, fold_g = 1, fold_phases = 1;
     if (recipe && *recipe) {
       r = Recipe::parse(recipe);
-      if (r.fold) {
+      if (r.fold && !r.pp) {
         // (c,s) fold: one 16-channel block holding C real channels, G taps per block
         fold = r.fold;
         fold_g = 16 / fold;
@@ -796,6 +937,10 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     P->fold = fold;
     P->fold_g = fold_g;
     P->fold_phases = fold_phases;
+    if (s.pp) {
+      P->pp = s.pp;
+      P->ppg = pp_geom(d, s.bn, mode);
+    }
     // 128-B filter rows pair channel blocks inside a stage: needs even kps dividing Cb
     P->b128 = s.kps % 2 == 0 && (d.nIfm / 16) % s.kps == 0 && std::getenv("PSCONV_NO_B128") == nullptr;
     P->flt_elems = kd.nOfm * kd.nIfm * kd.kh * kd.kw;

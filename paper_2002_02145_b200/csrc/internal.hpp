@@ -62,6 +62,7 @@ struct Recipe {
   int br = -1;                                                // halo: resident filter, -1 auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int eg = 0;                                                 // epilogue warp groups, 0 = auto (1)
+  int pp = 0;                                                 // parity-plane tap pairs: C real channels (<= 4)
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
   static Recipe parse(const std::string& text);  // throws ConfigError
@@ -89,6 +90,7 @@ struct Schedule {
   int split_all = 0;   // split every tile (zeroed output, all partials reduce-added)
                        // instead of only the last partial wave's (flag-ordered)
   int egroups = 1;     // epilogue warp groups draining alternate 32-channel rounds (1 or 2)
+  int pp = 0;          // few-channel kernel (conv_pp.cuh): C <= 4 real channels, tap pairs per MMA
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;
@@ -113,6 +115,17 @@ struct HaloGeom {
 bool halo_eligible(const conv_desc& d);
 void nest_recognise(const std::string& text, nest_info* out);  // nest.cpp, throws ConfigError
 HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode);
+
+// Parity-plane tap-pair geometry (conv_pp.cuh, recipe pp:C): s*s input parity
+// planes of PR x PC 16-B pixels per 8 x 16 output tile; taps sorted by operand
+// address and paired per K=8 MMA (tap_b = -1: zero second half).
+constexpr int kPpMaxMmaHost = 32;
+struct PpGeom {
+  int s, PR, PC, planes, plane_bytes, pitch, box_bytes, stage_bytes, lo_off, stages;
+  int bn, nmma, tiles_k, b_bytes, smem_bytes;
+  int a_off[kPpMaxMmaHost], a_lbo[kPpMaxMmaHost], tap_a[kPpMaxMmaHost], tap_b[kPpMaxMmaHost];
+};
+PpGeom pp_geom(const conv_desc& d, int bn, int mode);  // throws ConfigError
 
 // Closed-form model (select.cpp).
 struct ModelBreakdown {

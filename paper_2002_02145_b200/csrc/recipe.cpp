@@ -123,6 +123,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "halo") {
           r.halo = static_cast<int>(parse_int(val, "gpu halo"));
           if (r.halo != 0 && r.halo != 1) throw ConfigError("gpu halo must be 0 or 1");
+        } else if (key == "pp") {
+          r.pp = static_cast<int>(parse_int(val, "gpu parity-plane channels"));
+          if (r.pp < 1 || r.pp > 4) throw ConfigError("gpu pp must be in [1, 4] (real input channels)");
         } else if (key == "eg") {
           r.eg = static_cast<int>(parse_int(val, "gpu epilogue groups"));
           if (r.eg != 1 && r.eg != 2) throw ConfigError("gpu eg must be 1 or 2");
@@ -162,6 +165,7 @@ std::string Recipe::id() const {
     if (br >= 0) s += ",br:" + std::to_string(br);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (eg) s += ",eg:" + std::to_string(eg);
+    if (pp) s += ",pp:" + std::to_string(pp);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
   return s;
@@ -266,6 +270,36 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   }
   // --- tile axes
   const int64_t K = d.nOfm;
+  if (r.pp) {
+    // few-channel kernel (conv_pp.cuh): fixed 8 x 16 pixel tile, bn 64 or 128,
+    // the whole reduction in one MMA chain of tap pairs
+    if (r.fold) throw ConfigError("gpu pp and fold are exclusive");
+    const int pbn = r.bn ? r.bn : (K % 128 == 0 ? 128 : 64);
+    const PpGeom g = pp_geom(d, pbn, mode);  // validates
+    s.pp = r.pp;
+    s.bn = g.bn;
+    s.qb = 8;
+    s.pb = 16;
+    s.nb = 1;
+    s.cs = 1;
+    s.kps = 1;
+    s.stages = g.stages;
+    s.chunk = 0;
+    s.ksplit = 1;
+    s.egroups = 1;
+    Recipe canon;
+    for (int i = 0; i < L_COUNT; ++i)
+      if (order[i] != L_IMG || i != 0) canon.perm.push_back(loop_name(order[i]));
+    for (const auto& t : r.tiles) canon.tiles.push_back(t);
+    canon.has_gpu = true;
+    canon.bn = s.bn;
+    canon.box_q = 8;
+    canon.box_p = 16;
+    canon.box_n = 1;
+    canon.pp = r.pp;
+    s.recipe_id = canon.id();
+    return s;
+  }
   int bn = r.bn;
   if (tile_of.count("ofm_tile") && !bn) bn = static_cast<int>(16 * tile_of["ofm_tile"]);
   if (!bn) {
@@ -523,6 +557,69 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   }
   s.kps = kps;
   s.stages = ring(kps);
+}
+
+}  // namespace psconv
+
+namespace psconv {
+
+PpGeom pp_geom(const conv_desc& d, int bn, int mode) {
+  PpGeom g{};
+  if (d.nIfm != 16 || d.gemm_block != 16) throw ConfigError("gpu pp needs nIfm = gemm_block = 16");
+  if (d.stride_h != d.stride_w || d.stride_h < 1 || d.stride_h > 2)
+    throw ConfigError("gpu pp needs equal strides of 1 or 2");
+  if (bn != 64 && bn != 128) throw ConfigError("gpu pp needs bn 64 or 128");
+  if (d.nOfm % bn) throw ConfigError("gpu pp: nOfm is not a multiple of bn");
+  const int R = static_cast<int>(d.kh), S = static_cast<int>(d.kw), s = static_cast<int>(d.stride_h);
+  if (R * S > 2 * kPpMaxMmaHost || R * S < 2) throw ConfigError("gpu pp needs 2..64 filter taps");
+  g.s = s;
+  g.bn = bn;
+  g.PR = 16 + (R - 1) / s;
+  g.PC = 8 + (S - 1) / s;
+  g.planes = s * s;
+  g.pitch = g.PC * 16;
+  g.box_bytes = g.PR * g.PC * 16;
+  g.plane_bytes = (g.box_bytes + 127) / 128 * 128;
+  const bool split3 = mode == PSCONV_MODE_3XTF32;
+  g.lo_off = g.planes * g.plane_bytes;
+  g.stage_bytes = g.lo_off * (split3 ? 2 : 1);
+  // taps sorted by operand address; pairs (t0, t1), (t2, t3), ... -- with an odd
+  // count the lowest tap gets a zero-weight partner (the next tap, so every read
+  // stays inside the loaded planes) and is paired again below
+  std::vector<std::pair<int, int>> taps;  // (offset, tap index r*S + s)
+  for (int r = 0; r < R; ++r)
+    for (int c = 0; c < S; ++c) {
+      const int pl = (r % s) * s + (c % s);
+      taps.emplace_back(pl * g.plane_bytes + (r / s) * g.pitch + (c / s) * 16, r * S + c);
+    }
+  std::sort(taps.begin(), taps.end());
+  const int nt = static_cast<int>(taps.size());
+  int i = 0, k = 0;
+  if (nt % 2 == 1) {
+    g.a_off[k] = taps[0].first;
+    g.a_lbo[k] = nt > 1 ? taps[1].first - taps[0].first : 16;
+    g.tap_a[k] = taps[0].second;
+    g.tap_b[k] = -1;
+    ++k;
+    i = 1;
+  }
+  for (; i + 1 < nt; i += 2, ++k) {
+    g.a_off[k] = taps[i].first;
+    g.a_lbo[k] = taps[i + 1].first - taps[i].first;
+    g.tap_a[k] = taps[i].second;
+    g.tap_b[k] = taps[i + 1].second;
+  }
+  g.nmma = k;
+  g.tiles_k = static_cast<int>(d.nOfm / bn);
+  g.b_bytes = g.tiles_k * g.nmma * bn * 32;
+  const int bres = (g.b_bytes * (split3 ? 2 : 1) + 1023) / 1024 * 1024;
+  const int fixed = bres + 4 * 128 * 64 + 1024 + 1024;
+  const int avail = 227 * 1024 - fixed;
+  g.stages = std::min(16, avail / g.stage_bytes);
+  if (g.stages < 2)
+    throw ConfigError("gpu pp: the resident filter leaves fewer than two plane stages in shared memory");
+  g.smem_bytes = (g.stages * g.stage_bytes + 1023) / 1024 * 1024 + fixed;
+  return g;
 }
 
 }  // namespace psconv

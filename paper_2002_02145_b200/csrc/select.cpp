@@ -100,6 +100,24 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   ModelBreakdown b{};
   b.m_tiles = mt;
   b.tiles = tiles;
+  if (s.pp) {
+    // few-channel kernel (conv_pp.cuh): nmma tap-pair MMAs per tile (N=64: ~48
+    // cycles each, N=128: 64), the planes' 16-B pixels read once (32-B sectors),
+    // the filter resident; output written once
+    const PpGeom pg = pp_geom(d, s.bn, mode);
+    const double mma_cyc = pg.nmma * (s.bn == 64 ? 48.0 : 64.0) * mult;
+    b.us_mma = per_sm * mma_cyc / (m.clock_ghz * 1e3);
+    b.us_tensor = b.us_mma;
+    b.hbm_bytes = 32.0 * g.N * g.H * g.W + 4.0 * g.N * g.K * g.P * g.Q;
+    b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;
+    b.us_rows = per_sm * pg.planes * pg.PR * pg.PC / m.row_requests_per_cycle / (m.clock_ghz * 1e3);
+    b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;
+    const double hi = std::max({b.us_tensor, b.us_hbm, b.us_rows});
+    const double lo = std::max(std::min(b.us_tensor, b.us_hbm), 1e-9);
+    b.us_total = hi * std::pow(1.0 + std::pow(lo / hi, 4.0), 0.25) + m.launch_us + b.us_epi;
+    b.flops_issued = 2.0 * tiles * 128.0 * s.bn * 8.0 * pg.nmma * mult;
+    return b;
+  }
   const double tile_flops = 2.0 * 128 * s.bn * 16.0 * ksteps * mult;
   b.flops_issued = tile_flops * tiles;
 

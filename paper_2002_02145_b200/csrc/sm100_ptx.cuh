@@ -109,6 +109,14 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* m, uin
       "r"(c4)
       : "memory");
 }
+// Plain bulk copy global -> shared (contiguous bytes, multiple of 16), mbarrier completion.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // Same loads, completing on an mbarrier given as a shared::cluster address in
 // either CTA of the pair (the leader's barrier, from mapa): .cta_group::2.
 __device__ __forceinline__ void tma_load_3d_cb(void* dst, const CUtensorMap* m, uint32_t bar_cl,
@@ -386,6 +394,16 @@ __device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr, uint32_t lbo,
          (static_cast<uint64_t>(lbo >> 4) << 16) | (static_cast<uint64_t>(sbo >> 4) << 32) |
          (1ull << 46) |  // descriptor version (sm_100)
          (4ull << 61);   // layout type: SWIZZLE_64B
+}
+
+// K-major, no swizzle (canonical ((8,m),(T,2)):((1T,SBO),(1,LBO)) in 16-B units):
+// 8-row core matrices of 16-B rows; LBO = byte distance between the two K halves
+// (16 B of K each) of a K=8 tf32 MMA, SBO = byte distance between 8-row groups
+__device__ __forceinline__ uint64_t smem_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) |
+         (1ull << 46);  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
 }
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {

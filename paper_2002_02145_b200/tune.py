@@ -58,6 +58,13 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
             kv2.pop("box", None)  # the folded layer has its own box candidates
             kv2.pop("ch", None)
             alts.append({**kv2, "fold": str(c_logical)})
+    # few-channel kernel (conv_pp.cuh) when at most 4 input channels are real: tap pairs
+    # straight from the input's parity planes, no folded copy
+    if (0 < c_logical <= 4 and preset.nIfm == 16 and preset.stride_h == preset.stride_w <= 2
+            and 2 <= preset.kh * preset.kw <= 64):
+        for pbn in (64, 128):
+            if preset.nOfm % pbn == 0:
+                alts.append({"bn": str(pbn), "pp": str(c_logical)})
     for a in alts:
         rid = head + ";gpu=" + ",".join(f"{key}:{val}" for key, val in a.items())
         if rid not in out:

@@ -128,3 +128,21 @@ def test_epilogue_groups_recipe_key():
     assert ps.model_us(p, "gpu=bn:128,eg:2", "tf32") > 0
     with pytest.raises(ConfigRejectedError):  # accumulation chunks are 3xTF32-only
         ps.model_us(p, "gpu=bn:64,ch:4", "tf32")
+
+
+def test_parity_plane_recipe_key():
+    """pp:C (few-channel kernel): accepted for C <= 4 real channels of one 16-channel block,
+    stride 1 or 2, 2..64 taps; canonical id pins the 8x16 pixel tile; modelled far below the
+    16-channel kernel on the stem."""
+    stem = ConvPreset.parse("conv:256,64,16,112,112,7,7,2,2,16,3,3,224,224")
+    pp = ps.model_us(stem, "gpu=pp:3", "tf32")
+    assert 0 < pp < ps.model_us(stem, "gpu=bn:64", "tf32") / 3
+    top = ps.select_topk(stem, "tf32", 1)[0][0]
+    assert "pp:" not in top  # opt-in: the selector cannot know the real channel count
+    bad = [("gpu=pp:5", stem), ("gpu=pp:3,fold:3", stem), ("gpu=bn:256,pp:3", stem),
+           ("gpu=pp:3", ConvPreset.parse("conv:2,64,32,8,8,3,3,1,1,16,1,1,8,8")),   # nIfm 32
+           ("gpu=pp:3", ConvPreset.parse("conv:2,64,16,8,8,1,1,1,1,16,0,0,8,8")),   # 1 tap
+           ("gpu=pp:3", ConvPreset.parse("conv:2,64,16,8,8,3,3,3,3,16,1,1,24,24"))]  # stride 3
+    for rid, p in bad:
+        with pytest.raises(ConfigRejectedError):
+            ps.model_us(p, rid, "tf32")

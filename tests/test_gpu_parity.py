@@ -475,3 +475,40 @@ def test_two_epilogue_groups_accumulate():
                              out_init=init)
     assert "eg:2" in rec
     assert oracle.rel_l2(yg, ref) <= TOL["3xtf32"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    # the ResNet-50 stem (7x7/s2/p3, C = 3 of 16): 4 parity planes, 25 tap-pair MMAs
+    ("conv:2,64,16,112,112,7,7,2,2,16,3,3,224,224", 3, "gpu=pp:3"),
+    # ragged tiles (P, Q not multiples of 16 / 8), 5x5/s2, bn 128 and two N tiles of 64
+    ("conv:3,128,16,13,11,5,5,2,2,16,2,2,25,21", 2, "gpu=bn:128,pp:2"),
+    ("conv:3,128,16,13,11,5,5,2,2,16,2,2,25,21", 2, "gpu=bn:64,pp:2"),
+    # stride 1 (one plane), even tap count (3x4... 4x3), C = 4
+    ("conv:2,64,16,20,19,4,3,1,1,16,1,1,21,19", 4, "gpu=pp:4"),
+    ("conv:2,64,16,18,18,3,3,1,1,16,1,1,18,18", 1, "gpu=pp:1"),
+])
+def test_parity_plane_tap_pairs(conv, c_log, recipe, mode):
+    """Few-channel kernel (recipe pp:C, conv_pp.cuh): tap pairs per K=8 MMA read straight
+    from TMA-loaded input parity planes; same result as the plain conv on inputs whose
+    channels >= C are zero."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("pp", conv, c_log, 18, mode, n, recipe)
+
+
+@pytest.mark.gpu
+def test_parity_plane_accumulate_and_range():
+    p = ps.ConvPreset.parse("conv:5,64,16,30,30,7,7,2,2,16,3,3,60,60")
+    sx, sw = seeds(19)
+    init = np.random.default_rng(7).uniform(-1, 1, p.output_elems()).astype(np.float32)
+    x = oracle.fill_input(p, sx, 3)
+    w = oracle.fill_filter(p, sw, 3)
+    full = oracle.conv(p, x, w).ravel()
+    per = full.size // p.nImg
+    ref = init.copy()
+    ref[per:4 * per] += full[per:4 * per]
+    _, _, yg, rec = _run_gpu(p, 3, sx, sw, "3xtf32", recipe="gpu=pp:3", img_begin=1, img_count=3,
+                             accumulate=True, out_init=init)
+    assert "pp:3" in rec
+    assert oracle.rel_l2(yg, ref) <= TOL["3xtf32"]

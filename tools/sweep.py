@@ -93,15 +93,40 @@ def main():
         for r in recs:
             fh.write(json.dumps(r) + "\n")
     if args.md:
-        with open(args.md, "w") as fh:
-            fh.write(f"# Per-layer sweep (1 B200, peaks: {src}; tf32 = bf16/2, 3xtf32 = tf32/3)\n\n")
-            fh.write("| layer | mode | GFLOP | bound | roofline ms | step ms | kernel ms | GFLOP/s (step) | frac (step) | frac (kernel) | recipe |\n")
-            fh.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
-            for r in recs:
-                fh.write(f"| {r['layer']} | {r['mode']} | {r['gflop']} | {r['bound']} | {r['roofline_ms']} | "
-                         f"{r['step_ms']} | {r['kernel_ms']} | {r['gflops_step']} | {r['frac_step']} | "
-                         f"{r['frac_kernel']} | `{r['recipe']}` |\n")
+        write_md(args.md, recs, src)
+
+
+def write_md(path, recs, src):
+    import math
+    with open(path, "w") as fh:
+        fh.write(f"# Per-layer sweep (1 B200, peaks: {src}; tf32 = bf16/2, 3xtf32 = tf32/3)\n\n")
+        fh.write("| layer | mode | GFLOP | bound | roofline ms | step ms | kernel ms | GFLOP/s (step) | frac (step) | frac (kernel) | recipe |\n")
+        fh.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
+        for r in recs:
+            fh.write(f"| {r['layer']} | {r['mode']} | {r['gflop']} | {r['bound']} | {r['roofline_ms']} | "
+                     f"{r['step_ms']} | {r['kernel_ms']} | {r['gflops_step']} | {r['frac_step']} | "
+                     f"{r['frac_kernel']} | `{r['recipe']}` |\n")
+        for mode in ("3xtf32", "tf32"):
+            fr = [r["frac_step"] for r in recs if r["mode"] == mode]
+            if fr:
+                g = math.exp(sum(map(math.log, fr)) / len(fr))
+                fh.write(f"\nGeomean roofline fraction (step), {mode}: {g:.3f} over {len(fr)} layers; "
+                         f"layers >= 0.6: {sum(f >= 0.6 for f in fr)}/{len(fr)}\n")
+
+
+def merge(main_path, part_path, md_path):
+    """Replace the (layer, mode) records of main_path with those of part_path; rewrite the md."""
+    recs = [json.loads(l) for l in open(main_path) if l.strip()]
+    new = {(r["layer"], r["mode"]): r for r in (json.loads(l) for l in open(part_path) if l.strip())}
+    recs = [new.pop((r["layer"], r["mode"]), r) for r in recs] + list(new.values())
+    with open(main_path, "w") as fh:
+        for r in recs:
+            fh.write(json.dumps(r) + "\n")
+    write_md(md_path, recs, bench.peaks()[2])
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) == 5 and sys.argv[1] == "--merge":  # sweep.py --merge main.jsonl part.jsonl main.md
+        merge(sys.argv[2], sys.argv[3], sys.argv[4])
+    else:
+        main()
