@@ -30,6 +30,7 @@ struct conv_plan {
   psconv::Schedule sched;
   float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
+  bool ncat = false;           // 3xTF32 N-concat: prepacked rows [B_hi;B_lo] per N tile (ConvParams::ncat)
   // (c,s)-folded input (recipe fold:C, SURVEY §8d stem note): the layer has C <= 8
   // real input channels in one 16-channel block; G = 16 / C consecutive kw taps
   // are packed into one block, so the kernel runs the descriptor kd (kw' =
@@ -122,9 +123,11 @@ void encode(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
 // 3xTF32: also split x -> hi = x with the 13 low mantissa bits cleared
 // (exactly representable in tf32) and lo = x - hi (exact in fp32).
 // One 256-thread block per 16x16 [c][k] block, transposed through smem.
+// ncat_bn > 0 (3xTF32 N-concat): hi and lo rows interleaved per N tile of ncat_bn
+// output channels in one [.. ][2K][..] layout: rows tile*2bn + k%bn (hi), + bn (lo).
 __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __restrict__ hi,
                                       float* __restrict__ lo, int K, int CRS, int RS, int split,
-                                      int b128) {
+                                      int b128, int ncat_bn) {
   __shared__ float tile[16][17];
   ptx::griddep_launch_dependents();  // the conv kernel may start its prologue now
   const int blk = blockIdx.x;  // = kb * CRS + crs, crs = cb * RS + rs
@@ -136,6 +139,16 @@ __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __re
   const float x = tile[c16][k16];
   const int cb = crs / RS, rs = crs % RS;
   const int64_t k = kb * 16 + k16;
+  if (ncat_bn > 0) {
+    const int64_t K2 = 2 * static_cast<int64_t>(K);
+    const int64_t kh = (k / ncat_bn) * 2 * ncat_bn + k % ncat_bn;
+    const int64_t row0 = b128 ? (static_cast<int64_t>(cb >> 1) * RS + rs) * K2 : (static_cast<int64_t>(cb) * RS + rs) * K2;
+    const int64_t w = b128 ? 32 : 16, c = b128 ? (cb & 1) * 16 + c16 : c16;
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    hi[(row0 + kh) * w + c] = h;
+    hi[(row0 + kh + ncat_bn) * w + c] = x - h;
+    return;
+  }
   const int64_t o = b128 ? ((static_cast<int64_t>(cb >> 1) * RS + rs) * K + k) * 32 + (cb & 1) * 16 + c16
                          : ((static_cast<int64_t>(cb) * RS + rs) * K + k) * 16 + c16;
   if (split) {
@@ -330,7 +343,8 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
   prepack_filter_kernel<<<Kb * CRS, 256, 0, st>>>(flt, P->flt_pack,
                                                   split3 ? P->flt_pack + P->flt_elems : nullptr,
                                                   int(kd.nOfm), CRS, int(kd.kh * kd.kw),
-                                                  split3 ? 1 : 0, P->b128 ? 1 : 0);
+                                                  split3 ? 1 : 0, P->b128 ? 1 : 0,
+                                                  P->ncat ? P->sched.bn : 0);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -690,17 +704,19 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     P->prepacked = false;  // buffer now holds this call's filter
   }
   // B viewed as [16c][K][R*S][Cb] (b128: [32c][K][R*S][Cb/2]); box {c, rows, 1, blocks}
+  // (ncat: [B_hi;B_lo] rows per N tile -> 2K rows, boxes of 2 bn rows)
+  const int kr = P->ncat ? 2 : 1;
   if (P->b128) {
-    const cuuint64_t dims[4] = {32, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
-    const cuuint64_t strides[3] = {128, cuuint64_t(K) * 128, cuuint64_t(K) * 128 * R * S};
-    const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(s.kps / 2)};
+    const cuuint64_t dims[4] = {32, cuuint64_t(K) * kr, cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
+    const cuuint64_t strides[3] = {128, cuuint64_t(K) * kr * 128, cuuint64_t(K) * kr * 128 * R * S};
+    const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs) * kr, 1, cuuint32_t(s.kps / 2)};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     encode(&tb, b_hi, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
     encode(&tblo, b_lo, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
   } else {
-    const cuuint64_t dims[4] = {16, cuuint64_t(K), cuuint64_t(R) * S, cuuint64_t(Cb)};
-    const cuuint64_t strides[3] = {64, cuuint64_t(K) * 64, cuuint64_t(K) * 64 * R * S};
-    const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs), 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
+    const cuuint64_t dims[4] = {16, cuuint64_t(K) * kr, cuuint64_t(R) * S, cuuint64_t(Cb)};
+    const cuuint64_t strides[3] = {64, cuuint64_t(K) * kr * 64, cuuint64_t(K) * kr * 64 * R * S};
+    const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs) * kr, 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     encode(&tb, b_hi, 4, dims, strides, box, estr);
     encode(&tblo, b_lo, 4, dims, strides, box, estr);
@@ -759,8 +775,10 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
     prm.tmem_a = s.tmem_a;
     prm.egroups = s.egroups;
+    prm.ncat = P->ncat ? 1 : 0;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
-      prm.a_slot_col = (3 * s.bn + 31) / 32 * 32;
+      // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum
+      prm.a_slot_col = ((s.bn <= 64 ? 5 : 3) * s.bn + 31) / 32 * 32;
       prm.a_slots = std::min(kMaxStages, (512 - prm.a_slot_col) / 32);
       if (prm.a_slots < s.kps) throw RuntimeError("internal: TMEM A ring smaller than a stage");
     }
@@ -856,9 +874,10 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
                  (long long)(h[8 * kTraceStages + 5] - t0), (long long)(h[8 * kTraceStages + 6] - t0),
                  (long long)(h[8 * kTraceStages + 7] - t0));
     for (int i = 0; i < kTraceStages; ++i)
-      std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld\n", i,
+      std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld %8lld\n", i,
                    (long long)(h[i * 4] - t0), (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
-                   (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
+                   (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 3] - t0),
+                   (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
                    (long long)(h[4 * kTraceStages + i * 4 + 2] - t0));
   }
 }
@@ -943,6 +962,8 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     }
     // 128-B filter rows pair channel blocks inside a stage: needs even kps dividing Cb
     P->b128 = s.kps % 2 == 0 && (d.nIfm / 16) % s.kps == 0 && std::getenv("PSCONV_NO_B128") == nullptr;
+    P->ncat = mode == PSCONV_MODE_3XTF32 && s.bn <= 64 && !s.halo && !s.pp && s.cs == 1 &&
+              std::getenv("PSCONV_NO_NCAT") == nullptr;
     P->flt_elems = kd.nOfm * kd.nIfm * kd.kh * kd.kw;
     {
       int prev = 0;

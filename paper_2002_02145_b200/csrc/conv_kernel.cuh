@@ -103,6 +103,11 @@ struct ConvParams {
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
   int egroups;                    // host dispatch: epilogue warp groups (kernel template EG)
+  int ncat;                       // 3xTF32, BN <= 64, not halo: filter rows [B_hi;B_lo] per
+                                  // N tile; per K half one N = 2 BN MMA A_hi x [B_hi;B_lo]
+                                  // (-> D1 | D2) + one N = BN MMA A_lo x B_hi (-> D1);
+                                  // the epilogue adds D1 + D2. 45 + 64 instead of 3 x 45
+                                  // cycles per K half at BN = 64 (tools/probe_mma_pair.cu)
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -144,8 +149,11 @@ struct KernelCfg {
   static constexpr int kOutStageBytes = psconv::kOutStageBytes;
   // TMEM (per CTA: 128 lanes x BN columns per accumulator)
   static constexpr int kAccBufs = (SPLIT3 && BN == 256) ? 1 : 2;
-  static constexpr int kSumCol = kAccBufs * BN;
-  static constexpr int kColsNeeded = kAccBufs * BN + (SPLIT3 ? BN : 0);
+  // 3xTF32 at BN <= 64 (N-concat, ConvParams::ncat): an accumulator buffer is
+  // [D1 | D2], 2 x BN columns (A_hi x [B_hi;B_lo] in one N = 2 BN MMA)
+  static constexpr int kAccW = (SPLIT3 && BN <= 64) ? 2 * BN : BN;
+  static constexpr int kSumCol = kAccBufs * kAccW;
+  static constexpr int kColsNeeded = kAccBufs * kAccW + (SPLIT3 ? BN : 0);
   // 3xTF32 at BN <= 128 takes all 512 columns: the rest hold the TMEM A ring
   static constexpr int kTmemCols = (SPLIT3 && BN <= 128) ? 512
                                    : kColsNeeded <= 32    ? 32
@@ -402,7 +410,7 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
       ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
     else
       ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
-    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
     for (int cg = 0; cg < p.cbg; ++cg) {
       ptx::mbar_wait(&full[as], aph);  // PAIR: both CTAs' halos landed
       if (SPLIT3) ptx::mbar_wait(&split_full[as], aph);
@@ -519,7 +527,7 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
             ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
           else
             ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
-          d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+          d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
         }
         const int bi = kHaloB + bs;
         const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
@@ -734,13 +742,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           const int tw = s * tap_dw;  // input column of tap ki (tap dilation of the fold)
           if (issuer) {
             uint8_t* sa = sb + j * p.a_boxes * p.a_pitch;
-            uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes;
+            uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes * (p.ncat ? 2 : 1);
             if (!PAIR) {
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0, cb + i);
-              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, k0, rs, cb >> p.b128);
-              if (SPLIT3)
+              // (ncat: one box of [B_hi;B_lo] rows of the N tile)
+              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, p.ncat ? 2 * k0 : k0, rs, cb >> p.b128);
+              if (SPLIT3 && !p.ncat)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
                                  cb >> p.b128);
             } else {
@@ -794,8 +803,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // B: SW64 rows of one channel block, or (b128) SW128 rows of a block pair:
     // k-step j of the pair sits 64 B into the row, 8-row atoms 1024 B apart
     const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : desc0;
-    const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);                 // after an even j
-    const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
+    const uint32_t bstep = static_cast<uint32_t>(Cfg::kBBytes * (p.ncat ? 2 : 1)) >> 4;  // B of one k-step
+    const uint32_t b_even = p.b128 ? 4u : bstep;                 // after an even j
+    const uint32_t b_odd = p.b128 ? (2u * bstep - 4u) : bstep;
+    constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(BN <= 128 ? 2 * BN : BN), 128 * CS>();
     const uint32_t stage_desc = static_cast<uint32_t>(p.stage_bytes) >> 4;
     const uint32_t a_step = static_cast<uint32_t>(p.a_pitch) >> 4;  // next k-step's A tile
     const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
@@ -819,13 +830,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         else
           ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
         const int it0 = un.ib + c * p.chunk_stages;
         const int it_end = min(un.ie, it0 + p.chunk_stages);
         for (int it = it0; it < it_end; ++it) {
           const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
           ptx::mbar_wait(&full[stage], phase);  // PAIR: both CTAs' loads landed
+          if (tr) p.trace[4 * kTraceStages + gs * 4 + 3] = clock64();
           if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
           ptx::tc_fence_after();
           if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
@@ -845,12 +857,21 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                     printf("mma it=%d j=%d stage=%d aslot=%d ah=%u db=%llx dblo=%llx acc_in=%u d=%u\n", it, j, stage, aslot_j,
                            ah, (unsigned long long)db, (unsigned long long)db_lo, acc_in, d_tmem);
 #endif
+                  if (p.ncat) {
 #pragma unroll
-                  for (int h = 0; h < 2 && !skip_mma; ++h) {
-                    ptx::mma_tf32_ts(d_tmem, ah + 16 + h * 8, db + h * 2, kIdesc, acc_in);  // small terms first
-                    ptx::mma_tf32_ts(d_tmem, ah + h * 8, db_lo + h * 2, kIdesc, 1u);
-                    ptx::mma_tf32_ts(d_tmem, ah + h * 8, db + h * 2, kIdesc, 1u);
-                    acc_in = 1u;
+                    for (int h = 0; h < 2 && !skip_mma; ++h) {
+                      ptx::mma_tf32_ts(d_tmem, ah + h * 8, db + h * 2, kIdesc2, acc_in);  // -> D1 | D2
+                      ptx::mma_tf32_ts(d_tmem, ah + 16 + h * 8, db + h * 2, kIdesc, 1u);  // A_lo B_hi -> D1
+                      acc_in = 1u;
+                    }
+                  } else {
+#pragma unroll
+                    for (int h = 0; h < 2 && !skip_mma; ++h) {
+                      ptx::mma_tf32_ts(d_tmem, ah + 16 + h * 8, db + h * 2, kIdesc, acc_in);  // small terms first
+                      ptx::mma_tf32_ts(d_tmem, ah + h * 8, db_lo + h * 2, kIdesc, 1u);
+                      ptx::mma_tf32_ts(d_tmem, ah + h * 8, db + h * 2, kIdesc, 1u);
+                      acc_in = 1u;
+                    }
                   }
                   ptx::mma_commit(&aslot_empty[aslot_j]);
                   if (++aslot_j == p.a_slots) aslot_j = 0;
@@ -861,7 +882,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                if (SPLIT3) {
+                if (SPLIT3 && p.ncat) {
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc2, acc_in);        // -> D1 | D2
+                  ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, kIdesc, 1u);  // A_lo B_hi -> D1
+                } else if (SPLIT3) {
                   const uint64_t da_lo = da + alo_off + h * 2;
                   const uint64_t db_lo = db - b_off + blo_off + h * 2;
                   ptx::mma_tf32(d_tmem, da_lo, db + h * 2, kIdesc, acc_in);  // small terms first
@@ -961,13 +985,25 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
 #endif
         if (ev && store_thread && cit == 0) ev[4] = clock64();
         ptx::tc_fence_after();
-        const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
+        const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * Cfg::kAccW);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
 #pragma unroll 1
         for (int j = egrp; j < BN / DW; j += kGroups) {
           uint32_t v[DW];
           if constexpr (DW == 32) ptx::tmem_ld32(tacc + j * 32, v);
           else ptx::tmem_ld16(tacc + j * 16, v);
+          if constexpr (Cfg::kAccW == 2 * BN) {
+            if (p.ncat) {  // D1 + D2 (A_hi B_lo in its own accumulator)
+              uint32_t v2[DW];
+              if constexpr (DW == 32) ptx::tmem_ld32(tacc + BN + j * 32, v2);
+              else ptx::tmem_ld16(tacc + BN + j * 16, v2);
+              ptx::tmem_wait_ld();
+              ptx::reg_fence(v);
+              ptx::reg_fence(v2);
+#pragma unroll
+              for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(v2[i]));
+            }
+          }
           if (SPLIT3 && c > 0) {
             uint32_t sacc[DW];
             if constexpr (DW == 32) ptx::tmem_ld32(tsum + j * 32, sacc);

@@ -137,7 +137,11 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // MMA: two K=8 MMAs per k-step (x3 for 3xTF32) of max(BN/2, 46) cycles each --
   // an M=128 tf32 MMA takes >= ~46 cycles whatever N (tools/probe_mma_rate.cu:
   // N=64 48, N=128 64, N=256 128 cycles)
-  const double mma_cyc = 2.0 * mult * std::max(s.bn / 2.0, 46.0);
+  // 3xTF32 at BN <= 64 outside halo mode (N-concat): per K half one N = 2 BN MMA
+  // (A_hi x [B_hi;B_lo]) + one N = BN MMA (A_lo x B_hi) instead of three N = BN
+  const bool ncat = mult > 1 && s.bn <= 64 && !s.halo && std::max(1, s.cs) == 1;
+  const double mma_cyc = ncat ? 2.0 * (std::max(double(s.bn), 46.0) + std::max(s.bn / 2.0, 46.0))
+                              : 2.0 * mult * std::max(s.bn / 2.0, 46.0);
   // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows
   // per cycle per SM with every SM loading, for 64-B and 128-B rows alike
   // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows
