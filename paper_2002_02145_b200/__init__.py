@@ -211,6 +211,26 @@ class ConvPlan:
 
     __call__ = forward
 
+    def graph(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
+              accumulate: bool = False, prepacked: bool = True):
+        """Capture this call (fixed pointers) into a CUDA graph: returns a torch.cuda.CUDAGraph
+        whose replay() re-runs the conv (launch + PDL edges, plus a split-K flag reset when the
+        schedule splits tail tiles) with less host and launch overhead than forward() --
+        serving loops over the same buffers. One warm-up call runs first (lazy allocations)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            self.forward(inp, flt, out, img_begin, img_count, stream=side, accumulate=accumulate,
+                         prepacked=prepacked)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.forward(inp, flt, out, img_begin, img_count, stream=side, accumulate=accumulate,
+                         prepacked=prepacked)
+        return g
+
     def forward_host(self, inp, flt, out, img_begin: int = 0, img_count: int | None = None,
                      stream=None, accumulate: bool = False, prepacked: bool = False) -> None:
         """conv on HOST buffers (CPU tensors / numpy arrays; pinned for full overlap): the

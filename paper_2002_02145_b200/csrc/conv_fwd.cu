@@ -842,6 +842,12 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
       P->epoch = P->epoch == INT32_MAX ? 1 : P->epoch + 1;
       prm.epoch = P->epoch;
       prm.tile_flags = P->tile_flags + (P->epoch % kFlagRing) * P->flag_cap;
+      // CUDA-graph capture: the epoch is baked into the captured kernel, so every
+      // replay must start from cleared flags -- capture a reset of this region
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      CUDA_OK(cudaStreamIsCapturing(st, &cap));
+      if (cap == cudaStreamCaptureStatusActive)
+        CUDA_OK(cudaMemsetAsync(prm.tile_flags, 0, size_t(P->flag_cap) * sizeof(int), st));
     }
   }
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];

@@ -512,3 +512,33 @@ def test_parity_plane_accumulate_and_range():
                              accumulate=True, out_init=init)
     assert "pp:3" in rec
     assert oracle.rel_l2(yg, ref) <= TOL["3xtf32"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,recipe", [
+    ("tf32", "gpu=bn:64,box:8x8x2"),
+    ("3xtf32", "gpu=bn:64,box:8x8x2,ks:3"),          # tail split-K: flags reset per replay
+    ("tf32", "gpu=bn:64,box:8x8x2,ks:2,cl:2"),
+])
+def test_cuda_graph_replay(mode, recipe):
+    """ConvPlan.graph(): the captured launch (PDL edge, split-K flag reset) replays to the same
+    result as forward(), several times in a row."""
+    p = ps.ConvPreset.parse("conv:40,64,64,16,16,3,3,1,1,16,1,1,16,16")
+    sx, sw = seeds(21)
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), device=dev)
+    w = torch.empty(p.filter_elems(), device=dev)
+    ps.fill_input(p, sx, x, c_logical=64)
+    ps.fill_filter(p, sw, w, c_logical=64)
+    plan = ps.ConvPlan(p, mode=mode, device=0, recipe=recipe)
+    plan.prepack(w)
+    y0 = torch.empty(p.output_elems(), device=dev)
+    plan.forward(x, None, y0, prepacked=True)
+    y = torch.full((p.output_elems(),), float("nan"), device=dev)
+    g = plan.graph(x, None, y)
+    for _ in range(3):
+        y.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.isfinite(y).all()
+        assert oracle.rel_l2(y.cpu().numpy(), y0.cpu().numpy()) <= TOL[mode]
