@@ -542,3 +542,23 @@ def test_cuda_graph_replay(mode, recipe):
         torch.cuda.synchronize()
         assert torch.isfinite(y).all()
         assert oracle.rel_l2(y.cpu().numpy(), y0.cpu().numpy()) <= TOL[mode]
+
+
+@pytest.mark.gpu
+def test_parity_plane_forward_host():
+    """The few-channel kernel behind the host-buffer entry (conv_fwd_host): chunked images,
+    same result as its device path and within tolerance of the oracle."""
+    p = ps.ConvPreset.parse("conv:24,64,16,28,28,7,7,2,2,16,3,3,56,56")
+    sx, sw = seeds(22)
+    x = oracle.fill_input(p, sx, 3)
+    w = oracle.fill_filter(p, sw, 3)
+    ref = oracle.conv(p, x, w).ravel()
+    dev = torch.device("cuda:0")
+    plan = ps.ConvPlan(p, mode="tf32", device=0, recipe="gpu=pp:3")
+    yd = torch.empty(p.output_elems(), device=dev)
+    plan.forward(torch.from_numpy(x.ravel()).to(dev), torch.from_numpy(w.ravel()).to(dev), yd)
+    hy = np.full(p.output_elems(), np.nan, dtype=np.float32)
+    plan.forward_host(x.ravel(), w.ravel(), hy)
+    torch.cuda.synchronize()
+    assert np.array_equal(hy, yd.cpu().numpy())
+    assert oracle.rel_l2(hy, ref) <= TOL["tf32"]
