@@ -35,6 +35,8 @@ extern "C" {
 /* Arithmetic modes of the GPU path (BASELINE.json north_star). */
 #define PSCONV_MODE_3XTF32 0 /* fp32-faithful: D += Alo*Bhi + Ahi*Blo + Ahi*Bhi */
 #define PSCONV_MODE_TF32 1   /* fast mode: one TF32 product per MAC            */
+#define PSCONV_MODE_F16X2 2  /* fp32-faithful: power-of-two scaled fp16 hi/lo split,
+                                D += Alo*Bhi + Ahi*Blo + Ahi*Bhi as K=16 f16 MMAs */
 
 /* conv_fwd flags */
 #define PSCONV_FLAG_ACCUMULATE 1u /* out += conv (the reference body is `+=`,

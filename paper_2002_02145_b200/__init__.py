@@ -26,17 +26,18 @@ from ._lib import conv_desc, lib
 
 __all__ = [
     "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
-    "MODE_TF32", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
+    "MODE_TF32", "MODE_F16X2", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
     "brgemm", "fill_input", "fill_filter", "version", "parse_nest", "NestInfo", "GemmPlan",
     "model_stats", "ranker_train", "ranker_compare", "default_ranker_weights",
 ]
 
 MODE_3XTF32 = 0
 MODE_TF32 = 1
+MODE_F16X2 = 2  # fp32-faithful: power-of-two scaled fp16 hi/lo split (three K=16 f16 MMAs)
 FLAG_ACCUMULATE = 1
 FLAG_PREPACKED = 2
 FLAG_RELU = 4
-_MODES = {"3xtf32": MODE_3XTF32, "tf32": MODE_TF32}
+_MODES = {"3xtf32": MODE_3XTF32, "tf32": MODE_TF32, "f16x2": MODE_F16X2}
 
 
 class Error(RuntimeError):
@@ -328,7 +329,7 @@ def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5, ranker: str = "co
         if n < 0:
             _check(-n)
         ids = buf.value.decode().split("\n") if n else []
-        mname = "3xtf32" if mode == MODE_3XTF32 else "tf32"
+        mname = {v: k for k, v in _MODES.items()}[mode]
         return [(r, model_us(preset, r, mname)) for r in ids]
     us = (ctypes.c_double * k)()
     n = lib.conv_select_topk(ctypes.byref(d), mode, k, buf, len(buf), us)

@@ -31,6 +31,7 @@ struct conv_plan {
   float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
   bool ncat = false;           // 3xTF32 N-concat: prepacked rows [B_hi;B_lo] per N tile (ConvParams::ncat)
+  unsigned* absmax = nullptr;  // f16x2: |max| bits of [0] the last input range, [1] the filter
   // (c,s)-folded input (recipe fold:C, SURVEY §8d stem note): the layer has C <= 8
   // real input channels in one 16-channel block; G = 16 / C consecutive kw taps
   // are packed into one block, so the kernel runs the descriptor kd (kw' =
@@ -158,6 +159,42 @@ __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __re
   } else {
     hi[o] = x;
   }
+}
+
+// |max| over n floats (n % 4 == 0) into *out (as ordered uint bits; *out zeroed first)
+__global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned* out) {
+  unsigned m = 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n / 4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = x4[i];
+    m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                   max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// f16x2 filter prepack: the fp32 prepack's rows, each 16-channel group holding
+// fp16 hi (32 B) then lo (32 B) of x * sB, sB = pow2_scale(|max|)
+__global__ void prepack_filter_f16_kernel(const float* __restrict__ flt, uint16_t* __restrict__ out, int K,
+                                          int CRS, int RS, int b128, const unsigned* __restrict__ absmax) {
+  __shared__ float tile[16][17];
+  const int blk = blockIdx.x;
+  const int t = threadIdx.x;
+  tile[t >> 4][t & 15] = flt[static_cast<int64_t>(blk) * 256 + t];
+  __syncthreads();
+  const int k16 = t >> 4, c16 = t & 15;
+  const float x = tile[c16][k16] * pow2_scale(*absmax);
+  const int kb = blk / CRS, crs = blk % CRS;
+  const int cb = crs / RS, rs = crs % RS;
+  const int64_t k = kb * 16 + k16;
+  const int64_t o = b128 ? ((static_cast<int64_t>(cb >> 1) * RS + rs) * K + k) * 32 + (cb & 1) * 16 + c16
+                         : ((static_cast<int64_t>(cb) * RS + rs) * K + k) * 16 + c16;
+  const int64_t g = (o - c16) * 2;  // the 16-channel group in halves (64 B = 32 halves)
+  const __half h = __float2half_rn(x);
+  const __half l = __float2half_rn(x - __half2float(h));
+  out[g + c16] = *reinterpret_cast<const uint16_t*>(&h);
+  out[g + 16 + c16] = *reinterpret_cast<const uint16_t*>(&l);
 }
 
 // NCHW16c element e (relative to image img_begin) <- value(seed, logical NCHW index)
@@ -337,6 +374,19 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
     launch_fold_filter(P, flt, st);
     flt = P->wfold;
   }
+  if (P->mode == PSCONV_MODE_F16X2) {
+    // |max| of the filter -> B scale, then rows of fp16 hi|lo (same row layout as the
+    // fp32 prepack: 64-B rows, or 128-B rows pairing channel blocks)
+    const conv_desc& kd = P->kd;
+    const int Kb = int(kd.nOfm / 16), CRS = int(kd.nIfm / 16 * kd.kh * kd.kw);
+    const int64_t n = int64_t(kd.nOfm) * kd.nIfm * kd.kh * kd.kw;
+    CUDA_OK(cudaMemsetAsync(P->absmax + 1, 0, sizeof(unsigned), st));
+    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(flt, n, P->absmax + 1);
+    prepack_filter_f16_kernel<<<Kb * CRS, 256, 0, st>>>(flt, reinterpret_cast<uint16_t*>(P->flt_pack), int(kd.nOfm),
+                                                        CRS, int(kd.kh * kd.kw), P->b128 ? 1 : 0, P->absmax + 1);
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   const conv_desc& kd = P->kd;
   const int Kb = int(kd.nOfm / 16), CRS = int(kd.nIfm / 16 * kd.kh * kd.kw);
   const bool split3 = P->mode == PSCONV_MODE_3XTF32;
@@ -460,10 +510,10 @@ int grid_for(int64_t n) {
 }
 
 // ---------------------------------------------------------------- launch
-template <int BN, bool SPLIT3, int CS, int EPI, int EG>
+template <int BN, bool SPLIT3, int CS, int EPI, int EG, bool F16>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
-  if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2) || (EG == 2 && BN < 64)) {
+  if constexpr (BN / CS < 8 || (SPLIT3 && CS == 2) || (EG == 2 && BN < 64) || (F16 && (!SPLIT3 || CS == 2))) {
     throw RuntimeError("unsupported (bn, cluster, mode, epilogue groups) combination");
   } else {
     constexpr bool PAIR = CS == 2;
@@ -471,7 +521,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG>,
+      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG, F16>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     CUDA_OK(attr_err);
@@ -501,46 +551,49 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG>, prm, a, b, blo, o));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG, F16>, prm, a, b, blo, o));
   }
 }
 
-template <bool SPLIT3, int CS, int EPI, int EG>
+template <bool SPLIT3, int CS, int EPI, int EG, bool F16>
 void dispatch_bn_eg(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                     const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_conv<16, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
-    case 32: return launch_conv<32, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
-    case 64: return launch_conv<64, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
-    case 128: return launch_conv<128, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
-    case 256: return launch_conv<256, SPLIT3, CS, EPI, EG>(P, prm, a, b, blo, o, st);
+    case 16: return launch_conv<16, SPLIT3, CS, EPI, EG, F16>(P, prm, a, b, blo, o, st);
+    case 32: return launch_conv<32, SPLIT3, CS, EPI, EG, F16>(P, prm, a, b, blo, o, st);
+    case 64: return launch_conv<64, SPLIT3, CS, EPI, EG, F16>(P, prm, a, b, blo, o, st);
+    case 128: return launch_conv<128, SPLIT3, CS, EPI, EG, F16>(P, prm, a, b, blo, o, st);
+    case 256: return launch_conv<256, SPLIT3, CS, EPI, EG, F16>(P, prm, a, b, blo, o, st);
     default: throw RuntimeError("unsupported bn");
   }
 }
 
 // two epilogue groups (recipe eg:2) for bn >= 64; the fused (bias/ReLU)
 // epilogue always runs one group (fewer instantiations)
-template <bool SPLIT3, int CS, int EPI>
+template <bool SPLIT3, int CS, int EPI, bool F16>
 void dispatch_bn(int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   if constexpr (EPI != kEpiFused) {
-    if (prm.egroups == 2 && bn >= 64) return dispatch_bn_eg<SPLIT3, CS, EPI, 2>(bn, P, prm, a, b, blo, o, st);
+    if (prm.egroups == 2 && bn >= 64) return dispatch_bn_eg<SPLIT3, CS, EPI, 2, F16>(bn, P, prm, a, b, blo, o, st);
   }
-  return dispatch_bn_eg<SPLIT3, CS, EPI, 1>(bn, P, prm, a, b, blo, o, st);
+  return dispatch_bn_eg<SPLIT3, CS, EPI, 1, F16>(bn, P, prm, a, b, blo, o, st);
 }
 
-template <bool SPLIT3>
+template <bool SPLIT3, bool F16 = false>
 void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
                  const CUtensorMap& b, const CUtensorMap& blo, const CUtensorMap& o, cudaStream_t st) {
   switch (cs) {
     case 1:
-      if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 1, kEpiSplit>(bn, P, prm, a, b, blo, o, st);
-      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 1, kEpiFused>(bn, P, prm, a, b, blo, o, st)
-                                  : dispatch_bn<SPLIT3, 1, kEpiStore>(bn, P, prm, a, b, blo, o, st);
+      if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 1, kEpiSplit, F16>(bn, P, prm, a, b, blo, o, st);
+      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 1, kEpiFused, F16>(bn, P, prm, a, b, blo, o, st)
+                                  : dispatch_bn<SPLIT3, 1, kEpiStore, F16>(bn, P, prm, a, b, blo, o, st);
     case 2:
-      if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 2, kEpiSplit>(bn, P, prm, a, b, blo, o, st);
-      return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 2, kEpiFused>(bn, P, prm, a, b, blo, o, st)
-                                  : dispatch_bn<SPLIT3, 2, kEpiStore>(bn, P, prm, a, b, blo, o, st);
+      if constexpr (!F16) {
+        if (prm.ksplit > 1) return dispatch_bn<SPLIT3, 2, kEpiSplit, false>(bn, P, prm, a, b, blo, o, st);
+        return prm.bias || prm.relu ? dispatch_bn<SPLIT3, 2, kEpiFused, false>(bn, P, prm, a, b, blo, o, st)
+                                    : dispatch_bn<SPLIT3, 2, kEpiStore, false>(bn, P, prm, a, b, blo, o, st);
+      }
+      [[fallthrough]];
     default: throw RuntimeError("unsupported cluster size");
   }
 }
@@ -653,7 +706,14 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   const int Cb = int(d.nIfm / 16), Kb = int(d.nOfm / 16);
   const int H = int(d.ifh), W = int(d.ifw), R = int(d.kh), S = int(d.kw);
   const int Pp = int(d.ofh), Q = int(d.ofw);
-  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+  const bool split3 = split_mode(P->mode);  // 3xTF32 / f16x2: split-stage geometry
+  const bool f16 = P->mode == PSCONV_MODE_F16X2;
+  if (f16) {  // |max| of the input range -> the A scale (read by the kernel after griddepcontrol.wait)
+    const int64_t n = img_count * Cb * H * W * 16;
+    CUDA_OK(cudaMemsetAsync(P->absmax, 0, sizeof(unsigned), st));
+    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(in, n, P->absmax);
+    CUDA_OK(cudaGetLastError());
+  }
 
   // A: input viewed as [img_count][Cb][H][W][16] from the range's first image
   CUtensorMap ta, tb, tblo, tout;
@@ -698,7 +758,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
   const int K = Kb * 16;
   const float* b_hi = P->flt_pack;
-  const float* b_lo = split3 ? P->flt_pack + P->flt_elems : P->flt_pack;
+  const float* b_lo = P->mode == PSCONV_MODE_3XTF32 ? P->flt_pack + P->flt_elems : P->flt_pack;
   if (!prepacked) {
     launch_prepack(P, flt, st);
     P->prepacked = false;  // buffer now holds this call's filter
@@ -775,6 +835,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
     prm.tmem_a = s.tmem_a;
     prm.egroups = s.egroups;
+    prm.absmax = P->absmax;
     prm.ncat = P->ncat ? 1 : 0;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
       // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum
@@ -866,7 +927,9 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   prm.trace = (debug_env & 8) ? trace_buf : nullptr;
   prm.out = out;
   prm.out_img_stride = int64_t(Kb) * Pp * Q * 16;
-  if (split3)
+  if (P->mode == PSCONV_MODE_F16X2)
+    dispatch_cs<true, true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
+  else if (split3)
     dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
   else
     dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
@@ -906,7 +969,7 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
   return guarded([&] {
     if (!d_in || !out) throw ConfigError("null argument");
     *out = nullptr;
-    if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32)
+    if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32 && mode != PSCONV_MODE_F16X2)
       throw ConfigError("unknown mode " + std::to_string(mode));
     conv_desc d = *d_in;
     validate_desc(d);
@@ -977,12 +1040,14 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
       cudaSetDevice(device);
       const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
       cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&P->absmax, 2 * sizeof(unsigned));
       if (e == cudaSuccess && fold) e = cudaMalloc(&P->wfold, P->flt_elems * sizeof(float));
       if (e == cudaSuccess && fold)
         e = cudaMalloc(&P->xfold, size_t(kd.nImg) * fold_phases * kd.ifh * kd.ifw * 16 * sizeof(float));
       cudaSetDevice(prev);
       if (e != cudaSuccess) {
         cudaFree(P->flt_pack);
+        cudaFree(P->absmax);
         cudaFree(P->wfold);
         delete P;
         throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
@@ -1072,6 +1137,7 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->wfold);
     cudaFree(p->xfold);
     cudaFree(p->tile_flags);
+    cudaFree(p->absmax);
     cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }

@@ -41,6 +41,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "sm100_ptx.cuh"
 
@@ -108,6 +109,8 @@ struct ConvParams {
                                   // (-> D1 | D2) + one N = BN MMA A_lo x B_hi (-> D1);
                                   // the epilogue adds D1 + D2. 45 + 64 instead of 3 x 45
                                   // cycles per K half at BN = 64 (tools/probe_mma_pair.cu)
+  const unsigned* absmax;          // f16x2: |max| bits of [0] the input range, [1] the filter
+                                  // (power-of-two operand scales; the epilogue unscales)
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -253,6 +256,46 @@ __device__ __forceinline__ void split_lo(const float4* a, float4* alo, int n4, i
         alo[base + i * 128] = lo;
       }
     }
+  }
+}
+
+// f16x2 scale: 2^(14 - e) for |max| in [2^e, 2^(e+1)), so scaled operands stay
+// below 2^15 (fp16 max 65504) and keep the most precision in hi / lo
+__device__ __forceinline__ float pow2_scale(unsigned absmax_bits) {
+  if ((absmax_bits & 0x7FFFFFFFu) == 0) return 1.f;
+  int se = 14 - (static_cast<int>((absmax_bits >> 23) & 0xFFu) - 127);
+  se = se > 127 ? 127 : (se < -126 ? -126 : se);
+  return __uint_as_float(static_cast<uint32_t>(se + 127) << 23);
+}
+
+// f16x2 splitter: each 64-B fp32 row (16 channels, SW64 layout) of the stage's A
+// tiles -> a 64-B row of fp16 [hi 0..15 | lo 0..15] at the same offset of the out
+// region (same swizzle phase), x * s = hi + lo (both round-to-nearest). Each thread
+// walks its row's logical chunks (physical = logical ^ phase): conflict-free.
+__device__ __forceinline__ void split_f16(const uint8_t* a, uint8_t* out, int rows, int tid, float s) {
+  for (int r = tid; r < rows; r += 128) {
+    const uint32_t ph = (static_cast<uint32_t>(r) >> 1) & 3u;
+    float4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = *reinterpret_cast<const float4*>(a + r * 64 + ((k ^ ph) << 4));
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float v[4] = {x[k].x * s, x[k].y * s, x[k].z * s, x[k].w * s};
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        const __half2 h = __floats2half2_rn(v[e], v[e + 1]);
+        const float2 hf = __half22float2(h);
+        const __half2 l = __floats2half2_rn(v[e] - hf.x, v[e + 1] - hf.y);
+        hi[k * 2 + e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+        lo[k * 2 + e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+      }
+    }
+    uint8_t* o = out + r * 64;
+    *reinterpret_cast<uint4*>(o + ((0u ^ ph) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(o + ((1u ^ ph) << 4)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+    *reinterpret_cast<uint4*>(o + ((2u ^ ph) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    *reinterpret_cast<uint4*>(o + ((3u ^ ph) << 4)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
   }
 }
 
@@ -601,7 +644,9 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
 // 64->64 / 64->256): kEpiStore (store, or reduce-add for `+=`), kEpiFused
 // (+ bias / ReLU), kEpiSplit (tail split-K units, flag-ordered partials)
 // EG: epilogue warp groups (1, or 2 draining alternate 32-channel rounds; recipe eg:)
-template <int BN, bool SPLIT3, bool PAIR, int EPI, int EG>
+// F16 (with SPLIT3): the f16x2 mode -- the splitter writes scaled fp16 hi|lo rows
+// of A, the filter rows hold fp16 hi|lo, three K=16 kind::f16 MMAs per k-step
+template <int BN, bool SPLIT3, bool PAIR, int EPI, int EG, bool F16 = false>
 __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     conv_fwd_sm100(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tmap_in,
                    const __grid_constant__ CUtensorMap tmap_flt,
@@ -613,6 +658,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   const int kStages = p.stages;
   constexpr int kAccBufs = Cfg::kAccBufs;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
+  constexpr uint32_t kIdescF16 = ptx::idesc_f16_m128<BN, 128 * CS>();
 
   const long long t_entry = clock64();
   unsigned long long* ev = (kTrace && p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * kTraceStages : nullptr;
@@ -698,7 +744,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // expects both shares); the second CTA never arrives on its own.
     const bool skip_a = (p.debug & 1) != 0;
     const uint32_t tx1 =
-        ((skip_a ? 0u : a_step_bytes) + Cfg::kBBytes * (SPLIT3 ? 2 : 1)) * CS;  // per k-step
+        ((skip_a ? 0u : a_step_bytes) + Cfg::kBBytes * (SPLIT3 && !F16 ? 2 : 1)) * CS;  // per k-step
     const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
     // cb_group: one coordinate step per stage, boxes span kps channel blocks;
     // otherwise kps coordinate steps per stage (the last stage may be partial)
@@ -749,7 +795,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                   ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0, cb + i);
               // (ncat: one box of [B_hi;B_lo] rows of the N tile)
               ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, p.ncat ? 2 * k0 : k0, rs, cb >> p.b128);
-              if (SPLIT3 && !p.ncat)
+              if (SPLIT3 && !F16 && !p.ncat)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
                                  cb >> p.b128);
             } else {
@@ -880,6 +926,16 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                   continue;
                 }
               }
+              if constexpr (F16) {  // one K = 16 step: A (hi|lo) and B (hi|lo) rows, lo at +32 B
+                const uint64_t da16 = da + alo_off;
+                ptx::mma_f16(d_tmem, da16 + 2, db, kIdescF16, acc_in);  // A_lo B_hi (small terms first)
+                ptx::mma_f16(d_tmem, da16, db + 2, kIdescF16, 1u);      // A_hi B_lo
+                ptx::mma_f16(d_tmem, da16, db, kIdescF16, 1u);          // A_hi B_hi
+                acc_in = 1u;
+                da += a_step;
+                db += (j & 1) ? b_odd : b_even;
+                continue;
+              }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 if (SPLIT3 && p.ncat) {
@@ -959,6 +1015,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     const uint32_t row_swz = (static_cast<uint32_t>(srow) >> 1) & 3u;  // SW64: chunk ^= bits[7:8]
     int ostage = 0;                                                  // staging buffer toggle
     if (store_thread) ptx::prefetch_tmap(&tmap_out);
+    float out_scale = 1.f;
+    if constexpr (F16) {
+      ptx::griddep_wait();
+      out_scale = 1.f / (pow2_scale(p.absmax[0]) * pow2_scale(p.absmax[1]));
+    }
     int cit = 0;
     for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
@@ -1024,6 +1085,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           } else if (tc.live) {
             // fused epilogue on the finished sum: + bias[k], ReLU (the same
             // value for all lanes: broadcast loads through L1)
+            if constexpr (F16) {  // undo the operand scales (exact powers of two)
+#pragma unroll
+              for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * out_scale);
+            }
             if constexpr (EPI == kEpiFused) {
             if (p.bias != nullptr) {
               const float* bj = p.bias + tc.tk * BN + j * DW;
@@ -1105,6 +1170,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // ------------------------------------------------------------ splitter
     // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
     const int tid = threadIdx.x - 192;
+    float a_scale = 1.f;
+    if constexpr (F16) {
+      ptx::griddep_wait();  // the input |max| comes from the preceding kernel
+      a_scale = pow2_scale(p.absmax[0]);
+    }
     int stage = 0;
     uint32_t phase = 0;
     if (p.halo) {
@@ -1189,7 +1259,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         const float4* a = reinterpret_cast<const float4*>(stage_base(stage));
         float4* alo = reinterpret_cast<float4*>(stage_base(stage) + p.a_lo_off);
         const int n4 = (min(p.kps, p.ksteps - it * p.kps) * p.a_pitch) >> 4;
-        split_lo(a, alo, n4, tid);
+        if constexpr (F16)
+          split_f16(reinterpret_cast<const uint8_t*>(a), reinterpret_cast<uint8_t*>(alo), n4 >> 2, tid, a_scale);
+        else
+          split_lo(a, alo, n4, tid);
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);
         if (++stage == kStages) {

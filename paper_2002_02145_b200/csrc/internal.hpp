@@ -127,6 +127,10 @@ struct PpGeom {
 };
 PpGeom pp_geom(const conv_desc& d, int bn, int mode);  // throws ConfigError
 
+// Modes that split operands into hi/lo pieces (3xTF32, f16x2): same pipeline
+// stage structure (a lo / f16 region beside the fp32 A tile, chunked TMEM sums).
+inline bool split_mode(int mode) { return mode == PSCONV_MODE_3XTF32 || mode == PSCONV_MODE_F16X2; }
+
 // Closed-form model (select.cpp).
 struct ModelBreakdown {
   double us_total, us_tensor, us_hbm, us_l2, us_smem, us_epi;

@@ -270,6 +270,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   }
   // --- tile axes
   const int64_t K = d.nOfm;
+  if ((r.pp || r.halo) && mode == PSCONV_MODE_F16X2)
+    throw ConfigError("gpu pp / halo are not implemented for the f16x2 mode");
   if (r.pp) {
     // few-channel kernel (conv_pp.cuh): fixed 8 x 16 pixel tile, bn 64 or 128,
     // the whole reduction in one MMA chain of tap pairs
@@ -360,8 +362,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
   s.cs = r.cs ? r.cs : (mode == PSCONV_MODE_TF32 ? 2 : 1);
-  if (s.cs == 2 && mode == PSCONV_MODE_3XTF32)
-    throw ConfigError("GPU tile: the CTA pair (cl:2) is TF32-only; use cl:1 for 3xTF32");
+  if (s.cs == 2 && split_mode(mode))
+    throw ConfigError("GPU tile: the CTA pair (cl:2) is TF32-only; use cl:1 for 3xTF32 / f16x2");
   if (s.bn / s.cs < 8) throw ConfigError("GPU tile: bn / cluster size must be >= 8");
   canon.cs = s.cs;
   // TMEM accumulation chunk (3xTF32 numerics, see conv_kernel.cuh); tf32: whole reduction
@@ -372,14 +374,14 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   // each chunk boundary stalls the MMA on the drain (measured cfg5: ch 72 / 36 /
   // 32 / 24 -> 1738 / 1775 / 1789 / 1815 us; 40 k-steps ~ 4.8e-6 relL2)
   int chunk_def = ksteps;
-  if (mode == PSCONV_MODE_3XTF32) {
+  if (split_mode(mode)) {
     const int cmax = s.bn == 256 ? 40 : 16;
     const int nch = (ksteps + cmax - 1) / cmax;
     chunk_def = (ksteps + nch - 1) / nch;
   }
   // (TF32 accumulates the whole reduction in one TMEM buffer: the chunk running
   // sum needs the 3xTF32 TMEM layout, so ch: is a 3xTF32-only key)
-  if (r.chunk && mode != PSCONV_MODE_3XTF32) throw ConfigError("gpu ch (accumulation chunk) is a 3xtf32 option");
+  if (r.chunk && !split_mode(mode)) throw ConfigError("gpu ch (accumulation chunk) is a 3xtf32 / f16x2 option");
   s.chunk = r.chunk ? r.chunk : chunk_def;
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
@@ -426,14 +428,14 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
     const int64_t mgroups = (tq * tp * tn + std::max(1, s.cs) - 1) / std::max(1, s.cs);
     const int64_t tiles_k = d.nOfm / s.bn;
     const double a_bytes = 4.0 * d.nImg * d.nIfm * d.ifh * d.ifw;
-    const double b_bytes = 4.0 * d.nOfm * d.nIfm * d.kh * d.kw * (mode == PSCONV_MODE_3XTF32 ? 2 : 1);
+    const double b_bytes = 4.0 * d.nOfm * d.nIfm * d.kh * d.kw * (mode == PSCONV_MODE_3XTF32 ? 2 : 1);  // f16x2: hi|lo in 4 B
     int gm = 0;
     if (tiles_k >= 4 && mgroups >= 24 && a_bytes > 48e6 && b_bytes > 24e6) gm = 12;
     s.m_block = r.gm >= 0 ? r.gm : gm;
     canon.gm = r.gm >= 0 ? r.gm : -1;
   }
   s.chunk = (s.chunk + s.kps - 1) / s.kps * s.kps;  // chunks hold whole stages
-  canon.chunk = mode == PSCONV_MODE_3XTF32 ? s.chunk : 0;
+  canon.chunk = split_mode(mode) ? s.chunk : 0;
   canon.kg = r.kg ? s.kps : 0;
   s.egroups = r.eg ? r.eg : 1;
   canon.eg = s.egroups == 2 ? 2 : 0;
@@ -442,6 +444,8 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
 }
 
 int stage_bytes(const Schedule& s, int mode) {
+  // f16x2: fp32 A tile + its fp16 hi|lo tile (64-B rows) + B rows of fp16 hi|lo (64 B)
+  if (mode == PSCONV_MODE_F16X2) return s.kps * (128 * 64 * 2 + (s.bn / s.cs) * 64);
   const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
   // TMEM-A stages hold A once (its lo part lives in TMEM) and B hi + lo
   if (s.tmem_a) return s.kps * (128 * 64 + (s.bn / s.cs) * 64 * 2);

@@ -90,7 +90,10 @@ std::vector<std::tuple<int, int, int>> box_candidates(const conv_desc& d) {
 ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const Machine& m = kB200;
   const Geo g = geo(d);
-  const double mult = mode == PSCONV_MODE_3XTF32 ? 3.0 : 1.0;
+  // MMA work relative to TF32: 3xTF32 three K=8 products; f16x2 three K=16 f16
+  // products (one f16 MMA of K=16 ~ one tf32 MMA of K=8)
+  const double mult = mode == PSCONV_MODE_3XTF32 ? 3.0 : (mode == PSCONV_MODE_F16X2 ? 1.5 : 1.0);
+  const bool x3 = mode == PSCONV_MODE_3XTF32;  // separate B_lo rows (f16x2 packs hi|lo per row)
   const int64_t tq = (g.Q + s.qb - 1) / s.qb, tp = (g.P + s.pb - 1) / s.pb,
                 tn = (g.N + s.nb - 1) / s.nb, tk = g.K / s.bn;
   const int64_t mt = tq * tp * tn, tiles = mt * tk;
@@ -139,7 +142,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // N=64 48, N=128 64, N=256 128 cycles)
   // 3xTF32 at BN <= 64 outside halo mode (N-concat): per K half one N = 2 BN MMA
   // (A_hi x [B_hi;B_lo]) + one N = BN MMA (A_lo x B_hi) instead of three N = BN
-  const bool ncat = mult > 1 && s.bn <= 64 && !s.halo && std::max(1, s.cs) == 1;
+  const bool ncat = x3 && s.bn <= 64 && !s.halo && std::max(1, s.cs) == 1;
   const double mma_cyc = ncat ? 2.0 * (std::max(double(s.bn), 46.0) + std::max(s.bn / 2.0, 46.0))
                               : 2.0 * mult * std::max(s.bn / 2.0, 46.0);
   // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows
@@ -147,17 +150,17 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows
   // are 128 B when a stage pairs channel blocks (b128), halving their count.
   const bool b128 = s.kps % 2 == 0 && g.Cb % std::max(1, s.kps) == 0;
-  double rows = double(s.qb) * s.pb * s.nb + b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0);
+  double rows = double(s.qb) * s.pb * s.nb + b_rows * (x3 ? 2 : 1) * (b128 ? 0.5 : 1.0);
   double a_bytes = a_box;  // TMA writes of A per k-step
   if (s.halo) {
     // halo mode: the (Pb + R - 1) x (Q + S - 1) halo of a channel block is loaded
     // once for its R*S taps; the filter is resident (b_res: loaded once per CTA)
     // or streamed per tap through the B ring
     const double halo_rows = double(s.pb + g.R - 1) * (g.Q + g.S - 1) / (double(g.R) * g.S);
-    rows = halo_rows + (s.b_res ? 0.0 : b_rows * (mult > 1 ? 2 : 1) * (b128 ? 0.5 : 1.0));
+    rows = halo_rows + (s.b_res ? 0.0 : b_rows * (x3 ? 2 : 1) * (b128 ? 0.5 : 1.0));
     a_bytes = halo_rows * 64.0;
   }
-  const double deliver_b = a_bytes + (s.halo && s.b_res ? 0.0 : b_rows * 64.0 * (mult > 1 ? 2 : 1));
+  const double deliver_b = a_bytes + (s.halo && s.b_res ? 0.0 : b_rows * 64.0 * (x3 ? 2 : 1));
   const double del_cyc = rows / m.row_requests_per_cycle;
   // operand reads per k-step: 2 K-halves x (A 4 KB + B rows x 32 B) per MMA; with
   // TMEM-resident A (3xTF32) the MMAs read only B and the splitter reads A once
@@ -213,7 +216,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   b.us_mma = mma_cyc * to_us;
   b.us_smem_traffic = smem_cyc * to_us;
   b.us_rows = del_cyc * to_us;
-  b.l2_bytes = ksteps * (a_bytes + (s.halo && s.b_res ? 0.0 : s.bn * 64.0 * (mult > 1 ? 2 : 1) / cs)) * tiles;
+  b.l2_bytes = ksteps * (a_bytes + (s.halo && s.b_res ? 0.0 : s.bn * 64.0 * (x3 ? 2 : 1) / cs)) * tiles;
   b.us_l2 = b.l2_bytes / (m.l2_gbs * 1e9) * 1e6;
   (void)per_sm;
 

@@ -252,6 +252,18 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[smem] * B[smem], kind::f16 (fp16 operands, K = 16, fp32 accumulate).
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive (once) on an mbarrier when all previously issued tcgen05 ops finish.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
@@ -411,6 +423,16 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
          (static_cast<uint64_t>(lbo >> 4) << 16) | (static_cast<uint64_t>(sbo >> 4) << 32) |
          (1ull << 46) |  // descriptor version (sm_100)
          (2ull << 61);   // layout type: SWIZZLE_128B
+}
+
+// Instruction descriptor: kind::f16 with fp16 A and B (format 0), D=f32, K-major.
+template <int BN, int M = 128>
+__host__ __device__ constexpr uint32_t idesc_f16_m128() {
+  return (1u << 4)                                  // D format f32
+         | (0u << 7)                                // A format f16
+         | (0u << 10)                               // B format f16
+         | (static_cast<uint32_t>(BN >> 3) << 17)   // N >> 3
+         | (static_cast<uint32_t>(M >> 4) << 24);   // M >> 4
 }
 
 // Instruction descriptor: kind::tf32, D=f32, A and B K-major, M=128.

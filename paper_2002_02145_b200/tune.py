@@ -40,7 +40,7 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
         if 16 <= nb <= 256 and preset.nOfm % nb == 0:
             alt = {**kv, "bn": str(nb)}
             alt.pop("ta", None)
-            if mode == "3xtf32":
+            if mode in ("3xtf32", "f16x2"):
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
     # tail split-K: the model's split decision both ways

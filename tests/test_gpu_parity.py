@@ -13,7 +13,7 @@ from tests.cases import ALL, BASELINE, R50, seeds, with_images
 torch = pytest.importorskip("torch")
 ps = pytest.importorskip("paper_2002_02145_b200")
 
-TOL = {"3xtf32": 1e-5, "tf32": 5e-3}
+TOL = {"3xtf32": 1e-5, "tf32": 5e-3, "f16x2": 1e-5}
 
 
 def _run_gpu(p, c_logical, sx, sw, mode, recipe=None, img_begin=0, img_count=None,
@@ -562,3 +562,65 @@ def test_parity_plane_forward_host():
     torch.cuda.synchronize()
     assert np.array_equal(hy, yd.cpu().numpy())
     assert oracle.rel_l2(hy, ref) <= TOL["tf32"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    ("conv:2,64,64,14,14,3,3,1,1,16,1,1,14,14", 64, None),
+    ("conv:2,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, "gpu=bn:256,box:1x1x128"),
+    ("conv:2,256,256,14,14,3,3,1,1,16,1,1,14,14", 256, "gpu=bn:128,box:2x2x32,kg:2"),   # b128 rows
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:256,box:7x1x18,ks:2,eg:2"),
+    ("conv:6,512,512,7,7,3,3,1,1,16,1,1,7,7", 512, "gpu=bn:128,box:1x7x18,ks:3,kt:1"),
+    ("conv:3,128,128,28,28,3,3,2,2,16,1,1,56,56", 128, "gpu=bn:128,box:4x4x8,kg:1,ch:5"),
+    ("conv:28,64,256,56,56,1,1,1,1,16,0,0,56,56", 256, "gpu=bn:64,box:8x8x2"),
+    ("conv:300,64,32,8,16,1,1,1,1,16,0,0,8,16", 32, "gpu=bn:16,box:16x8x1"),
+    ("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32", 3, "gpu=bn:64,fold:3"),
+])
+def test_f16x2_mode(conv, c_log, recipe):
+    """f16x2 (fp32-faithful): power-of-two scaled fp16 hi/lo split of both operands, three
+    K=16 kind::f16 MMAs per 16-channel k-step; relative L2 <= 1e-5 like 3xTF32."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("f16x2", conv, c_log, 23, "f16x2", n, recipe)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("xs,ws", [(1e-3, 1.0), (1.0, 1e4), (3e4, 2e-5), (1e-6, 1e-6)])
+def test_f16x2_dynamic_range(xs, ws):
+    """The operand scales follow the data: inputs / filters far from unit magnitude keep the
+    1e-5 bound (hi/lo stay in fp16's normal range after scaling)."""
+    p = ps.ConvPreset.parse("conv:3,128,64,12,12,3,3,1,1,16,1,1,12,12")
+    sx, sw = seeds(24)
+    x = (oracle.fill_input(p, sx, 64) * np.float32(xs)).astype(np.float32)
+    w = (oracle.fill_filter(p, sw, 64) * np.float32(ws)).astype(np.float32)
+    ref = oracle.conv(p, x, w).ravel()
+    dev = torch.device("cuda:0")
+    y = torch.full((p.output_elems(),), float("nan"), device=dev)
+    plan = ps.ConvPlan(p, mode="f16x2", device=0)
+    plan.forward(torch.from_numpy(x.ravel()).to(dev), torch.from_numpy(w.ravel()).to(dev), y)
+    torch.cuda.synchronize()
+    err = oracle.rel_l2(y.cpu().numpy(), ref)
+    assert err <= TOL["f16x2"], f"relL2 {err:.3e} at scales {xs}, {ws}"
+
+
+@pytest.mark.gpu
+def test_f16x2_accumulate_bias_relu():
+    p = ps.ConvPreset.parse("conv:4,128,64,12,12,3,3,1,1,16,1,1,12,12")
+    sx, sw = seeds(25)
+    x = oracle.fill_input(p, sx, 64)
+    w = oracle.fill_filter(p, sw, 64)
+    conv = oracle.conv(p, x, w).ravel()
+    dev = torch.device("cuda:0")
+    xd, wd = torch.from_numpy(x.ravel()).to(dev), torch.from_numpy(w.ravel()).to(dev)
+    init = np.random.default_rng(8).uniform(-1, 1, p.output_elems()).astype(np.float32)
+    y = torch.from_numpy(init.copy()).to(dev)
+    plan = ps.ConvPlan(p, mode="f16x2", device=0)
+    plan.forward(xd, wd, y, accumulate=True)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(y.cpu().numpy(), conv + init) <= TOL["f16x2"]
+    bias = np.random.default_rng(9).uniform(-1, 1, p.nOfm).astype(np.float32)
+    y2 = torch.empty(p.output_elems(), device=dev)
+    plan.forward(xd, wd, y2, bias=torch.from_numpy(bias).to(dev), relu=True)
+    torch.cuda.synchronize()
+    ref = conv.reshape(p.nImg, p.nOfm // 16, p.ofh, p.ofw, 16) + bias.reshape(1, p.nOfm // 16, 1, 1, 16)
+    ref = np.maximum(ref, 0).ravel()
+    assert oracle.rel_l2(y2.cpu().numpy(), ref) <= TOL["f16x2"]
