@@ -222,7 +222,11 @@ def run_ours(args, rank, world, local_rank):
     ps.fill_filter(p, sw, w, c_logical=c_logical)
     # schedule: the selector's model top-k timed on the device (untimed plan creation,
     # PAPER.md:224-226), rank 0's choice broadcast so every rank runs the same recipe
-    recipes = {args.mode: args.recipe, "tf32" if args.mode == "3xtf32" else "3xtf32": None}
+    # legs: the requested mode, the other of 3xTF32 / TF32, and f16x2 (the second
+    # fp32-faithful split) beside a 3xTF32 headline
+    recipes = {args.mode: args.recipe, ("tf32" if args.mode != "tf32" else "3xtf32"): None}
+    if args.mode == "3xtf32" and not args.no_f16x2:
+        recipes["f16x2"] = None
     if args.tune > 0:
         from paper_2002_02145_b200.tune import autotune
         for m in list(recipes):
@@ -291,7 +295,7 @@ def run_ours(args, rank, world, local_rank):
     local_flops = p.flops(c_logical, n_img=n_local)
     hbm_gbs, bf16_tflops, peak_src = peaks()
     p_tf32 = bf16_tflops / 2.0
-    p_mode = p_tf32 / 3.0 if args.mode == "3xtf32" else p_tf32
+    p_mode = p_tf32 / 3.0 if args.mode == "3xtf32" else (bf16_tflops / 3.0 if args.mode == "f16x2" else p_tf32)
 
     with ClockSampler(local_rank) as clk:
         # (1) the step: filter repack + conv kernel (= conv_fwd), L2 flushed before each
@@ -299,12 +303,24 @@ def run_ours(args, rank, world, local_rank):
         step_ms, kern_ms = timed_step(plan, args.steps, args.warmup)
         ms_max = max_over_ranks(statistics.mean(step_ms))
         kms = max_over_ranks(statistics.mean(kern_ms))
-        # (3) the other arithmetic mode, same protocol
-        other = "tf32" if args.mode == "3xtf32" else "3xtf32"
+        # (3) the other arithmetic mode(s), same protocol
+        other = "tf32" if args.mode != "tf32" else "3xtf32"
         plan2 = ps.ConvPlan(p, mode=other, device=local_rank, recipe=recipes[other])
         step2, kern2 = timed_step(plan2, args.steps, args.warmup)
         ms2 = max_over_ranks(statistics.mean(step2))
         kms2 = max_over_ranks(statistics.mean(kern2))
+        f16_leg = None
+        if "f16x2" in recipes:
+            # f16x2: fp16 hi/lo split of both operands with power-of-two scales (the input
+            # |max| pre-pass is inside the step), three K=16 f16 MMAs per k-step
+            plan3 = ps.ConvPlan(p, mode="f16x2", device=local_rank, recipe=recipes["f16x2"])
+            step3, kern3 = timed_step(plan3, args.steps, args.warmup)
+            ms3 = max_over_ranks(statistics.mean(step3))
+            kms3 = max_over_ranks(statistics.mean(kern3))
+            y16 = torch.empty_like(y)
+            plan3.forward(x, w, y16, b0, n_local, stream)
+            torch.cuda.synchronize()
+            f16_leg = (plan3.recipe, ms3, kms3, y16)
         # restore this mode's output for verification
         plan.forward(x, w, y, b0, n_local, stream)
         # (4) end to end through the public API with host buffers
@@ -395,6 +411,18 @@ def run_ours(args, rank, world, local_rank):
         bi = 4 * (n_local * in_elems_img + p.filter_elems())
         bo = 4 * n_local * out_elems_img
         e2e_value = total_flops / (e2e_ms * 1e-3) / 1e9
+        f16 = None
+        if f16_leg is not None:
+            rid3, ms3, kms3, y16 = f16_leg
+            sl = slice(b0 * out_elems_img, b1 * out_elems_img)
+            d16 = float(torch.linalg.vector_norm((y16[sl] - y[sl]).double()) / torch.linalg.vector_norm(y[sl].double()))
+            f16 = {"mode": "f16x2", "value": round(total_flops / (ms3 * 1e-3) / 1e9, 1),
+                   "ms_per_step": round(ms3, 4), "kernel_ms": round(kms3, 4),
+                   "kernel_tflops": round(f_alg / (kms3 * 1e-3) / 1e12, 2),
+                   "frac_of_peak": round(f_alg / (kms3 * 1e-3) / 1e12 / (bf16_tflops / 3.0), 4),
+                   "peak": f"bf16/fp16 {bf16_tflops} TFLOP/s / 3 (three K=16 f16 MMAs per 16-channel k-step)",
+                   "rel_l2_vs_3xtf32": float(f"{d16:.3g}"), "recipe": rid3,
+                   "speedup_vs_3xtf32_step": round(ms_max / ms3, 3)}
         tf32 = {"mode": other, "value": round(total_flops / (ms2 * 1e-3) / 1e9, 1),
                 "ms_per_step": round(ms2, 4), "kernel_ms": round(kms2, 4),
                 "kernel_tflops": round(f_alg / (kms2 * 1e-3) / 1e12, 2),
@@ -405,7 +433,8 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 (3xtf32 tensor-core split, fp32 in/out)" if args.mode == "3xtf32" else "f32 in/out, tf32 tensor-core",
+            "dtype": {"3xtf32": "f32 (3xtf32 tensor-core split, fp32 in/out)", "tf32": "f32 in/out, tf32 tensor-core",
+                      "f16x2": "f32 (scaled fp16 hi/lo tensor-core split, fp32 in/out)"}[args.mode],
             "data": "synthetic: seeded uniform[-1,1) by logical NCHW/KCRS index (BASELINE configs)",
             "config": {"workload": f"{args.workload} {conv}", "mode": args.mode,
                        "recipe": plan.recipe, "images_per_gpu": n_local, "parallelism": f"dp{world} (img split)",
@@ -420,7 +449,8 @@ def run_ours(args, rank, world, local_rank):
                     "path": "ConvPlan.forward_host (C ABI conv_fwd_host): pinned host -> device -> pinned host, chunked and overlapped"},
             "gpu_launches": args.steps * plan.launches,
             "clocks": clocks,
-            args.mode if args.mode != "3xtf32" else "tf32_mode": tf32,
+            ("tf32_mode" if other == "tf32" else "3xtf32_mode"): tf32,
+            **({"f16x2_mode": f16} if f16 is not None else {}),
             "verified": verified,
         }
     return result
@@ -487,7 +517,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5")
-    ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32", "f16x2"])
+    ap.add_argument("--no-f16x2", action="store_true", help="skip the f16x2 leg beside 3xTF32")
     ap.add_argument("--recipe", default=None)
     ap.add_argument("--tune", type=int, default=4,
                     help="time the selector's top-k recipes before the run (0: model top-1)")

@@ -52,7 +52,7 @@ def main():
         plan = ps.ConvPlan(p, mode=r["mode"], recipe=rid)
         plan.prepack(w, st)
         ms = time_it(lambda: plan.forward(x, None, y, stream=st, prepacked=True), flush, args.steps, 3, st)
-        peak = bf16 / 2 / (3 if r["mode"] == "3xtf32" else 1)
+        peak = (bf16 / 3 if r["mode"] == "f16x2" else bf16 / 2 / (3 if r["mode"] == "3xtf32" else 1))
         t_roof = max(p.flops(c_log) / (peak * 1e12), bench.compulsory_bytes(p, c_log) / (hbm * 1e9)) * 1e3
         fr.append(t_roof / ms)
         print(f"{r['layer']:28s} {r['mode']:6s} {ms * 1e3:8.1f} us (was {r['kernel_ms'] * 1e3:8.1f})"

@@ -33,7 +33,7 @@ def main():
     ps.fill_filter(p, sw, w, c_logical=c_log)
     flush = L2Flush(dev)
     hbm, bf16, _ = bench.peaks()
-    peak = bf16 / 2 / (3 if mode == "3xtf32" else 1)
+    peak = (bf16 / 3 if mode == "f16x2" else bf16 / 2 / (3 if mode == "3xtf32" else 1))
     flops = p.flops(c_log)
     t_roof = max(flops / (peak * 1e12), bench.compulsory_bytes(p, c_log) / (hbm * 1e9)) * 1e3
     for r in recipes:

@@ -42,7 +42,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default=None, help="comma list of workload names")
-    ap.add_argument("--modes", default="3xtf32,tf32")
+    ap.add_argument("--modes", default="3xtf32,tf32,f16x2")
     ap.add_argument("--recipe", default=None)
     ap.add_argument("--tune", type=int, default=0, help="time the model's top-k per layer")
     ap.add_argument("--rows", default=None, help="append tuner `ranked` rows here")
@@ -75,7 +75,7 @@ def main():
             plan.prepack(w, stream)
             kern = time_it(lambda: plan.forward(x, None, y, stream=stream, prepacked=True), flush,
                            args.steps, args.warmup, stream)
-            peak = bf16 / 2 / (3 if mode == "3xtf32" else 1)
+            peak = (bf16 / 3 if mode == "f16x2" else bf16 / 2 / (3 if mode == "3xtf32" else 1))
             t_roof = max(flops / (peak * 1e12), bytes_c / (hbm * 1e9)) * 1e3
             rec = {"layer": name, "conv": conv, "mode": mode, "recipe": plan.recipe,
                    "gflop": round(flops / 1e9, 3), "mb_compulsory": round(bytes_c / 1e6, 1),
@@ -99,14 +99,14 @@ def main():
 def write_md(path, recs, src):
     import math
     with open(path, "w") as fh:
-        fh.write(f"# Per-layer sweep (1 B200, peaks: {src}; tf32 = bf16/2, 3xtf32 = tf32/3)\n\n")
+        fh.write(f"# Per-layer sweep (1 B200, peaks: {src}; tf32 = bf16/2, 3xtf32 = tf32/3, f16x2 = bf16/3)\n\n")
         fh.write("| layer | mode | GFLOP | bound | roofline ms | step ms | kernel ms | GFLOP/s (step) | frac (step) | frac (kernel) | recipe |\n")
         fh.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in recs:
             fh.write(f"| {r['layer']} | {r['mode']} | {r['gflop']} | {r['bound']} | {r['roofline_ms']} | "
                      f"{r['step_ms']} | {r['kernel_ms']} | {r['gflops_step']} | {r['frac_step']} | "
                      f"{r['frac_kernel']} | `{r['recipe']}` |\n")
-        for mode in ("3xtf32", "tf32"):
+        for mode in ("3xtf32", "tf32", "f16x2"):
             fr = [r["frac_step"] for r in recs if r["mode"] == mode]
             if fr:
                 g = math.exp(sum(map(math.log, fr)) / len(fr))
