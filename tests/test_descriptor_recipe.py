@@ -146,3 +146,18 @@ def test_parity_plane_recipe_key():
     for rid, p in bad:
         with pytest.raises(ConfigRejectedError):
             ps.model_us(p, rid, "tf32")
+
+
+def test_f16x2_mode_selection():
+    """f16x2 plans through the same selector: half the 3xTF32 MMA work is modelled faster on a
+    compute-bound layer; halo and the few-channel kernel are rejected for it."""
+    cfg5 = ConvPreset.parse("conv:2048,256,256,14,14,3,3,1,1,16,1,1,14,14")
+    top = ps.select_topk(cfg5, "f16x2", 2)
+    assert len(top) == 2 and all("ch:" in r for r, _ in top)  # chunked sums as in 3xTF32
+    assert ps.model_us(cfg5, top[0][0], "f16x2") < ps.model_us(cfg5, top[0][0], "3xtf32")
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(cfg5, "gpu=bn:256,halo:1", "f16x2")
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(ConvPreset.parse("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32"), "gpu=pp:3", "f16x2")
+    with pytest.raises(ConfigRejectedError):
+        ps.model_us(cfg5, "gpu=bn:256,cl:2", "f16x2")  # the CTA pair is TF32-only
