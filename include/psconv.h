@@ -145,6 +145,18 @@ int conv_plan_create(const conv_desc* d, int mode, int device, const char* recip
  * Returns 0 / 2 (stride > 1) / 1. */
 int conv_plan_create_bwd_data(const conv_desc* d, int mode, int device, const char* recipe_or_null,
                               conv_plan** out);
+/* Backward-weight plan: for the FORWARD descriptor d (stride 1,
+ * nImg a multiple of 16), dW = dL/dFilter from the forward input X and dY:
+ *   dW[k][c][r][s] = sum_{n,p,q} X[n][c][p+r-pad][q+s-pad] * dY[n][k][p][q]
+ * computed as a forward conv on the same kernel with the roles swapped -- the
+ * input channels become images, the batch the reduction channels, dY the filter
+ * (P x Q taps) and R x S the output extent -- split-K over the long reduction
+ * (kt:1, units reduce-added). tf32 / 3xtf32 modes. Returns 0 / 2 / 1. */
+int conv_plan_create_bwd_weight(const conv_desc* d, int mode, int device, const char* recipe_or_null,
+                                conv_plan** out);
+/* Runs a backward-weight plan: x = X (NCHW16c), dy = dY (NKPQ16k), dw = dW
+ * (KCRS16c16k, overwritten), all device arrays of the forward layer's sizes. */
+int conv_bwd_weight(const conv_plan* p, const float* x, const float* dy, float* dw, void* cuda_stream);
 void conv_plan_destroy(conv_plan* p);
 
 /* The plan's recipe id in the reference's grammar plus the gpu clause. */

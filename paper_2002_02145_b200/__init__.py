@@ -26,7 +26,7 @@ from ._lib import conv_desc, lib
 
 __all__ = [
     "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
-    "MODE_TF32", "MODE_F16X2", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
+    "MODE_TF32", "MODE_F16X2", "WgradPlan", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
     "brgemm", "fill_input", "fill_filter", "version", "parse_nest", "NestInfo", "GemmPlan",
     "model_stats", "ranker_train", "ranker_compare", "default_ranker_weights",
 ]
@@ -151,6 +151,41 @@ def _ptr(t) -> int:
     if hasattr(t, "ctypes"):  # numpy array (host buffers for forward_host)
         return t.ctypes.data
     return int(t)
+
+
+class WgradPlan:
+    """Backward-weight plan of a stride-1 forward layer (C ABI conv_plan_create_bwd_weight):
+    forward(x, dy, dw) computes dW (KCRS16c16k) from X (NCHW16c) and dY (NKPQ16k) as the
+    role-swapped forward conv on the same kernel, split-K over the N*P*Q reduction."""
+
+    def __init__(self, preset: "ConvPreset", mode="3xtf32", device: int = 0, recipe: str | None = None):
+        if isinstance(mode, str):
+            mode = _MODES[mode.lower()]
+        self.preset = ConvPreset(**{f.name: getattr(preset, f.name) for f in fields(preset)}).validate()
+        self.mode = mode
+        self.device = device
+        self._d = self.preset.to_c()
+        h = ctypes.c_void_p()
+        _check(lib.conv_plan_create_bwd_weight(ctypes.byref(self._d), mode, device,
+                                               recipe.encode() if recipe else None, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def recipe(self) -> str:
+        """The role-swapped conv's schedule."""
+        return lib.conv_plan_recipe(self._h).decode()
+
+    def forward(self, x, dy, dw, stream=None) -> None:
+        _check(lib.conv_bwd_weight(self._h, _ptr(x), _ptr(dy), _ptr(dw), _stream_ptr(stream)))
+
+    __call__ = forward
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.conv_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
 
 
 class ConvPlan:

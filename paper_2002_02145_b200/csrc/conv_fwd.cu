@@ -50,6 +50,13 @@ struct conv_plan {
   bool bwd_data = false;
   conv_desc fwd{};                // the forward layer's descriptor
   float* wtrans = nullptr;
+  // backward-weight plan (conv_plan_create_bwd_weight): d is the role-swapped conv
+  // (images = forward input channels, channels = batch, filter = dY); scratch for
+  // the transposed input, dY as that conv's KCRS16c16k filter, and its output
+  bool bwd_weight = false;
+  float* wg_x = nullptr;
+  float* wg_dy = nullptr;
+  float* wg_dw = nullptr;
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
   // conv_fwd_host staging (lazily created): double-buffered device chunks,
@@ -195,6 +202,47 @@ __global__ void prepack_filter_f16_kernel(const float* __restrict__ flt, uint16_
   const __half l = __float2half_rn(x - __half2float(h));
   out[g + c16] = *reinterpret_cast<const uint16_t*>(&h);
   out[g + 16 + c16] = *reinterpret_cast<const uint16_t*>(&l);
+}
+
+// ---- backward weight: layout moves around the role-swapped forward conv
+// X [N][C/16][HW][16c] -> Xt [C][N/16][HW][16n]: one 16x16 (n, c) tile per pixel
+// through shared memory (coalesced 64-B rows both ways)
+__global__ void wgrad_transpose_x_kernel(const float* __restrict__ x, float* __restrict__ xt, int N, int Cb,
+                                         int64_t HW) {
+  __shared__ float tile[16][17];
+  const int t = threadIdx.x;
+  const int Nb = N / 16;
+  for (int64_t b = blockIdx.x; b < int64_t(Nb) * Cb * HW; b += gridDim.x) {
+    const int64_t pix = b % HW;
+    const int cb = int((b / HW) % Cb), nb = int(b / HW / Cb);
+    __syncthreads();
+    tile[t >> 4][t & 15] = x[((int64_t(nb * 16 + (t >> 4)) * Cb + cb) * HW + pix) * 16 + (t & 15)];
+    __syncthreads();
+    xt[((int64_t(cb * 16 + (t >> 4)) * Nb + nb) * HW + pix) * 16 + (t & 15)] = tile[t & 15][t >> 4];
+  }
+}
+// dY [N][K/16][PQ][16k] -> the swapped conv's filter KCRS16c16k [K/16][N/16][PQ][16n][16k]
+__global__ void wgrad_dy_filter_kernel(const float* __restrict__ dy, float* __restrict__ f, int N, int Kb,
+                                       int64_t PQ) {
+  const int64_t n_el = int64_t(N) * Kb * PQ * 16;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
+    const int ki = int(e & 15), ni = int((e >> 4) & 15);
+    const int64_t r = e >> 8;  // (kb, nb, pq)
+    const int64_t pq = r % PQ;
+    const int nb = int((r / PQ) % (N / 16)), kb = int(r / PQ / (N / 16));
+    f[e] = dy[((int64_t(nb * 16 + ni) * Kb + kb) * PQ + pq) * 16 + ki];
+  }
+}
+// the swapped conv's output [C][K/16][RS][16k] -> dW KCRS16c16k [K/16][C/16][RS][16c][16k]
+__global__ void wgrad_dw_kernel(const float* __restrict__ o, float* __restrict__ dw, int C, int Kb, int RS) {
+  const int64_t n_el = int64_t(C) * Kb * RS * 16;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
+    const int ki = int(e & 15), ci = int((e >> 4) & 15);
+    const int64_t r = e >> 8;  // (kb, cb, rs)
+    const int rs = int(r % RS);
+    const int cb = int((r / RS) % (C / 16)), kb = int(r / RS / (C / 16));
+    dw[e] = o[((int64_t(cb * 16 + ci) * Kb + kb) * RS + rs) * 16 + ki];
+  }
 }
 
 // NCHW16c element e (relative to image img_begin) <- value(seed, logical NCHW index)
@@ -1106,6 +1154,93 @@ int conv_plan_create_bwd_data(const conv_desc* d_in, int mode, int device, const
   });
 }
 
+int conv_plan_create_bwd_weight(const conv_desc* d_in, int mode, int device, const char* recipe,
+                                conv_plan** out) {
+  return guarded([&] {
+    if (!d_in || !out) throw ConfigError("null argument");
+    *out = nullptr;
+    conv_desc f = *d_in;
+    validate_desc(f);
+    if (f.stride_h != 1 || f.stride_w != 1)
+      throw ConfigError("backward weight: only stride-1 layers are supported");
+    if (f.nImg % 16) throw ConfigError("backward weight: nImg must be a multiple of 16 (it becomes the reduction channels)");
+    if (mode == PSCONV_MODE_F16X2) throw ConfigError("backward weight: tf32 / 3xtf32 modes only");
+    // dW[k][c][r][s] = sum_{n,p,q} X[n][c][r+p-pad][s+q-pad] dY[n][k][p][q]: the forward
+    // conv with images = input channels, channels = batch, filter = dY (P x Q taps),
+    // output extent R x S, same padding
+    conv_desc t{};
+    t.nImg = f.nIfm;
+    t.nOfm = f.nOfm;
+    t.nIfm = f.nImg;
+    t.ofh = f.kh;
+    t.ofw = f.kw;
+    t.kh = f.ofh;
+    t.kw = f.ofw;
+    t.stride_h = t.stride_w = 1;
+    t.gemm_block = f.gemm_block;
+    t.pad_h = f.pad_h;
+    t.pad_w = f.pad_w;
+    t.ifh = f.ifh;
+    t.ifw = f.ifw;
+    conv_plan* P = nullptr;
+    auto create = [&](const char* r) {
+      const int rc = conv_plan_create(&t, mode, device, r, &P);
+      if (rc != PSCONV_OK) {
+        if (rc == PSCONV_ERR_CONFIG) throw ConfigError(conv_last_error());
+        throw RuntimeError(conv_last_error());
+      }
+    };
+    create(recipe && *recipe ? recipe : nullptr);
+    if (!(recipe && std::strstr(recipe, "ks:"))) {
+      // few tiles (C*R*S x K outputs) over a reduction of N*P*Q: split every tile
+      // into ks units (~2 per SM), partial sums reduce-added into the zeroed output
+      const Schedule& s = P->sched;
+      const int64_t tiles = ((t.ofw + s.qb - 1) / s.qb) * ((t.ofh + s.pb - 1) / s.pb) *
+                            ((t.nImg + s.nb - 1) / s.nb) * (t.nOfm / s.bn);
+      const int ks = int(std::min<int64_t>(64, std::max<int64_t>(1, (2 * P->num_sms + tiles - 1) / tiles)));
+      if (ks > 1) {
+        const std::string r2 = s.recipe_id + ",ks:" + std::to_string(ks) + ",kt:1";
+        conv_plan_destroy(P);
+        P = nullptr;
+        create(r2.c_str());
+      }
+    }
+    P->bwd_weight = true;
+    P->fwd = f;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaError_t e = cudaMalloc(&P->wg_x, size_t(f.nImg) * f.nIfm * f.ifh * f.ifw * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&P->wg_dy, size_t(f.nImg) * f.nOfm * f.ofh * f.ofw * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&P->wg_dw, size_t(f.nOfm) * f.nIfm * f.kh * f.kw * sizeof(float));
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      conv_plan_destroy(P);
+      throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    *out = P;
+  });
+}
+
+int conv_bwd_weight(const conv_plan* P, const float* x, const float* dy, float* dw, void* stream) {
+  return guarded([&] {
+    if (!P || !x || !dy || !dw) throw ConfigError("null argument");
+    if (!P->bwd_weight) throw ConfigError("not a backward-weight plan (conv_plan_create_bwd_weight)");
+    const conv_desc& t = P->d;  // the role-swapped conv
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int N = int(t.nIfm), C = int(t.nImg), Kb = int(t.nOfm / 16);
+    const int64_t HW = t.ifh * t.ifw, PQ = t.kh * t.kw;
+    const int64_t xb = int64_t(N / 16) * (C / 16) * HW;
+    wgrad_transpose_x_kernel<<<int(std::min<int64_t>(xb, 148 * 32)), 256, 0, st>>>(x, P->wg_x, N, C / 16, HW);
+    wgrad_dy_filter_kernel<<<grid_for(int64_t(N) * Kb * PQ * 16), 256, 0, st>>>(dy, P->wg_dy, N, Kb, PQ);
+    CUDA_OK(cudaGetLastError());
+    launch_range(P, P->wg_x, P->wg_dy, P->wg_dw, C, st, 0u);
+    wgrad_dw_kernel<<<grid_for(int64_t(C) * Kb * t.ofh * t.ofw * 16), 256, 0, st>>>(P->wg_dw, dw, C, Kb,
+                                                                                  int(t.ofh * t.ofw));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
 void conv_plan_destroy(conv_plan* p) {
   if (!p) return;
   if (p->pipe) {
@@ -1138,6 +1273,9 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->xfold);
     cudaFree(p->tile_flags);
     cudaFree(p->absmax);
+    cudaFree(p->wg_x);
+    cudaFree(p->wg_dy);
+    cudaFree(p->wg_dw);
     cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }

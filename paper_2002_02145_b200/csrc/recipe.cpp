@@ -104,7 +104,7 @@ Recipe Recipe::parse(const std::string& text) {
             throw ConfigError("gpu kg must be 1, 2, 4 or 8");
         } else if (key == "ks") {
           r.ks = static_cast<int>(parse_int(val, "gpu split-K"));
-          if (r.ks < 1 || r.ks > 16) throw ConfigError("gpu ks must be in [1, 16]");
+          if (r.ks < 1 || r.ks > 64) throw ConfigError("gpu ks must be in [1, 64]");
         } else if (key == "br") {
           r.br = static_cast<int>(parse_int(val, "gpu resident filter"));
           if (r.br != 0 && r.br != 1) throw ConfigError("gpu br must be 0 or 1");

@@ -111,7 +111,7 @@ def test_split_k_recipe_keys():
     base = "gpu=bn:256,box:1x1x128,cl:1,ch:36"
     assert ps.model_us(p, base + ",ks:3", "3xtf32") < ps.model_us(p, base + ",ks:1", "3xtf32")
     assert ps.model_us(p, base + ",ks:3,kt:1", "3xtf32") > 0
-    for bad in (",kt:2", ",ks:0", ",ks:17"):
+    for bad in (",kt:2", ",ks:0", ",ks:65"):
         with pytest.raises(ConfigRejectedError):
             ps.model_us(p, base + bad, "3xtf32")
 

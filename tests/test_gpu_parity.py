@@ -624,3 +624,55 @@ def test_f16x2_accumulate_bias_relu():
     ref = conv.reshape(p.nImg, p.nOfm // 16, p.ofh, p.ofw, 16) + bias.reshape(1, p.nOfm // 16, 1, 1, 16)
     ref = np.maximum(ref, 0).ravel()
     assert oracle.rel_l2(y2.cpu().numpy(), ref) <= TOL["f16x2"]
+
+
+def _wgrad_ref(p, x, dy):
+    """dW[k][c][r][s] = sum_{n,p,q} X[n][c][p+r-pad][q+s-pad] dY[n][k][p][q] in float64,
+    returned in KCRS16c16k."""
+    N, K, C = p.nImg, p.nOfm, p.nIfm
+    P, Q, R, S, H, W_ = p.ofh, p.ofw, p.kh, p.kw, p.ifh, p.ifw
+    xl = x.reshape(N, C // 16, H, W_, 16).transpose(0, 1, 4, 2, 3).reshape(N, C, H, W_).astype(np.float64)
+    dyl = dy.reshape(N, K // 16, P, Q, 16).transpose(0, 1, 4, 2, 3).reshape(N, K, P, Q).astype(np.float64)
+    xp = np.zeros((N, C, H + 2 * p.pad_h, W_ + 2 * p.pad_w))
+    xp[:, :, p.pad_h:p.pad_h + H, p.pad_w:p.pad_w + W_] = xl
+    dw = np.zeros((K, C, R, S))
+    for r in range(R):
+        for s in range(S):
+            dw[:, :, r, s] = np.einsum("nkpq,ncpq->kc", dyl, xp[:, :, r:r + P, s:s + Q])
+    return dw.reshape(K // 16, 16, C // 16, 16, R, S).transpose(0, 2, 4, 5, 3, 1).ravel()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,recipe", [
+    ("conv:16,48,32,10,10,3,3,1,1,16,1,1,10,10", None),
+    ("conv:32,64,16,12,12,1,1,1,1,16,0,0,12,12", None),
+    ("conv:16,16,16,9,9,5,5,1,1,16,2,2,9,9", None),
+    ("conv:64,64,64,14,14,3,3,1,1,16,1,1,14,14", None),          # ResNet-style 3x3 at small N
+    ("conv:16,48,32,10,10,3,3,1,1,16,1,1,10,10", "gpu=bn:16,ks:5,kt:1"),
+])
+def test_backward_weight(conv, recipe, mode):
+    """dW = conv_bwd_weight(X, dY): the role-swapped forward conv (images = input channels,
+    channels = batch, filter = dY) split-K over N*P*Q, against float64."""
+    p = ps.ConvPreset.parse(conv)
+    rng = np.random.default_rng(26)
+    x = rng.uniform(-1, 1, p.input_elems()).astype(np.float32)
+    dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
+    ref = _wgrad_ref(p, x, dy)
+    dev = torch.device("cuda:0")
+    dw = torch.full((p.filter_elems(),), float("nan"), device=dev)
+    plan = ps.WgradPlan(p, mode=mode, device=0, recipe=recipe)
+    plan.forward(torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev), dw)
+    torch.cuda.synchronize()
+    got = dw.cpu().numpy()
+    assert np.isfinite(got).all()
+    err = oracle.rel_l2(got, ref)
+    print(f"wgrad {conv} {mode} {plan.recipe} relL2={err:.2e}")
+    assert err <= TOL[mode], f"relL2 {err:.3e} ({plan.recipe})"
+
+
+def test_backward_weight_rejects():
+    with pytest.raises(ps.ConfigRejectedError):
+        ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"))   # nImg % 16
+    with pytest.raises(ps.ConfigRejectedError):
+        ps.WgradPlan(ps.ConvPreset.parse("conv:16,64,64,5,5,3,3,2,2,16,1,1,10,10"))    # stride 2
