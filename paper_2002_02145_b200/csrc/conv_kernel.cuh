@@ -659,6 +659,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   constexpr int kAccBufs = Cfg::kAccBufs;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128 * CS>();
   constexpr uint32_t kIdescF16 = ptx::idesc_f16_m128<BN, 128 * CS>();
+  // N-concat only exists at BN <= 64 (3xTF32): wider tiles fold the check away (a
+  // runtime test in the MMA issue loop cost 9% on cfg5)
+  const bool ncat = SPLIT3 && !F16 && BN <= 64 && p.ncat != 0;
 
   const long long t_entry = clock64();
   unsigned long long* ev = (kTrace && p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * kTraceStages : nullptr;
@@ -788,14 +791,14 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           const int tw = s * tap_dw;  // input column of tap ki (tap dilation of the fold)
           if (issuer) {
             uint8_t* sa = sb + j * p.a_boxes * p.a_pitch;
-            uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes * (p.ncat ? 2 : 1);
+            uint8_t* sbb = sb + p.b_off + j * Cfg::kBBytes * (ncat ? 2 : 1);
             if (!PAIR) {
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0, cb + i);
               // (ncat: one box of [B_hi;B_lo] rows of the N tile)
-              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, p.ncat ? 2 * k0 : k0, rs, cb >> p.b128);
-              if (SPLIT3 && !F16 && !p.ncat)
+              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, ncat ? 2 * k0 : k0, rs, cb >> p.b128);
+              if (SPLIT3 && !F16 && !ncat)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
                                  cb >> p.b128);
             } else {
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // B: SW64 rows of one channel block, or (b128) SW128 rows of a block pair:
     // k-step j of the pair sits 64 B into the row, 8-row atoms 1024 B apart
     const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : desc0;
-    const uint32_t bstep = static_cast<uint32_t>(Cfg::kBBytes * (p.ncat ? 2 : 1)) >> 4;  // B of one k-step
+    const uint32_t bstep = static_cast<uint32_t>(Cfg::kBBytes * (ncat ? 2 : 1)) >> 4;  // B of one k-step
     const uint32_t b_even = p.b128 ? 4u : bstep;                 // after an even j
     const uint32_t b_odd = p.b128 ? (2u * bstep - 4u) : bstep;
     constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(BN <= 128 ? 2 * BN : BN), 128 * CS>();
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                     printf("mma it=%d j=%d stage=%d aslot=%d ah=%u db=%llx dblo=%llx acc_in=%u d=%u\n", it, j, stage, aslot_j,
                            ah, (unsigned long long)db, (unsigned long long)db_lo, acc_in, d_tmem);
 #endif
-                  if (p.ncat) {
+                  if (ncat) {
 #pragma unroll
                     for (int h = 0; h < 2 && !skip_mma; ++h) {
                       ptx::mma_tf32_ts(d_tmem, ah + h * 8, db + h * 2, kIdesc2, acc_in);  // -> D1 | D2
@@ -938,7 +941,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                if (SPLIT3 && p.ncat) {
+                if (ncat) {
                   ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc2, acc_in);        // -> D1 | D2
                   ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, kIdesc, 1u);  // A_lo B_hi -> D1
                 } else if (SPLIT3) {
@@ -1054,7 +1057,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           if constexpr (DW == 32) ptx::tmem_ld32(tacc + j * 32, v);
           else ptx::tmem_ld16(tacc + j * 16, v);
           if constexpr (Cfg::kAccW == 2 * BN) {
-            if (p.ncat) {  // D1 + D2 (A_hi B_lo in its own accumulator)
+            if (ncat) {  // D1 + D2 (A_hi B_lo in its own accumulator)
               uint32_t v2[DW];
               if constexpr (DW == 32) ptx::tmem_ld32(tacc + BN + j * 32, v2);
               else ptx::tmem_ld16(tacc + BN + j * 16, v2);
