@@ -901,6 +901,19 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                 if (p.tmem_a) {  // A_hi / A_lo from the TMEM slot of this k-step
                   const uint32_t ah = tmem_base + static_cast<uint32_t>(p.a_slot_col + aslot_j * 32);
                   const uint64_t db_lo = db - b_off + blo_off;
+                  if constexpr (F16) {  // A_hi at ah, A_lo at ah + 8; B_hi / B_lo = the row's K halves
+                    if (!skip_mma) {
+                      ptx::mma_f16_ts(d_tmem, ah + 8, db, kIdescF16, acc_in);  // A_lo B_hi (small first)
+                      ptx::mma_f16_ts(d_tmem, ah, db + 2, kIdescF16, 1u);      // A_hi B_lo
+                      ptx::mma_f16_ts(d_tmem, ah, db, kIdescF16, 1u);          // A_hi B_hi
+                    }
+                    acc_in = 1u;
+                    ptx::mma_commit(&aslot_empty[aslot_j]);
+                    if (++aslot_j == p.a_slots) aslot_j = 0;
+                    da += a_step;
+                    db += (j & 1) ? b_odd : b_even;
+                    continue;
+                  }
 #ifdef PSCONV_DBG_PRINT
                   if (blockIdx.x == 0)
                     printf("mma it=%d j=%d stage=%d aslot=%d ah=%u db=%llx dblo=%llx acc_in=%u d=%u\n", it, j, stage, aslot_j,
@@ -1216,6 +1229,30 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
             ptx::mbar_wait(&aslot_empty[slot], sph ^ 1);  // the MMAs of slot's last use retired
             ptx::tc_fence_after();
             const uint8_t* a = stage_base(stage) + j * p.a_pitch + row_off;
+            if constexpr (F16) {
+              // f16x2: the slot's first 16 columns = [hi halves 0..15 | lo halves 0..15],
+              // two halves per 32-bit column (the kind::f16 A-from-TMEM layout)
+              uint32_t v[16];
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 x = *reinterpret_cast<const float4*>(a + ((static_cast<uint32_t>(c4) ^ row_swz) << 4));
+                const float xs[4] = {x.x * a_scale, x.y * a_scale, x.z * a_scale, x.w * a_scale};
+#pragma unroll
+                for (int e = 0; e < 4; e += 2) {
+                  const __half2 h = __floats2half2_rn(xs[e], xs[e + 1]);
+                  const float2 hf = __half22float2(h);
+                  const __half2 l = __floats2half2_rn(xs[e] - hf.x, xs[e + 1] - hf.y);
+                  v[c4 * 2 + e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+                  v[8 + c4 * 2 + e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+                }
+              }
+              ptx::tmem_st16(lane_base + static_cast<uint32_t>(p.a_slot_col + slot * 32), v);
+              if (++slot == p.a_slots) {
+                slot = 0;
+                sph ^= 1;
+              }
+              continue;
+            }
             uint32_t hi[16], lo[16];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {

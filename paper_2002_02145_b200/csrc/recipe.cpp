@@ -445,7 +445,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
 
 int stage_bytes(const Schedule& s, int mode) {
   // f16x2: fp32 A tile + its fp16 hi|lo tile (64-B rows) + B rows of fp16 hi|lo (64 B)
-  if (mode == PSCONV_MODE_F16X2) return s.kps * (128 * 64 * 2 + (s.bn / s.cs) * 64);
+  if (mode == PSCONV_MODE_F16X2) return s.kps * (128 * 64 * (s.tmem_a ? 1 : 2) + (s.bn / s.cs) * 64);
   const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
   // TMEM-A stages hold A once (its lo part lives in TMEM) and B hi + lo
   if (s.tmem_a) return s.kps * (128 * 64 + (s.bn / s.cs) * 64 * 2);
@@ -486,7 +486,7 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   // 390 us); at bn 128 only 4 slots fit beside the accumulators (l2 3x3 312 ->
   // 339 us), so it is a tuner option there (recipe ta:1)
   {
-    const bool ok = mode == PSCONV_MODE_3XTF32 && s.bn <= 128 && !s.halo;
+    const bool ok = split_mode(mode) && s.bn <= 128 && !s.halo;
     const bool want = s.ta == 1 || (s.ta < 0 && s.bn <= 64);
     s.tmem_a = (ok && want && std::getenv("PSCONV_NO_TMEMA") == nullptr) ? 1 : 0;
   }

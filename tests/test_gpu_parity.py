@@ -575,6 +575,11 @@ def test_parity_plane_forward_host():
     ("conv:28,64,256,56,56,1,1,1,1,16,0,0,56,56", 256, "gpu=bn:64,box:8x8x2"),
     ("conv:300,64,32,8,16,1,1,1,1,16,0,0,8,16", 32, "gpu=bn:16,box:16x8x1"),
     ("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32", 3, "gpu=bn:64,fold:3"),
+    # TMEM-resident fp16 A (default at bn <= 64; ta:1 at bn 128) and the smem path (ta:0)
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,kg:4,ta:1"),
+    ("conv:3,64,64,20,20,3,3,1,1,16,1,1,20,20", 64, "gpu=bn:64,box:8x4x2,ta:0"),
+    ("conv:2,128,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:128,box:2x4x16,ta:1"),
+    ("conv:300,64,32,8,16,1,1,1,1,16,0,0,8,16", 32, "gpu=bn:64,box:16x8x1,ta:1,ch:1"),
 ])
 def test_f16x2_mode(conv, c_log, recipe):
     """f16x2 (fp32-faithful): power-of-two scaled fp16 hi/lo split of both operands, three
