@@ -31,7 +31,8 @@ struct conv_plan {
   float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
   bool ncat = false;           // 3xTF32 N-concat: prepacked rows [B_hi;B_lo] per N tile (ConvParams::ncat)
-  unsigned* absmax = nullptr;  // f16x2: |max| bits of [0] the last input range, [1] the filter
+  unsigned* absmax = nullptr;  // f16x2: |max| bits of [0] the filter, [1] / [2] alternating input slots
+  mutable int absmax_slot = 0;  // the input slot of the next call (the conv zeroes the other one)
   // (c,s)-folded input (recipe fold:C, SURVEY §8d stem note): the layer has C <= 8
   // real input channels in one 16-channel block; G = 16 / C consecutive kw taps
   // are packed into one block, so the kernel runs the descriptor kd (kw' =
@@ -170,6 +171,8 @@ __global__ void prepack_filter_kernel(const float* __restrict__ flt, float* __re
 
 // |max| over n floats (n % 4 == 0) into *out (as ordered uint bits; *out zeroed first)
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned* out) {
+  ptx::griddep_wait();  // PDL launch: the input may come from the preceding kernel
+  ptx::griddep_launch_dependents();
   unsigned m = 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n / 4; i += int64_t(gridDim.x) * blockDim.x) {
@@ -428,10 +431,10 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
     const conv_desc& kd = P->kd;
     const int Kb = int(kd.nOfm / 16), CRS = int(kd.nIfm / 16 * kd.kh * kd.kw);
     const int64_t n = int64_t(kd.nOfm) * kd.nIfm * kd.kh * kd.kw;
-    CUDA_OK(cudaMemsetAsync(P->absmax + 1, 0, sizeof(unsigned), st));
-    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(flt, n, P->absmax + 1);
+    CUDA_OK(cudaMemsetAsync(P->absmax, 0, sizeof(unsigned), st));
+    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(flt, n, P->absmax);
     prepack_filter_f16_kernel<<<Kb * CRS, 256, 0, st>>>(flt, reinterpret_cast<uint16_t*>(P->flt_pack), int(kd.nOfm),
-                                                        CRS, int(kd.kh * kd.kw), P->b128 ? 1 : 0, P->absmax + 1);
+                                                        CRS, int(kd.kh * kd.kw), P->b128 ? 1 : 0, P->absmax);
     CUDA_OK(cudaGetLastError());
     return;
   }
@@ -756,11 +759,33 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   const int Pp = int(d.ofh), Q = int(d.ofw);
   const bool split3 = split_mode(P->mode);  // 3xTF32 / f16x2: split-stage geometry
   const bool f16 = P->mode == PSCONV_MODE_F16X2;
-  if (f16) {  // |max| of the input range -> the A scale (read by the kernel after griddepcontrol.wait)
+  unsigned* amax_a = nullptr;
+  unsigned* amax_reset = nullptr;
+  if (f16) {
+    // |max| of the input range -> the A scale (read by the kernel after griddepcontrol.wait).
+    // Two slots alternate: this call's conv zeroes the previous call's slot, so no memset
+    // launch per call; PDL chains the pass to the previous kernel. (Under graph capture
+    // the slot is fixed, so it is cleared by a captured memset instead.)
     const int64_t n = img_count * Cb * H * W * 16;
-    CUDA_OK(cudaMemsetAsync(P->absmax, 0, sizeof(unsigned), st));
-    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(in, n, P->absmax);
-    CUDA_OK(cudaGetLastError());
+    amax_a = P->absmax + 1 + P->absmax_slot;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_OK(cudaStreamIsCapturing(st, &cap));
+    if (cap == cudaStreamCaptureStatusActive) {
+      CUDA_OK(cudaMemsetAsync(amax_a, 0, sizeof(unsigned), st));
+    } else {
+      amax_reset = P->absmax + 1 + (1 - P->absmax_slot);
+      P->absmax_slot ^= 1;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid_for(n / 4));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, absmax_kernel, in, n, amax_a));
   }
 
   // A: input viewed as [img_count][Cb][H][W][16] from the range's first image
@@ -883,7 +908,9 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
     prm.tmem_a = s.tmem_a;
     prm.egroups = s.egroups;
-    prm.absmax = P->absmax;
+    prm.absmax_a = amax_a;
+    prm.absmax_b = P->absmax;
+    prm.absmax_reset = amax_reset;
     prm.ncat = P->ncat ? 1 : 0;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
       // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum
@@ -1088,7 +1115,8 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
       cudaSetDevice(device);
       const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
       cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
-      if (e == cudaSuccess) e = cudaMalloc(&P->absmax, 2 * sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMalloc(&P->absmax, 3 * sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMemset(P->absmax, 0, 3 * sizeof(unsigned));
       if (e == cudaSuccess && fold) e = cudaMalloc(&P->wfold, P->flt_elems * sizeof(float));
       if (e == cudaSuccess && fold)
         e = cudaMalloc(&P->xfold, size_t(kd.nImg) * fold_phases * kd.ifh * kd.ifw * 16 * sizeof(float));

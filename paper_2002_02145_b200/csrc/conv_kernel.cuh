@@ -109,8 +109,9 @@ struct ConvParams {
                                   // (-> D1 | D2) + one N = BN MMA A_lo x B_hi (-> D1);
                                   // the epilogue adds D1 + D2. 45 + 64 instead of 3 x 45
                                   // cycles per K half at BN = 64 (tools/probe_mma_pair.cu)
-  const unsigned* absmax;          // f16x2: |max| bits of [0] the input range, [1] the filter
-                                  // (power-of-two operand scales; the epilogue unscales)
+  const unsigned* absmax_a;        // f16x2: |max| bits of the input range (power-of-two
+  const unsigned* absmax_b;        // operand scales; the epilogue unscales) and the filter;
+  unsigned* absmax_reset;          // the other input slot, zeroed for the next call
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -1034,7 +1035,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     float out_scale = 1.f;
     if constexpr (F16) {
       ptx::griddep_wait();
-      out_scale = 1.f / (pow2_scale(p.absmax[0]) * pow2_scale(p.absmax[1]));
+      out_scale = 1.f / (pow2_scale(*p.absmax_a) * pow2_scale(*p.absmax_b));
     }
     int cit = 0;
     for (int u = cluster; u < p.units; u += nclusters) {
@@ -1189,7 +1190,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     float a_scale = 1.f;
     if constexpr (F16) {
       ptx::griddep_wait();  // the input |max| comes from the preceding kernel
-      a_scale = pow2_scale(p.absmax[0]);
+      a_scale = pow2_scale(*p.absmax_a);
+      if (tid == 0 && p.absmax_reset) *p.absmax_reset = 0u;  // the previous call's slot
     }
     int stage = 0;
     uint32_t phase = 0;

@@ -33,7 +33,7 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     # epilogue-heavy layers, slower on others
     if int(kv["bn"]) >= 64:
         alts.append({**kv, "eg": "2"})
-    if mode == "3xtf32" and bn == 128:  # TMEM-resident A is opt-in at bn 128
+    if mode in ("3xtf32", "f16x2") and bn == 128:  # TMEM-resident A is opt-in at bn 128
         alts.append({**kv, "ta": "1"})
     widest = max(c for c in (16, 32, 64, 128, 256) if preset.nOfm % c == 0)
     for nb in (bn * 2, bn // 2, widest):
