@@ -411,7 +411,7 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
       t.tap_b[i] = g.tap_b[i];
     }
     const int64_t n = int64_t(g.b_bytes) / 4;
-    const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+    const bool split3 = P->mode != PSCONV_MODE_TF32;  // (f16x2 plans: the pp kernel's 3xTF32 arithmetic)
     pp_pack_filter_kernel<<<int((n + 255) / 256), 256, 0, st>>>(
         flt, P->flt_pack, split3 ? P->flt_pack + n : nullptr, n, g.bn, g.nmma, int(P->d.kh * P->d.kw), P->pp, t);
     CUDA_OK(cudaGetLastError());
@@ -728,7 +728,7 @@ void launch_pp(const conv_plan* P, const float* in, const float* flt, float* out
   }
   prm.bpack = P->flt_pack;
   prm.accumulate = (flags & PSCONV_FLAG_ACCUMULATE) ? 1 : 0;
-  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+  const bool split3 = P->mode != PSCONV_MODE_TF32;  // (f16x2 plans: the pp kernel's 3xTF32 arithmetic)
   if (g.bn == 64)
     split3 ? launch_pp_kernel<64, true>(P, prm, ta, tout, g.smem_bytes, st)
            : launch_pp_kernel<64, false>(P, prm, ta, tout, g.smem_bytes, st);

@@ -270,8 +270,9 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   }
   // --- tile axes
   const int64_t K = d.nOfm;
-  if ((r.pp || r.halo) && mode == PSCONV_MODE_F16X2)
-    throw ConfigError("gpu pp / halo are not implemented for the f16x2 mode");
+  // f16x2: no halo variant; the few-channel kernel has no fp16 variant either, so an
+  // f16x2 pp plan runs its 3xTF32 arithmetic (equally fp32-faithful)
+  if (r.halo && mode == PSCONV_MODE_F16X2) throw ConfigError("gpu halo is not implemented for the f16x2 mode");
   if (r.pp) {
     // few-channel kernel (conv_pp.cuh): fixed 8 x 16 pixel tile, bn 64 or 128,
     // the whole reduction in one MMA chain of tap pairs
@@ -584,7 +585,7 @@ PpGeom pp_geom(const conv_desc& d, int bn, int mode) {
   g.pitch = g.PC * 16;
   g.box_bytes = g.PR * g.PC * 16;
   g.plane_bytes = (g.box_bytes + 127) / 128 * 128;
-  const bool split3 = mode == PSCONV_MODE_3XTF32;
+  const bool split3 = mode != PSCONV_MODE_TF32;  // f16x2 plans use the 3xTF32 arithmetic here
   g.lo_off = g.planes * g.plane_bytes;
   g.stage_bytes = g.lo_off * (split3 ? 2 : 1);
   // taps sorted by operand address; pairs (t0, t1), (t2, t3), ... -- with an odd

@@ -157,7 +157,8 @@ def test_f16x2_mode_selection():
     assert ps.model_us(cfg5, top[0][0], "f16x2") < ps.model_us(cfg5, top[0][0], "3xtf32")
     with pytest.raises(ConfigRejectedError):
         ps.model_us(cfg5, "gpu=bn:256,halo:1", "f16x2")
-    with pytest.raises(ConfigRejectedError):
-        ps.model_us(ConvPreset.parse("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32"), "gpu=pp:3", "f16x2")
+    # the few-channel kernel has no fp16 variant: f16x2 pp plans run its 3xTF32 arithmetic
+    stem = ConvPreset.parse("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32")
+    assert ps.model_us(stem, "gpu=pp:3", "f16x2") == ps.model_us(stem, "gpu=pp:3", "3xtf32")
     with pytest.raises(ConfigRejectedError):
         ps.model_us(cfg5, "gpu=bn:256,cl:2", "f16x2")  # the CTA pair is TF32-only

@@ -498,6 +498,12 @@ def test_parity_plane_tap_pairs(conv, c_log, recipe, mode):
 
 
 @pytest.mark.gpu
+def test_parity_plane_f16x2_plan():
+    """An f16x2 plan with pp:C runs the few-channel kernel in its 3xTF32 arithmetic."""
+    _check("pp-f16x2", "conv:2,64,16,112,112,7,7,2,2,16,3,3,224,224", 3, 18, "f16x2", 2, "gpu=pp:3")
+
+
+@pytest.mark.gpu
 def test_parity_plane_accumulate_and_range():
     p = ps.ConvPreset.parse("conv:5,64,16,30,30,7,7,2,2,16,3,3,60,60")
     sx, sw = seeds(19)
