@@ -377,27 +377,31 @@ void launch_bwd_filter(const conv_plan* P, const float* flt, cudaStream_t st);
 struct PpTaps {
   int tap_a[psconv::kPpMaxMma], tap_b[psconv::kPpMaxMma];
 };
-__global__ void pp_pack_filter_kernel(const float* __restrict__ flt, float* __restrict__ hi,
-                                      float* __restrict__ lo, int64_t n_elems, int bn, int nmma, int RS,
+// (split: 3xTF32 N-concat blocks of 2 bn rows, [kh][2 bn / 8 groups][8][4]: groups < bn/8
+// hold hi = trunc_tf32(x), the rest lo = x - hi; n_elems counts both halves)
+__global__ void pp_pack_filter_kernel(const float* __restrict__ flt, float* __restrict__ out,
+                                      int split, int64_t n_elems, int bn, int nmma, int RS,
                                       int C, const __grid_constant__ PpTaps taps) {
   ptx::griddep_launch_dependents();
+  const int rows = split ? 2 * bn : bn;  // B rows per MMA block
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int c4 = int(e & 3), nr = int((e >> 2) & 7);
     const int64_t rest = e >> 5;
-    const int ng = int(rest % (bn / 8)), kh = int((rest / (bn / 8)) & 1);
-    const int64_t blk = rest / (bn / 4);  // tk * nmma + i
+    const int g = int(rest % (rows / 8)), kh = int((rest / (rows / 8)) & 1);
+    const int64_t blk = rest / (rows / 4);  // tk * nmma + i
     const int i = int(blk % nmma), tk = int(blk / nmma);
     const int tap = kh == 0 ? taps.tap_a[i] : taps.tap_b[i];
+    const bool is_lo = split && g >= bn / 8;
+    const int ng = is_lo ? g - bn / 8 : g;
     const int64_t n = int64_t(tk) * bn + ng * 8 + nr;
     float x = 0.f;
     if (tap >= 0 && c4 < C) x = flt[((n / 16) * RS + tap) * 256 + c4 * 16 + (n & 15)];
-    if (lo) {
+    if (split) {
       const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-      hi[e] = h;
-      lo[e] = x - h;
+      out[e] = is_lo ? x - h : h;
     } else {
-      hi[e] = x;
+      out[e] = x;
     }
   }
 }
@@ -410,10 +414,10 @@ void launch_prepack(const conv_plan* P, const float* flt, cudaStream_t st) {
       t.tap_a[i] = g.tap_a[i];
       t.tap_b[i] = g.tap_b[i];
     }
-    const int64_t n = int64_t(g.b_bytes) / 4;
     const bool split3 = P->mode != PSCONV_MODE_TF32;  // (f16x2 plans: the pp kernel's 3xTF32 arithmetic)
+    const int64_t n = int64_t(g.b_bytes) / 4 * (split3 ? 2 : 1);
     pp_pack_filter_kernel<<<int((n + 255) / 256), 256, 0, st>>>(
-        flt, P->flt_pack, split3 ? P->flt_pack + n : nullptr, n, g.bn, g.nmma, int(P->d.kh * P->d.kw), P->pp, t);
+        flt, P->flt_pack, split3 ? 1 : 0, n, g.bn, g.nmma, int(P->d.kh * P->d.kw), P->pp, t);
     CUDA_OK(cudaGetLastError());
     return;
   }

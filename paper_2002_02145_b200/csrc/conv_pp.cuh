@@ -59,8 +59,13 @@ struct PpCfg {
   static constexpr int kThreads = SPLIT3 ? 320 : 192;
   static constexpr int kOutBytes = 128 * 64;  // one 128-pixel x 16-channel staging block
   static constexpr int kOutBlocks = 4;        // two 32-channel rounds in flight
-  static constexpr int kMmaBBytes = BN * 32;  // one MMA's B block: BN rows x 8 tf32
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  // one MMA's B block: BN rows x 8 tf32 ([kh][BN/8][8][16 B]); 3xTF32 N-concat: 2 BN
+  // rows, B_hi then B_lo, so A_hi x [B_hi;B_lo] is ONE N = 2 BN MMA (-> D1 | D2) and
+  // A_lo x B_hi an N = BN MMA on the block's first half (-> D1); the epilogue adds D2
+  static constexpr int kBRowsMma = SPLIT3 ? 2 * BN : BN;
+  static constexpr int kMmaBBytes = kBRowsMma * 32;
+  static constexpr int kAccW = SPLIT3 ? 2 * BN : BN;  // accumulator columns per buffer
+  static constexpr int kTmemCols = 2 * kAccW < 32 ? 32 : 2 * kAccW;
   static_assert(BN == 64 || BN == 128, "BN");
 };
 
@@ -141,7 +146,8 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
     ptx::mbar_wait(b_full, 0);
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t bbase = ptx::smem_u32(bres);
-    constexpr uint32_t kBLbo = (BN / 8) * 128;  // B block: [kh][BN/8 groups][8 rows][16 B]
+    constexpr uint32_t kBLbo = (Cfg::kBRowsMma / 8) * 128;  // B block: [kh][rows/8 groups][8 rows][16 B]
+    constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(SPLIT3 ? 2 * BN : BN), 128>();
     int stage = 0, t = 0;
     uint32_t phase = 0;
     for (int g = blockIdx.x; g < p.groups; g += gridDim.x, ++t) {
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
       if (SPLIT3) ptx::mbar_wait(&split_full[stage], phase);
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
         const uint32_t a0 = sbase + static_cast<uint32_t>(stage * p.stage_bytes);
         const uint32_t b0 = bbase + static_cast<uint32_t>(tk * p.nmma * Cfg::kMmaBBytes);
         for (int i = 0; i < p.nmma; ++i) {
@@ -163,11 +169,8 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
           if (SPLIT3) {
             const uint64_t da_lo =
                 ptx::smem_desc_none(ao + static_cast<uint32_t>(p.lo_off), lbo, static_cast<uint32_t>(p.pitch));
-            const uint64_t db_lo = ptx::smem_desc_none(
-                b0 + static_cast<uint32_t>(p.b_bytes + i * Cfg::kMmaBBytes), kBLbo, 128u);
-            ptx::mma_tf32(d_tmem, da_lo, db, kIdesc, i > 0 ? 1u : 0u);  // small terms first
-            ptx::mma_tf32(d_tmem, da, db_lo, kIdesc, 1u);
-            ptx::mma_tf32(d_tmem, da, db, kIdesc, 1u);
+            ptx::mma_tf32(d_tmem, da, db, kIdesc2, i > 0 ? 1u : 0u);  // A_hi x [B_hi;B_lo] -> D1 | D2
+            ptx::mma_tf32(d_tmem, da_lo, db, kIdesc, 1u);            // A_lo x B_hi -> D1
           } else {
             ptx::mma_tf32(d_tmem, da, db, kIdesc, i > 0 ? 1u : 0u);
           }
@@ -198,11 +201,20 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
       const int buf = t & 1;
       ptx::mbar_wait(&acc_full[buf], (t >> 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * BN);
+      const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * Cfg::kAccW);
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
         uint32_t v[32];
         ptx::tmem_ld32(tacc + j * 32, v);
+        if constexpr (SPLIT3) {  // D1 + D2
+          uint32_t v2[32];
+          ptx::tmem_ld32(tacc + BN + j * 32, v2);
+          ptx::tmem_wait_ld();
+          ptx::reg_fence(v);
+          ptx::reg_fence(v2);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(v2[i]));
+        }
         ptx::tmem_wait_ld();
         ptx::reg_fence(v);
         uint8_t* st = out_stage + ostage * (2 * Cfg::kOutBytes);

@@ -108,7 +108,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
     // cycles each, N=128: 64), the planes' 16-B pixels read once (32-B sectors),
     // the filter resident; output written once
     const PpGeom pg = pp_geom(d, s.bn, mode);
-    const double mma_cyc = pg.nmma * (s.bn == 64 ? 48.0 : 64.0) * (mode == PSCONV_MODE_TF32 ? 1.0 : 3.0);
+    // per tap pair: TF32 one N = BN MMA; 3xTF32 (N-concat) one N = 2 BN + one N = BN
+    auto mma_n = [](double n) { return std::max(n / 2.0, 48.0); };
+    const double mma_cyc = pg.nmma * (mode == PSCONV_MODE_TF32 ? mma_n(s.bn) : mma_n(2.0 * s.bn) + mma_n(s.bn));
     b.us_mma = per_sm * mma_cyc / (m.clock_ghz * 1e3);
     b.us_tensor = b.us_mma;
     b.hbm_bytes = 32.0 * g.N * g.H * g.W + 4.0 * g.N * g.K * g.P * g.Q;
