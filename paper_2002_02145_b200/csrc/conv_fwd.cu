@@ -1110,7 +1110,7 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     }
     // 128-B filter rows pair channel blocks inside a stage: needs even kps dividing Cb
     P->b128 = s.kps % 2 == 0 && (d.nIfm / 16) % s.kps == 0 && std::getenv("PSCONV_NO_B128") == nullptr;
-    P->ncat = mode == PSCONV_MODE_3XTF32 && s.bn <= 64 && !s.halo && !s.pp && s.cs == 1 &&
+    P->ncat = mode == PSCONV_MODE_3XTF32 && s.bn <= 64 && !s.pp && s.cs == 1 &&
               std::getenv("PSCONV_NO_NCAT") == nullptr;
     P->flt_elems = kd.nOfm * kd.nIfm * kd.kh * kd.kw;
     {

@@ -339,6 +339,7 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   const bool skip_a = (p.debug & 1) != 0;
   const uint32_t a_tx = (skip_a ? 0u : static_cast<uint32_t>(p.kps * p.hr * p.hw * 64)) * CS;
   const uint32_t b_tx = static_cast<uint32_t>(Cfg::kBBytes * p.kps * (SPLIT3 ? 2 : 1)) * CS;
+  const bool hncat = SPLIT3 && BN <= 64 && p.ncat != 0;  // 3xTF32 N-concat filter rows
   const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
   const int taps = p.R * p.S;
   int as = 0, bs = 0, gs = 0;
@@ -354,8 +355,10 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
           uint8_t* sb = smem + p.hb_ring_off + (cg * taps + t) * p.hb_stage_bytes;
           const int cb = cg * p.kps;
           if (!PAIR) {
-            ptx::tma_load_4d(sb, tmap_flt, &full[kHaloB], 0, k0, t, cb >> p.b128);
-            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[kHaloB], 0, k0, t, cb >> p.b128);
+            // (N-concat: one box of [B_hi; B_lo] rows per block, conv_fwd.cu)
+            ptx::tma_load_4d(sb, tmap_flt, &full[kHaloB], 0, hncat ? 2 * k0 : k0, t, cb >> p.b128);
+            if (SPLIT3 && !hncat)
+              ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[kHaloB], 0, k0, t, cb >> p.b128);
           } else {
             ptx::tma_load_4d_cb(sb, tmap_flt, full_leader + 8u * kHaloB, 0, k0, t, cb >> p.b128);
           }
@@ -396,8 +399,9 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
           uint8_t* sb = smem + p.hb_ring_off + bs * p.hb_stage_bytes;
           if (!PAIR) {
             ptx::mbar_expect_tx(&full[bi], b_tx);
-            ptx::tma_load_4d(sb, tmap_flt, &full[bi], 0, k0, t, cb >> p.b128);
-            if (SPLIT3) ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[bi], 0, k0, t, cb >> p.b128);
+            ptx::tma_load_4d(sb, tmap_flt, &full[bi], 0, hncat ? 2 * k0 : k0, t, cb >> p.b128);
+            if (SPLIT3 && !hncat)
+              ptx::tma_load_4d(sb + p.b_lo_off, tmap_flt_lo, &full[bi], 0, k0, t, cb >> p.b128);
           } else {
             if (leader) ptx::mbar_expect_tx(&full[bi], b_tx);
             ptx::tma_load_4d_cb(sb, tmap_flt, full_leader + 8u * bi, 0, k0, t, cb >> p.b128);
@@ -431,8 +435,11 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
   constexpr int kAccBufs = Cfg::kAccBufs;
   const uint64_t adesc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
   const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : adesc0;
-  const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);
-  const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
+  const bool hncat = SPLIT3 && BN <= 64 && p.ncat != 0;  // [B_hi; B_lo] rows per block
+  const uint32_t bblk = static_cast<uint32_t>(Cfg::kBBytes * (hncat ? 2 : 1)) >> 4;
+  const uint32_t b_even = p.b128 ? 4u : bblk;
+  const uint32_t b_odd = p.b128 ? (2u * bblk - 4u) : bblk;
+  constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(BN <= 128 ? 2 * BN : BN), 128 * Cfg::kCS>();
   const uint32_t a_tile = static_cast<uint32_t>(p.a_tile) >> 4;
   const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
   const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
@@ -478,7 +485,10 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (!skip_mma) {
-                if (SPLIT3) {
+                if (SPLIT3 && hncat) {
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc2, acc_in);        // -> D1 | D2
+                  ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, 1u);   // A_lo B_hi
+                } else if (SPLIT3) {
                   ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, acc_in);
                   ptx::mma_tf32(d_tmem, da + h * 2, db + blo_off + h * 2, idesc, 1u);
                   ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, 1u);
@@ -538,8 +548,11 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
   constexpr int kAccBufs = Cfg::kAccBufs;
   const uint64_t adesc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
   const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : adesc0;
-  const uint32_t b_even = p.b128 ? 4u : (Cfg::kBBytes >> 4);
-  const uint32_t b_odd = p.b128 ? (2u * (Cfg::kBBytes >> 4) - 4u) : (Cfg::kBBytes >> 4);
+  const bool hncat = SPLIT3 && BN <= 64 && p.ncat != 0;  // [B_hi; B_lo] rows per block
+  const uint32_t bblk = static_cast<uint32_t>(Cfg::kBBytes * (hncat ? 2 : 1)) >> 4;
+  const uint32_t b_even = p.b128 ? 4u : bblk;
+  const uint32_t b_odd = p.b128 ? (2u * bblk - 4u) : bblk;
+  constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(BN <= 128 ? 2 * BN : BN), 128 * Cfg::kCS>();
   const uint32_t a_tile = static_cast<uint32_t>(p.a_tile) >> 4;
   const uint32_t alo_off = static_cast<uint32_t>(p.a_lo_off) >> 4;
   const uint32_t blo_off = static_cast<uint32_t>(p.b_lo_off) >> 4;
@@ -590,7 +603,10 @@ __device__ __forceinline__ void halo_mma(const ConvParams& p, uint8_t* smem, uin
           for (int j = 0; j < kps && !skip_mma; ++j) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (SPLIT3) {
+              if (SPLIT3 && hncat) {
+                ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc2, acc_in);        // -> D1 | D2
+                ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, 1u);   // A_lo B_hi
+              } else if (SPLIT3) {
                 ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, acc_in);
                 ptx::mma_tf32(d_tmem, da + h * 2, db + blo_off + h * 2, idesc, 1u);
                 ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, idesc, 1u);

@@ -144,7 +144,7 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // N=64 48, N=128 64, N=256 128 cycles)
   // 3xTF32 at BN <= 64 outside halo mode (N-concat): per K half one N = 2 BN MMA
   // (A_hi x [B_hi;B_lo]) + one N = BN MMA (A_lo x B_hi) instead of three N = BN
-  const bool ncat = x3 && s.bn <= 64 && !s.halo && std::max(1, s.cs) == 1;
+  const bool ncat = x3 && s.bn <= 64 && std::max(1, s.cs) == 1;
   const double mma_cyc = ncat ? 2.0 * (std::max(double(s.bn), 46.0) + std::max(s.bn / 2.0, 46.0))
                               : 2.0 * mult * std::max(s.bn / 2.0, 46.0);
   // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows

@@ -58,6 +58,13 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
             kv2.pop("box", None)  # the folded layer has its own box candidates
             kv2.pop("ch", None)
             alts.append({**kv2, "fold": str(c_logical)})
+    # 3xTF32 halo mode with the N-concat filter rows and ONE accumulation chunk (the lean
+    # 3x3 issuer needs it; <= 40 k-steps keeps the chunk error ~5e-6): the model ranks it
+    # low, measured best on the K = 64 3x3 layers
+    ksteps = preset.nIfm // 16 * preset.kh * preset.kw
+    if (mode == "3xtf32" and preset.stride_h == preset.stride_w == 1 and preset.kh * preset.kw > 1
+            and bn <= 64 and ksteps <= 40):
+        alts.append({"bn": str(bn), "halo": "1", "ch": str(ksteps), "eg": "2"})
     # few-channel kernel (conv_pp.cuh) when at most 4 input channels are real: tap pairs
     # straight from the input's parity planes, no folded copy
     if (0 < c_logical <= 4 and preset.nIfm == 16 and preset.stride_h == preset.stride_w <= 2
