@@ -687,3 +687,23 @@ def test_backward_weight_rejects():
         ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"))   # nImg % 16
     with pytest.raises(ps.ConfigRejectedError):
         ps.WgradPlan(ps.ConvPreset.parse("conv:16,64,64,5,5,3,3,2,2,16,1,1,10,10"))    # stride 2
+
+
+@pytest.mark.gpu
+def test_f16x2_forward_host_chunks():
+    """f16x2 behind conv_fwd_host: every chunk launch runs its own input |max| pass (the two
+    scale slots alternate per launch); result within the faithful bound of the oracle."""
+    conv = "conv:200,32,32,56,56,3,3,1,1,16,1,1,56,56"
+    p = ps.ConvPreset.parse(conv)
+    sx, sw = seeds(27)
+    x = oracle.fill_input(p, sx, 32)
+    w = oracle.fill_filter(p, sw, 32)
+    x[: x.size // 2] *= 1e-3  # the chunks see different input ranges
+    plan = ps.ConvPlan(p, mode="f16x2", device=0)
+    hy = np.full(p.output_elems(), np.nan, dtype=np.float32)
+    plan.forward_host(x.ravel(), w.ravel(), hy, img_begin=0, img_count=p.nImg)
+    torch.cuda.synchronize()
+    ref = oracle.conv(p, x, w).ravel()
+    per = p.output_elems(1)
+    for lo, hi in ((0, 5), (195, 200)):  # images from early and late chunks
+        assert oracle.rel_l2(hy[lo * per:hi * per], ref[lo * per:hi * per]) <= TOL["f16x2"]
