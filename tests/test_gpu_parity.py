@@ -242,7 +242,7 @@ def test_relu_with_accumulate_rejected():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32", "f16x2"])
 def test_gemm_from_nest_document(mode):
     """a matmul nest document runs on the conv kernel as a 1x1 conv."""
     import os
@@ -336,7 +336,7 @@ def _bwd_data_ref(p, dy, w):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32", "f16x2"])
 @pytest.mark.parametrize("conv", ["conv:2,64,32,12,12,3,3,1,1,16,1,1,12,12",
                                   "conv:2,32,48,9,11,5,5,1,1,16,2,2,9,11",
                                   "conv:3,128,64,7,7,1,1,1,1,16"])
@@ -707,3 +707,18 @@ def test_f16x2_forward_host_chunks():
     per = p.output_elems(1)
     for lo, hi in ((0, 5), (195, 200)):  # images from early and late chunks
         assert oracle.rel_l2(hy[lo * per:hi * per], ref[lo * per:hi * per]) <= TOL["f16x2"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32", "f16x2"])
+def test_empty_image_range_is_a_noop(mode):
+    """img_count = 0 launches nothing and leaves the output untouched (every mode)."""
+    p = ps.ConvPreset.parse("conv:4,64,64,10,10,3,3,1,1,16,1,1,10,10")
+    dev = torch.device("cuda:0")
+    x = torch.ones(p.input_elems(), device=dev)
+    w = torch.ones(p.filter_elems(), device=dev)
+    y = torch.full((p.output_elems(),), 7.0, device=dev)
+    plan = ps.ConvPlan(p, mode=mode, device=0)
+    plan.forward(x, w, y, img_begin=2, img_count=0)
+    torch.cuda.synchronize()
+    assert bool((y == 7.0).all())
