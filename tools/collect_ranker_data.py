@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--out", default="profiles/r01_ranker_data.jsonl")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--modes", default="3xtf32,tf32,f16x2")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream()
@@ -37,7 +38,7 @@ def main():
             y = torch.empty(p.output_elems(), device=dev)
             ps.fill_input(p, sx, x, c_logical=c_log)
             ps.fill_filter(p, sw, w, c_logical=c_log)
-            for mode in ("3xtf32", "tf32"):
+            for mode in args.modes.split(","):
                 for rid, mus in ps.select_topk(p, mode, k=args.k):
                     plan = ps.ConvPlan(p, mode=mode, recipe=rid)
                     plan.prepack(w, st)
