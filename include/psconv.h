@@ -246,6 +246,13 @@ int conv_select_topk_dnn(const conv_desc* d, int mode, int k, const char* weight
 /* Modelled time (microseconds) of one recipe, -1 on error. */
 double conv_model_us(const conv_desc* d, int mode, const char* recipe);
 
+/* Machine constants of the selector's model (the reference's machine file,
+ * cachefit.hpp:43-106, re-expressed for B200): "<key> <value>" lines with keys
+ * hbm_gbs, tf32_tflops, clock_ghz, sms, l2_bytes ('#' comments). The Python
+ * layer feeds this pod's MEASURED_PEAKS.json at import. Not thread-safe with a
+ * concurrent ranking. Returns 0 / 2. */
+int conv_select_set_machine(const char* text);
+
 /* ---------------------------------------------------------------------------
  * Device-side helpers (same stream semantics as conv_fwd).
  * Seeded generator: value(seed, i) = (int)(splitmix64(splitmix64(seed) ^ i) >> 40) * 2^-23 - 1,

@@ -28,7 +28,8 @@ __all__ = [
     "Error", "ConfigRejectedError", "AnalysisError", "ConvPreset", "ConvPlan", "MODE_3XTF32",
     "MODE_TF32", "MODE_F16X2", "WgradPlan", "FLAG_ACCUMULATE", "emit_driver", "select_topk", "model_us", "gemm_microkernel",
     "brgemm", "fill_input", "fill_filter", "version", "parse_nest", "NestInfo", "GemmPlan",
-    "model_stats", "ranker_train", "ranker_compare", "default_ranker_weights",
+    "model_stats", "ranker_train", "ranker_compare", "default_ranker_weights", "pack_input",
+    "pack_filter", "unpack_output", "set_machine", "load_measured_peaks",
 ]
 
 MODE_3XTF32 = 0
@@ -439,6 +440,50 @@ def brgemm(preset: ConvPreset, out_ptr: int, flt_ptrs, in_ptrs) -> None:
     _check(lib.brgemm_f32(ctypes.byref(d), out_ptr, fa, ia, n))
 
 
+def pack_input(preset: ConvPreset, nchw, out, c_logical: int = 0, stream=None) -> None:
+    """NCHW (c_logical channels) -> NCHW16c of `preset` (device buffers; channels >= c_logical
+    zero-filled): the blocked layout of the reference's input ArrayRef (presets.hpp:93-97)."""
+    d = preset.to_c()
+    _check(lib.conv_pack_input(ctypes.byref(d), _ptr(nchw), c_logical, _ptr(out), _stream_ptr(stream)))
+
+
+def pack_filter(preset: ConvPreset, kcrs, out, c_logical: int = 0, stream=None) -> None:
+    """KCRS (c_logical input channels) -> KCRS16c16k (presets.hpp:93-97 filter subscripts)."""
+    d = preset.to_c()
+    _check(lib.conv_pack_filter(ctypes.byref(d), _ptr(kcrs), c_logical, _ptr(out), _stream_ptr(stream)))
+
+
+def unpack_output(preset: ConvPreset, nkpq16k, out, stream=None) -> None:
+    """NKPQ16k (the reference's output ArrayRef) -> plain NKPQ."""
+    d = preset.to_c()
+    _check(lib.conv_unpack_output(ctypes.byref(d), _ptr(nkpq16k), _ptr(out), _stream_ptr(stream)))
+
+
+def set_machine(**consts: float) -> None:
+    """Selector machine constants (C ABI conv_select_set_machine): hbm_gbs, tf32_tflops,
+    clock_ghz, sms, l2_bytes."""
+    text = "\n".join(f"{k} {float(v)!r}" for k, v in consts.items())
+    _check(lib.conv_select_set_machine(text.encode()))
+
+
+def load_measured_peaks(path: str | None = None) -> dict | None:
+    """Feeds the pod's measured peaks (MEASURED_PEAKS.json: HBM copy GB/s, cuBLAS bf16
+    TFLOP/s -> tf32 = bf16 / 2) to the selector's model; returns what was set, or None when
+    the file is absent (the model keeps its built-in constants)."""
+    import json
+    import os
+    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        consts = {"hbm_gbs": float(j["hbm_gbs"]), "tf32_tflops": float(j["bf16_tflops"]) / 2.0}
+    except (OSError, KeyError, ValueError, TypeError):
+        return None
+    set_machine(**consts)
+    return consts
+
+
 def fill_input(preset: ConvPreset, seed: int, inp, c_logical: int = 0, img_begin: int = 0,
                img_count: int | None = None, stream=None) -> None:
     """Seeded uniform[-1,1) activations on the device (NCHW16c, logical-index keyed)."""
@@ -452,3 +497,6 @@ def fill_input(preset: ConvPreset, seed: int, inp, c_logical: int = 0, img_begin
 def fill_filter(preset: ConvPreset, seed: int, flt, c_logical: int = 0, stream=None) -> None:
     d = preset.to_c()
     _check(lib.conv_fill_filter(ctypes.byref(d), seed, c_logical, _ptr(flt), _stream_ptr(stream)))
+
+
+MACHINE = load_measured_peaks()  # this pod's peaks into the selector (None: built-in constants)

@@ -31,8 +31,7 @@ struct conv_plan {
   float* flt_pack = nullptr;   // prepacked K-major filter: hi (| lo for 3xTF32), see prepack
   bool b128 = false;           // filter rows of 32 channels (128 B, SWIZZLE_128B) vs 16 (64 B)
   bool ncat = false;           // 3xTF32 N-concat: prepacked rows [B_hi;B_lo] per N tile (ConvParams::ncat)
-  unsigned* absmax = nullptr;  // f16x2: |max| bits of [0] the filter, [1] / [2] alternating input slots
-  mutable int absmax_slot = 0;  // the input slot of the next call (the conv zeroes the other one)
+  unsigned* absmax = nullptr;  // f16x2: |max| bits of [0] the filter, [1] the call's input range
   // (c,s)-folded input (recipe fold:C, SURVEY §8d stem note): the layer has C <= 8
   // real input channels in one 16-channel block; G = 16 / C consecutive kw taps
   // are packed into one block, so the kernel runs the descriptor kd (kw' =
@@ -73,13 +72,15 @@ struct conv_plan {
     cudaEvent_t h2d[kSlots] = {}, conv[kSlots] = {}, d2h[kSlots] = {};
   };
   mutable HostPipe* pipe = nullptr;
-  // split-tile flags (tail split-K): kFlagRing regions of flag_cap ints, one
-  // region per launch epoch so stream-ordered launches never reset them
-  mutable int* tile_flags = nullptr;
-  mutable int64_t flag_cap = 0;
-  mutable int epoch = 0;
+  // split-K scratch (ConvParams::split_ctr / split_ws), sized at plan creation for the
+  // largest launch of the plan (img_count = nImg): ticket/done counters per split tile
+  // slot (zero between launches) and one 128 x bn partial per (slot, split)
+  int* split_ctr = nullptr;
+  float* split_ws = nullptr;
+  int64_t split_slots = 0;  // split tiles x CTAs per cluster the scratch holds
+  int split_k = 1;          // units per split tile the scratch holds
+  int64_t user_flt_elems = 0;  // the caller's filter (KCRS16c16k of d): nOfm*nIfm*kh*kw
 };
-constexpr int kFlagRing = 8;
 
 namespace psconv {
 namespace {
@@ -564,6 +565,78 @@ int grid_for(int64_t n) {
   return int(g);
 }
 
+// ---------------------------------------------------------------- launch geometry
+// Switches to the plan's device for the duration of an entry point (every C-ABI call that
+// launches or allocates), restoring the caller's current device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    int cur = 0;
+    CUDA_OK(cudaGetDevice(&cur));
+    if (cur != device) {
+      CUDA_OK(cudaSetDevice(device));
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: set once per
+// (kernel instantiation, device) -- the caller's current device is the plan's (DeviceGuard).
+struct SmemAttr {
+  std::mutex mu;
+  uint64_t done = 0;  // bit d: set on device d
+  template <typename K>
+  cudaError_t ensure(K kernel, int bytes, int device) {
+    std::lock_guard<std::mutex> g(mu);
+    if (device < 64 && ((done >> device) & 1u)) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && device < 64) done |= uint64_t(1) << device;
+    return e;
+  }
+};
+
+// Output-tile groups of a launch over img_count images (conv_fwd_sm100's persistent
+// schedule: M tiles of the pixel box, CS of them per cluster, times the N tiles).
+int64_t launch_groups(const conv_plan* P, int64_t img_count) {
+  const conv_desc& d = P->kd;
+  const Schedule& s = P->sched;
+  const int64_t mt = ((d.ofw + s.qb - 1) / s.qb) * ((d.ofh + s.pb - 1) / s.pb) * ((img_count + s.nb - 1) / s.nb);
+  return (mt + s.cs - 1) / s.cs * (d.nOfm / s.bn);
+}
+
+// Pipeline stages per whole tile (halo mode: one B stage per (channel group, tap)).
+int launch_nst(const conv_plan* P) {
+  const conv_desc& d = P->kd;
+  const Schedule& s = P->sched;
+  const int Cb = int(d.nIfm / 16);
+  if (s.halo) return (Cb % s.kps == 0 ? Cb / s.kps : Cb) * int(d.kh * d.kw);
+  return (Cb * int(d.kh * d.kw) + s.kps - 1) / s.kps;
+}
+
+// Split-K work units (recipe ks:S): the tail split cuts only the tiles of the last, partial
+// wave into ksplit stage ranges; kt:1 (split_all) cuts every tile. Fused epilogues (ReLU
+// needs the whole sum) and halo mode never split.
+struct SplitGeom {
+  int ksplit, split_stages, split_from, units;
+};
+SplitGeom split_geom(const conv_plan* P, int groups, int nst, bool fused) {
+  const Schedule& s = P->sched;
+  SplitGeom g{};
+  g.ksplit = (fused || s.halo) ? 1 : std::max(1, s.ksplit);
+  g.split_stages = (nst + g.ksplit - 1) / g.ksplit;
+  g.ksplit = (nst + g.split_stages - 1) / g.split_stages;  // no empty units
+  const int clusters = P->num_sms / s.cs;
+  g.split_from = g.ksplit > 1 ? (s.split_all ? 0 : groups / clusters * clusters) : groups;
+  if (g.split_from == groups) g.ksplit = 1;  // no partial wave: nothing to split
+  g.units = g.split_from + (groups - g.split_from) * g.ksplit;
+  return g;
+}
+
 // ---------------------------------------------------------------- launch
 template <int BN, bool SPLIT3, int CS, int EPI, int EG, bool F16>
 void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a,
@@ -573,13 +646,8 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
   } else {
     constexpr bool PAIR = CS == 2;
     using Cfg = KernelCfg<BN, SPLIT3, PAIR, EG>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG, F16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    });
-    CUDA_OK(attr_err);
+    static SmemAttr attr_once;  // per instantiation, per device
+    CUDA_OK(attr_once.ensure(conv_fwd_sm100<BN, SPLIT3, PAIR, EPI, EG, F16>, Cfg::kSmemBytes, P->device));
     const int max_clusters = P->num_sms / CS;
     const int clusters = prm.groups < max_clusters ? prm.groups : max_clusters;
     cudaLaunchConfig_t cfg{};
@@ -658,13 +726,8 @@ void dispatch_cs(int cs, int bn, const conv_plan* P, const ConvParams& prm, cons
 template <int BN, bool SPLIT3>
 void launch_pp_kernel(const conv_plan* P, const PpParams& prm, const CUtensorMap& ta, const CUtensorMap& tout,
                       int smem, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(conv_pp_sm100<BN, SPLIT3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024);
-  });
-  CUDA_OK(attr_err);
+  static SmemAttr attr_once;  // per instantiation, per device
+  CUDA_OK(attr_once.ensure(conv_pp_sm100<BN, SPLIT3>, 227 * 1024, P->device));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(prm.groups, P->num_sms));
   cfg.blockDim = dim3(PpCfg<BN, SPLIT3>::kThreads);
@@ -764,32 +827,15 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   const bool split3 = split_mode(P->mode);  // 3xTF32 / f16x2: split-stage geometry
   const bool f16 = P->mode == PSCONV_MODE_F16X2;
   unsigned* amax_a = nullptr;
-  unsigned* amax_reset = nullptr;
   if (f16) {
-    // |max| of the input range -> the A scale (read by the kernel after griddepcontrol.wait).
-    // Two slots alternate: this call's conv zeroes the previous call's slot, so no memset
-    // launch per call; PDL chains the pass to the previous kernel. (Under graph capture
-    // the slot is fixed, so it is cleared by a captured memset instead.)
+    // |max| of the input range -> the A scale (read by the kernel after griddepcontrol.wait),
+    // in the plan's input slot, cleared first by every call (eager or captured alike: a
+    // replayed graph and a later eager call never see each other's value)
     const int64_t n = img_count * Cb * H * W * 16;
-    amax_a = P->absmax + 1 + P->absmax_slot;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CUDA_OK(cudaStreamIsCapturing(st, &cap));
-    if (cap == cudaStreamCaptureStatusActive) {
-      CUDA_OK(cudaMemsetAsync(amax_a, 0, sizeof(unsigned), st));
-    } else {
-      amax_reset = P->absmax + 1 + (1 - P->absmax_slot);
-      P->absmax_slot ^= 1;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid_for(n / 4));
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CUDA_OK(cudaLaunchKernelEx(&cfg, absmax_kernel, in, n, amax_a));
+    amax_a = P->absmax + 1;
+    CUDA_OK(cudaMemsetAsync(amax_a, 0, sizeof(unsigned), st));
+    absmax_kernel<<<grid_for(n / 4), 256, 0, st>>>(in, n, amax_a);
+    CUDA_OK(cudaGetLastError());
   }
 
   // A: input viewed as [img_count][Cb][H][W][16] from the range's first image
@@ -914,7 +960,6 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.egroups = s.egroups;
     prm.absmax_a = amax_a;
     prm.absmax_b = P->absmax;
-    prm.absmax_reset = amax_reset;
     prm.ncat = P->ncat ? 1 : 0;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
       // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum
@@ -946,48 +991,21 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   }
   const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;
   prm.chunk_stages = (chunk + s.kps - 1) / s.kps;
-  // split-K units (not with a fused epilogue: ReLU needs the whole sum)
-  // Only the tiles of the last partial wave are split (tail split): the first
-  // (groups / clusters) * clusters tiles run whole, each later tile becomes
-  // ksplit units of split_stages stages.
-  prm.ksplit = (bias || (flags & PSCONV_FLAG_RELU) || s.halo) ? 1 : std::max(1, s.ksplit);
-  prm.split_stages = (prm.nst + prm.ksplit - 1) / prm.ksplit;
-  prm.ksplit = (prm.nst + prm.split_stages - 1) / prm.split_stages;  // no empty units
   prm.tile_chunks = (prm.nst + prm.chunk_stages - 1) / prm.chunk_stages;
   {
-    const int clusters = P->num_sms / s.cs;
-    // (kt:1: every tile split, the output zeroed first and every partial reduce-added;
-    // measured faster than the tail split on some 3xTF32 layers at ~1.3 waves)
-    prm.split_from = prm.ksplit > 1 ? (s.split_all ? 0 : prm.groups / clusters * clusters) : prm.groups;
-    if (prm.split_from == prm.groups) prm.ksplit = 1;  // no partial wave: nothing to split
-    prm.units = prm.split_from + (prm.groups - prm.split_from) * prm.ksplit;
-    prm.tile_flags = nullptr;
-    prm.epoch = 0;
-    if (s.split_all && prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE)) {
-      CUDA_OK(cudaMemsetAsync(out, 0, size_t(img_count) * Kb * Pp * Q * 16 * sizeof(float), st));
-      flags |= PSCONV_FLAG_ACCUMULATE;
-    }
-    if (prm.ksplit > 1 && !(flags & PSCONV_FLAG_ACCUMULATE)) {
-      const int64_t need = int64_t(prm.groups - prm.split_from) * s.cs;
-      if (need > P->flag_cap) {
-        if (P->tile_flags) {
-          CUDA_OK(cudaStreamSynchronize(st));
-          CUDA_OK(cudaFree(P->tile_flags));
-        }
-        CUDA_OK(cudaMalloc(&P->tile_flags, size_t(need) * kFlagRing * sizeof(int)));
-        CUDA_OK(cudaMemsetAsync(P->tile_flags, 0, size_t(need) * kFlagRing * sizeof(int), st));
-        P->flag_cap = need;
-        P->epoch = 0;
-      }
-      P->epoch = P->epoch == INT32_MAX ? 1 : P->epoch + 1;
-      prm.epoch = P->epoch;
-      prm.tile_flags = P->tile_flags + (P->epoch % kFlagRing) * P->flag_cap;
-      // CUDA-graph capture: the epoch is baked into the captured kernel, so every
-      // replay must start from cleared flags -- capture a reset of this region
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      CUDA_OK(cudaStreamIsCapturing(st, &cap));
-      if (cap == cudaStreamCaptureStatusActive)
-        CUDA_OK(cudaMemsetAsync(prm.tile_flags, 0, size_t(P->flag_cap) * sizeof(int), st));
+    // split-K units (not with a fused epilogue, whose ReLU needs the whole sum; not halo)
+    const SplitGeom sg = split_geom(P, prm.groups, prm.nst, bias != nullptr || (flags & PSCONV_FLAG_RELU));
+    prm.ksplit = sg.ksplit;
+    prm.split_stages = sg.split_stages;
+    prm.split_from = sg.split_from;
+    prm.units = sg.units;
+    prm.split_ctr = nullptr;
+    prm.split_ws = nullptr;
+    if (prm.ksplit > 1) {  // scratch sized by conv_plan_create for img_count = nImg
+      if (int64_t(prm.groups - prm.split_from) * s.cs > P->split_slots || prm.ksplit > P->split_k)
+        throw RuntimeError("internal: split-K scratch smaller than the launch");
+      prm.split_ctr = P->split_ctr;
+      prm.split_ws = P->split_ws;
     }
   }
   for (int i = 0; i < 3; ++i) prm.kord[i] = s.kord[i];
@@ -1113,22 +1131,45 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
     P->ncat = mode == PSCONV_MODE_3XTF32 && s.bn <= 64 && !s.pp && s.cs == 1 &&
               std::getenv("PSCONV_NO_NCAT") == nullptr;
     P->flt_elems = kd.nOfm * kd.nIfm * kd.kh * kd.kw;
+    P->user_flt_elems = d.nOfm * d.nIfm * d.kh * d.kw;
+    if (!s.pp) {
+      // split-K scratch for the largest launch (all nImg images): the tail split cuts at
+      // most one partial wave (< clusters tiles), kt:1 every tile
+      const int64_t groups = launch_groups(P, d.nImg);
+      if (groups >= (int64_t(1) << 31)) {
+        delete P;
+        throw ConfigError("too many tiles");
+      }
+      const SplitGeom sg = split_geom(P, int(groups), launch_nst(P), false);
+      if (sg.ksplit > 1) {
+        const int64_t clusters = P->num_sms / s.cs;
+        const int64_t tiles = s.split_all ? groups : std::min<int64_t>(groups, clusters);
+        P->split_slots = tiles * s.cs;
+        P->split_k = sg.ksplit;
+      }
+    }
     {
-      int prev = 0;
-      cudaGetDevice(&prev);
-      cudaSetDevice(device);
+      DeviceGuard guard(device);
       const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
       cudaError_t e = cudaMalloc(&P->flt_pack, copies * P->flt_elems * sizeof(float));
-      if (e == cudaSuccess) e = cudaMalloc(&P->absmax, 3 * sizeof(unsigned));
-      if (e == cudaSuccess) e = cudaMemset(P->absmax, 0, 3 * sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMalloc(&P->absmax, 2 * sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMemset(P->absmax, 0, 2 * sizeof(unsigned));
       if (e == cudaSuccess && fold) e = cudaMalloc(&P->wfold, P->flt_elems * sizeof(float));
       if (e == cudaSuccess && fold)
         e = cudaMalloc(&P->xfold, size_t(kd.nImg) * fold_phases * kd.ifh * kd.ifw * 16 * sizeof(float));
-      cudaSetDevice(prev);
+      if (e == cudaSuccess && P->split_slots > 0) {
+        e = cudaMalloc(&P->split_ctr, size_t(P->split_slots) * 2 * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemset(P->split_ctr, 0, size_t(P->split_slots) * 2 * sizeof(int));
+        if (e == cudaSuccess)
+          e = cudaMalloc(&P->split_ws, size_t(P->split_slots) * P->split_k * 128 * s.bn * sizeof(float));
+      }
       if (e != cudaSuccess) {
         cudaFree(P->flt_pack);
         cudaFree(P->absmax);
         cudaFree(P->wfold);
+        cudaFree(P->xfold);
+        cudaFree(P->split_ctr);
+        cudaFree(P->split_ws);
         delete P;
         throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
       }
@@ -1258,6 +1299,7 @@ int conv_bwd_weight(const conv_plan* P, const float* x, const float* dy, float* 
   return guarded([&] {
     if (!P || !x || !dy || !dw) throw ConfigError("null argument");
     if (!P->bwd_weight) throw ConfigError("not a backward-weight plan (conv_plan_create_bwd_weight)");
+    DeviceGuard guard(P->device);
     const conv_desc& t = P->d;  // the role-swapped conv
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int N = int(t.nIfm), C = int(t.nImg), Kb = int(t.nOfm / 16);
@@ -1303,7 +1345,8 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->flt_pack);
     cudaFree(p->wfold);
     cudaFree(p->xfold);
-    cudaFree(p->tile_flags);
+    cudaFree(p->split_ctr);
+    cudaFree(p->split_ws);
     cudaFree(p->absmax);
     cudaFree(p->wg_x);
     cudaFree(p->wg_dy);
@@ -1355,6 +1398,8 @@ int conv_fwd_ex(const conv_plan* P, const float* in, const float* flt, float* ou
          reinterpret_cast<uintptr_t>(out)) & 15)
       throw ConfigError("tensor pointers must be 16-byte aligned");
     if (img_count == 0) return;
+    if (P->bwd_weight) throw ConfigError("a backward-weight plan runs through conv_bwd_weight");
+    DeviceGuard guard(P->device);
     const int64_t in_img = d.nIfm * d.ifh * d.ifw, out_img = d.nOfm * d.ofh * d.ofw;
     launch_range(P, in + img_begin * in_img, flt, out + img_begin * out_img, img_count,
                  static_cast<cudaStream_t>(stream), flags, bias);
@@ -1370,6 +1415,7 @@ int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
   return guarded([&] {
     if (!P || !flt) throw ConfigError("null argument");
     if (reinterpret_cast<uintptr_t>(flt) & 15) throw ConfigError("filter must be 16-byte aligned");
+    DeviceGuard guard(P->device);
     launch_prepack(P, flt, static_cast<cudaStream_t>(stream));
     P->prepacked = true;
   });
@@ -1387,10 +1433,9 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     if (img_begin < 0 || img_count < 0 || img_begin + img_count > d.nImg)
       throw ConfigError("image range outside nImg");
     if (img_count == 0) return;
+    if (P->bwd_weight) throw ConfigError("a backward-weight plan runs through conv_bwd_weight");
     const int64_t in_img = d.nIfm * d.ifh * d.ifw, out_img = d.nOfm * d.ofh * d.ofw;
-    int prev = 0;
-    CUDA_OK(cudaGetDevice(&prev));
-    CUDA_OK(cudaSetDevice(P->device));
+    DeviceGuard guard(P->device);
     if (!P->pipe) {  // ~32 MB of input per chunk, kSlots buffers
       auto* h = new conv_plan::HostPipe();
       P->pipe = h;
@@ -1404,7 +1449,9 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
         CUDA_OK(cudaEventCreateWithFlags(&h->conv[i], cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&h->d2h[i], cudaEventDisableTiming));
       }
-      CUDA_OK(cudaMalloc(&h->dflt, P->flt_elems * sizeof(float)));
+      // the caller's filter (KCRS16c16k of d): for a fold:C plan this is the unfolded
+      // filter, larger than the folded operand count flt_elems
+      CUDA_OK(cudaMalloc(&h->dflt, P->user_flt_elems * sizeof(float)));
       CUDA_OK(cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&h->flt, cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&h->end, cudaEventDisableTiming));
@@ -1419,7 +1466,7 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     CUDA_OK(cudaStreamWaitEvent(h->sout, h->start, 0));
     unsigned kflags = flags;
     if (!prepacked) {
-      CUDA_OK(cudaMemcpyAsync(h->dflt, h_flt, P->flt_elems * sizeof(float), cudaMemcpyHostToDevice, h->sin));
+      CUDA_OK(cudaMemcpyAsync(h->dflt, h_flt, P->user_flt_elems * sizeof(float), cudaMemcpyHostToDevice, h->sin));
       CUDA_OK(cudaEventRecord(h->flt, h->sin));
       CUDA_OK(cudaStreamWaitEvent(cs, h->flt, 0));
     }
@@ -1466,7 +1513,6 @@ int conv_fwd_host(const conv_plan* P, const float* h_in, const float* h_flt, flo
     }
     CUDA_OK(cudaEventRecord(h->end, h->sout));
     CUDA_OK(cudaStreamWaitEvent(cs, h->end, 0));
-    CUDA_OK(cudaSetDevice(prev));
   });
 }
 

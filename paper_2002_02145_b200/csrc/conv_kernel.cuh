@@ -20,7 +20,8 @@
 //               (filter prepacked K-major [C*R*S/16][K][16c])
 //   warp 1      TMEM owner; MMA issuer (single CTA, or the pair's leader);
 //               in the pair's second CTA: forwards "stage ready" to the leader
-//   warps 2-5   epilogue: tcgen05.ld -> registers -> st.global.v4 (NKPQ16k)
+//   warps 2-5   epilogue: tcgen05.ld -> registers -> SW64 staging tiles in smem ->
+//               one TMA tensor store (or reduce-add for `+=`) per 16-channel block (NKPQ16k)
 //   warps 6-9   (3xTF32 only) splitter: A -> lo = A - tf32(A) in shared memory
 //
 // PAIR (cluster of 2, tcgen05.mma.cta_group::2, M = 256): the two SMs of a
@@ -92,13 +93,21 @@ struct ConvParams {
   int a_lo_off, b_off, b_lo_off;  // region offsets inside a stage
   int chunk_stages;               // stages per TMEM accumulation chunk
   int ksplit;                     // split-K: work units per tile (reduction split into ksplit
-                                  // stage ranges of split_stages, partial sums reduce-added
-                                  // into the pre-zeroed output); 1 = whole tiles
+                                  // stage ranges of split_stages); 1 = whole tiles
   int split_stages;
   int split_from;                 // tiles [0, split_from) are whole units; later tiles split
   int units;                      // split_from + (groups - split_from) * ksplit
-  int* tile_flags;                // per split tile: the first unit's stores landed (== epoch)
-  int epoch;                      // launch counter of the plan (flags need no reset)
+  // Split tiles combine deterministically without any CTA waiting on a CTA that may not
+  // be resident: every unit of a split tile takes a ticket (split_ctr[2t], relaxed atomic)
+  // when its partial is ready; the first ksplit-1 units write their partial to their slot
+  // of split_ws and count themselves done (split_ctr[2t+1], release); the last ticket
+  // holder -- whose peers have all taken tickets, i.e. are running their epilogue --
+  // waits for the done count, adds the partials in split order ((p0 + p1) + p2 ...) and
+  // stores the tile once, then zeroes both counters for the next launch. The workspace and
+  // counters are plan-owned (sized at conv_plan_create); no output memset, no atomics on
+  // the output, bitwise reproducible.
+  int* split_ctr;                 // [2 * split tiles * CS] {tickets, done}
+  float* split_ws;                // [split tiles * CS][ksplit][128 x BN] partials
   int tile_chunks;                // accumulation chunks of a whole tile (ksplit == 1)
   int kord[3];                    // stage order outer->inner over {0 ifm group, 1 kj, 2 ki}
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
@@ -110,8 +119,7 @@ struct ConvParams {
                                   // the epilogue adds D1 + D2. 45 + 64 instead of 3 x 45
                                   // cycles per K half at BN = 64 (tools/probe_mma_pair.cu)
   const unsigned* absmax_a;        // f16x2: |max| bits of the input range (power-of-two
-  const unsigned* absmax_b;        // operand scales; the epilogue unscales) and the filter;
-  unsigned* absmax_reset;          // the other input slot, zeroed for the next call
+  const unsigned* absmax_b;        // operand scales; the epilogue unscales) and the filter
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
@@ -698,6 +706,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   uint64_t* acc_empty = acc_full + 2;            // chunk accumulator drained [kAccBufs] (4 warps x CS)
   uint64_t* aslot_empty = acc_empty + 2;         // TMEM A slot consumed by the MMA [kMaxStages]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aslot_empty + kMaxStages);
+  volatile int* split_word = reinterpret_cast<volatile int*>(tmem_slot + 1);  // split-K ticket broadcast
 
   const int warp = threadIdx.x >> 5;
   const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
@@ -1061,13 +1070,15 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
       const TileCoord tc = decode_group(p, un.g, rank, CS);
       const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
       const int kb0 = tc.tk * (BN / 16);
-      // split tile (no `+=`): its first unit stores and then raises the tile's
-      // flag; the other units reduce-add once the flag shows this launch's epoch
-      // (they wait only on smaller unit indices of co-resident persistent CTAs)
-      const bool flagged = EPI == kEpiSplit && un.sp >= 0 && !p.accumulate;
-      const bool reduce = p.accumulate || (EPI == kEpiSplit && un.sp > 0);
-      int* const flag = flagged ? p.tile_flags + (un.g - p.split_from) * CS + rank : nullptr;
-      bool wait_flag = flagged && un.sp > 0;
+      // split tile: ticket -> write the partial to the workspace, or (last ticket)
+      // combine all partials in split order and store the tile (ConvParams::split_ctr)
+      const bool split = EPI == kEpiSplit && un.sp >= 0 && tc.live;
+      const int stile = split ? (un.g - p.split_from) * CS + rank : 0;
+      int* const ctr = split ? p.split_ctr + 2 * stile : nullptr;
+      float4* const ws = split ? reinterpret_cast<float4*>(p.split_ws) + static_cast<long long>(stile) * p.ksplit * (32 * BN)
+                               : nullptr;
+      bool fixer = false;
+      const bool reduce = p.accumulate != 0;  // `+=`: TMA reduce-add of the finished tile
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -1079,6 +1090,20 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
 #endif
         if (ev && store_thread && cit == 0) ev[4] = clock64();
         ptx::tc_fence_after();
+        if (EPI == kEpiSplit && split && last) {
+          // the unit's partial is complete: take a ticket; the last holder waits until the
+          // other ksplit-1 units (all past their own ticket, so running) have written theirs
+          if (threadIdx.x == 64) {
+            const int t = ptx::atom_add_relaxed_gpu(ctr, 1);
+            if (t == p.ksplit - 1)
+              while (ptx::ld_acquire_gpu(ctr + 1) != p.ksplit - 1) {
+              }
+            *split_word = t;
+          }
+          ptx::named_bar(3, 128 * kGroups);
+          fixer = *split_word == p.ksplit - 1;
+          if (fixer) ptx::fence_acq_rel_gpu();
+        }
         const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * Cfg::kAccW);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
 #pragma unroll 1
@@ -1122,6 +1147,31 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
 #pragma unroll
               for (int i = 0; i < DW; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * out_scale);
             }
+            if constexpr (EPI == kEpiSplit) {
+              if (split) {
+                // workspace slot layout per round: [DW/4][128 rows] float4s (coalesced per warp)
+                const int wbase = j * (DW / 4) * 128 + row;
+                // every unit writes its partial (the last ticket too: its sum then reads only
+                // the workspace, in split order, and its registers stay free)
+#pragma unroll
+                for (int c4 = 0; c4 < DW / 4; ++c4)
+                  __stcg(ws + un.sp * (32 * BN) + wbase + c4 * 128,
+                         make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
+                                     __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3])));
+                if (!fixer) continue;  // no staging, no store
+#pragma unroll 1
+                for (int sp = 0; sp < p.ksplit; ++sp) {  // v accumulates (own partial re-read)
+#pragma unroll
+                  for (int c4 = 0; c4 < DW / 4; ++c4) {
+                    const float4 x = __ldcg(ws + sp * (32 * BN) + wbase + c4 * 128);
+                    const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                      v[4 * c4 + e] = __float_as_uint(sp == 0 ? xs[e] : __uint_as_float(v[4 * c4 + e]) + xs[e]);
+                  }
+                }
+              }
+            }
             if constexpr (EPI == kEpiFused) {
             if (p.bias != nullptr) {
               const float* bj = p.bias + tc.tk * BN + j * DW;
@@ -1155,13 +1205,6 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
             }
             ptx::fence_proxy_async_smem();
             ptx::named_bar(ebar, 128);
-            if (EPI == kEpiSplit && store_thread && wait_flag) {
-              const uint64_t t0 = ptx::globaltimer();
-              while (ptx::ld_acquire_gpu(flag) != p.epoch)
-                if (ptx::globaltimer() - t0 > 10000000000ull) __trap();  // 10 s: not co-resident
-              ptx::fence_proxy_async_global();
-              wait_flag = false;
-            }
             if (store_thread && !(p.debug & 4)) {
 #pragma unroll
               for (int blk = 0; blk < kBlk; ++blk) {
@@ -1187,13 +1230,18 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         }
         __syncwarp();
       }
-      if (EPI == kEpiSplit && flagged && un.sp == 0) {  // the tile's first partial is in memory
-        if (store_thread) {
-          ptx::bulk_wait_all();
-          ptx::fence_proxy_async_global();
+      if (EPI == kEpiSplit && split) {
+        if (!fixer) {  // partial written by every epilogue thread -> count this unit done
+          __threadfence();
+          ptx::named_bar(3, 128 * kGroups);
+          if (threadIdx.x == 64) ptx::red_release_gpu_add(ctr + 1, 1);
+        } else {  // tile stored; reset the counters for the next launch (stream-ordered)
+          ptx::named_bar(3, 128 * kGroups);
+          if (threadIdx.x == 64) {
+            ctr[0] = 0;
+            ctr[1] = 0;
+          }
         }
-        if (kGroups > 1) ptx::named_bar(3, 128 * kGroups);  // both groups' stores landed
-        if (threadIdx.x == 64) ptx::st_release_gpu(flag, p.epoch);
       }
     }
     if (ev && store_thread) ev[5] = clock64();  // last store issued
@@ -1207,7 +1255,6 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     if constexpr (F16) {
       ptx::griddep_wait();  // the input |max| comes from the preceding kernel
       a_scale = pow2_scale(*p.absmax_a);
-      if (tid == 0 && p.absmax_reset) *p.absmax_reset = 0u;  // the previous call's slot
     }
     int stage = 0;
     uint32_t phase = 0;

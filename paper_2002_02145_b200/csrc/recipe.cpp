@@ -387,8 +387,10 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   if (s.chunk > ksteps) s.chunk = ksteps;
   plan_stages(d, s, mode, r.kg);
   // Tail split-K (wave quantisation): the tiles of the last partial wave are
-  // split into ks stage ranges run as separate work units (the first stores,
-  // the others reduce-add once it landed). Auto: the ks in 1..8 (>= 4 stages
+  // split into ks stage ranges run as separate work units (each writes its
+  // partial to the plan's workspace; the last to finish adds them in split order
+  // and stores the tile: deterministic, no inter-CTA waits on non-running CTAs,
+  // conv_kernel.cuh ConvParams::split_ctr). Auto: the ks in 1..8 (>= 4 stages
   // each) with the lowest modelled time, charging the per-unit refill/drain
   // and the extra output traffic (select.cpp); a split must win by 3%.
   {

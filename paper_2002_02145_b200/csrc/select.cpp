@@ -20,6 +20,8 @@
 #include <cstring>
 #include <map>
 #include <set>
+#include <sstream>
+#include <string>
 #include <tuple>
 
 #include "internal.hpp"
@@ -28,9 +30,10 @@ namespace psconv {
 
 namespace {
 
-// B200 machine model. Peaks: MEASURED_PEAKS.json (HBM copy 6538.9 GB/s,
-// bf16 1622.7 TFLOP/s -> tf32 811.4 derived); the rest are modelling
-// constants to be refined from measurements.
+// B200 machine model. Peaks: defaults from an earlier pod's MEASURED_PEAKS.json;
+// the Python layer loads this pod's file at import (conv_select_set_machine:
+// HBM copy GB/s, tf32 = bf16 / 2); the rest are modelling constants (DESIGN.md
+// §4) fitted to r01 measurements.
 struct Machine {
   double sms = 148;
   double hbm_gbs = 6538.9;
@@ -45,7 +48,7 @@ struct Machine {
   double drain_round_trip_cyc = 100.0;  // one 32-column TMEM drain step
   double row_requests_per_cycle = 0.75;  // TMA rows per cycle per SM, all SMs loading
 };
-const Machine kB200{};
+Machine kB200{};  // set once, before any ranking (conv_select_set_machine)
 
 struct Geo {
   int64_t N, C, K, H, W, P, Q, R, S, Cb, Kb;
@@ -202,10 +205,11 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   const int64_t waves = s.split_all && ks > 1 ? 0 : groups / clusters, rem = groups - waves * clusters;
   const int kt = rem > 0 ? ks : 1;
   const double tile_cyc = double(ksteps) * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
-  // (a split unit also refills the pipeline (~1500 cycles) and drains a whole
-  // output tile that the later units wait for (128 x BN fp32 at ~64 B/cycle);
-  // fitted to the r01 tail-split A/B timings of cfg3 / cfg5 / l3 / l4)
-  const double split_cyc = 1500.0 + 128.0 * s.bn * 4.0 / 64.0;
+  // (a split unit also refills the pipeline (~1500 cycles) and writes its
+  // 128 x BN fp32 partial to the workspace; the last unit of the tile then reads
+  // all kt partials back in split order before its store (~64 B/cycle each way;
+  // r01 A/B fit of the refill, conv_kernel.cuh ConvParams::split_ctr)
+  const double split_cyc = 1500.0 + (1.0 + ks) * 128.0 * s.bn * 4.0 / 64.0;
   const double unit_cyc = double(ksteps) / kt * kstep_cyc +
                           (drain_exposed ? nchunks / kt * drain_cyc : drain_cyc) + (kt > 1 ? split_cyc : 0.0);
   double tail_units = std::ceil(double(rem) * kt / clusters);
@@ -232,9 +236,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   double in_reads = 1.0;
   if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
   b.hbm_bytes = in_b * in_reads + flt_b + out_b;
-  // split-K: every extra unit of a split tile reduce-adds its partial (in L2
-  // while the tile's lines stay resident, partly in HBM)
-  if (kt > 1) b.hbm_bytes += out_b * double(rem) / groups * (kt - 1) + (s.split_all ? out_b : 0.0);
+  // split-K: every unit of a split tile writes its partial to the workspace and the
+  // last reads them all back (mostly in L2, partly written back to HBM)
+  if (kt > 1) b.hbm_bytes += 0.5 * out_b * double(s.split_all ? groups : rem) / groups * kt;
   b.us_hbm = b.hbm_bytes / (0.8 * m.hbm_gbs * 1e9) * 1e6;  // ~80% of copy bandwidth sustained
   b.us_smem = 0;
   b.us_epi = 128.0 * s.bn * 4.0 / (64.0 * 1.8e9) * 1e6;  // one trailing tile's drain
@@ -318,6 +322,33 @@ int conv_select_topk(const conv_desc* d_in, int mode, int k, char* buf, size_t l
     std::memcpy(buf, txt.c_str(), txt.size() + 1);
   });
   return rc == PSCONV_OK ? written : -rc;
+}
+
+int conv_select_set_machine(const char* text) {
+  return guarded([&] {
+    if (!text) throw ConfigError("null machine text");
+    Machine m = kB200;
+    std::istringstream in(text);
+    std::string line;
+    int lineno = 0;
+    while (std::getline(in, line)) {
+      ++lineno;
+      const size_t hash = line.find('#');
+      if (hash != std::string::npos) line.resize(hash);
+      std::istringstream ls(line);
+      std::string key;
+      double v = 0;
+      if (!(ls >> key)) continue;
+      if (!(ls >> v) || !(v > 0)) throw ConfigError("machine line " + std::to_string(lineno) + ": expected '<key> <positive number>'");
+      if (key == "hbm_gbs") m.hbm_gbs = v;
+      else if (key == "tf32_tflops") m.tf32_tflops = v;
+      else if (key == "clock_ghz") m.clock_ghz = v;
+      else if (key == "sms") m.sms = v;
+      else if (key == "l2_bytes") m.l2_bytes = v;
+      else throw ConfigError("machine line " + std::to_string(lineno) + ": unknown key '" + key + "'");
+    }
+    kB200 = m;
+  });
 }
 
 double conv_model_us(const conv_desc* d_in, int mode, const char* recipe) {

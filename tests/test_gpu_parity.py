@@ -370,8 +370,9 @@ def test_backward_data_rejects_strided():
     ("conv:2,32,48,9,9,3,3,1,1,16,1,1,9,9", 48, "gpu=bn:32,box:9x9x1,kg:4,ks:2"),
 ])
 def test_split_k(conv, c_log, recipe, mode):
-    """Split-K work units: each tile's reduction in ks stage ranges, partials reduce-added
-    into the zeroed output (also with the pair, TMEM-A and partial-stage paths)."""
+    """Split-K work units: each tile's reduction in ks stage ranges, the partials combined
+    in split order by the tile's last unit (also with the pair, TMEM-A and partial-stage
+    paths)."""
     n = ps.ConvPreset.parse(conv).nImg
     _check("ks", conv, c_log, 16, mode, n, recipe)
     if mode == "tf32":
@@ -390,8 +391,8 @@ TAIL = "conv:8,64,64,56,56,3,3,1,1,16,1,1,56,56"  # 196 tiles of 8x8x2 px: 1 wav
     "gpu=bn:64,box:8x8x2,ks:3,kt:1",  # every tile split: zeroed output, all partials added
 ])
 def test_tail_split(recipe, mode):
-    """Tail split-K: only the last partial wave's tiles are split; a split tile's first
-    unit stores, the others reduce-add after its flag (no output memset)."""
+    """Tail split-K: only the last partial wave's tiles are split; every unit writes its
+    partial to the plan workspace and the last one adds them and stores (no output memset)."""
     if "cl:2" in recipe and mode == "3xtf32":
         pytest.skip("the CTA pair is TF32-only")
     _check("tail", TAIL, 64, 16, mode, 8, recipe)
@@ -399,8 +400,8 @@ def test_tail_split(recipe, mode):
 
 @pytest.mark.gpu
 def test_tail_split_relaunch():
-    """Flags are epoch-tagged in a ring: repeated launches of one plan on one stream stay
-    correct with no reset (each launch overwrites a NaN-filled output)."""
+    """The split tiles' ticket counters return to zero at the end of every launch: repeated
+    launches of one plan on one stream stay correct (each overwrites a NaN-filled output)."""
     p = ps.ConvPreset.parse(TAIL)
     sx, sw = seeds(16)
     dev = torch.device("cuda:0")
@@ -523,12 +524,12 @@ def test_parity_plane_accumulate_and_range():
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode,recipe", [
     ("tf32", "gpu=bn:64,box:8x8x2"),
-    ("3xtf32", "gpu=bn:64,box:8x8x2,ks:3"),          # tail split-K: flags reset per replay
+    ("3xtf32", "gpu=bn:64,box:8x8x2,ks:3"),          # tail split-K: counters back at zero per replay
     ("tf32", "gpu=bn:64,box:8x8x2,ks:2,cl:2"),
 ])
 def test_cuda_graph_replay(mode, recipe):
-    """ConvPlan.graph(): the captured launch (PDL edge, split-K flag reset) replays to the same
-    result as forward(), several times in a row."""
+    """ConvPlan.graph(): the captured launch (PDL edge) replays to the same result as forward(),
+    bit for bit, several times in a row (split-K combines partials in a fixed order)."""
     p = ps.ConvPreset.parse("conv:40,64,64,16,16,3,3,1,1,16,1,1,16,16")
     sx, sw = seeds(21)
     dev = torch.device("cuda:0")
@@ -547,7 +548,7 @@ def test_cuda_graph_replay(mode, recipe):
         g.replay()
         torch.cuda.synchronize()
         assert torch.isfinite(y).all()
-        assert oracle.rel_l2(y.cpu().numpy(), y0.cpu().numpy()) <= TOL[mode]
+        assert torch.equal(y, y0), "graph replay differs from forward()"
 
 
 @pytest.mark.gpu

@@ -106,3 +106,39 @@ def test_stem_channel_padding_zero():
     w = oracle.fill_filter(p, 2, c_logical=3)
     assert np.all(x[..., 3:] == 0) and np.any(x[..., :3] != 0)
     assert np.all(w[:, :, :, :, 3:, :] == 0)
+
+
+# ------------------------------------------------------- BASELINE-size pins (slices.json)
+SLICES = json.load(open(os.path.join(GOLDEN, "slices.json")))
+
+
+def _slice(entry):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("make_slices", os.path.join(GOLDEN, "make_slices.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    return mk, mk.slice_inputs(entry["conv"], entry["c_logical"], entry["cfg_id"], entry["image"],
+                                entry["ofm_blocks"])
+
+
+@pytest.mark.parametrize("entry", SLICES, ids=lambda e: e["name"])
+def test_oracle_bit_exact_vs_reference_ir_at_baseline_size(entry):
+    """One-image slices of cfg1/2/3/5 and the stem at full channel / spatial size: the oracle's
+    output is bit-identical to the reference IR's (sha256 committed by make_slices.py from
+    ConvPreset::build + for_each_iteration), and within 1e-6 of float64."""
+    mk, (s, x, w) = _slice(entry)
+    got = oracle.conv(s, x, w)
+    assert mk.sha(got) == entry["sha256"], f"{entry['name']}: oracle differs from the reference IR"
+    assert entry["iterations"] == s.nImg * s.nOfm * s.nIfm * s.ofh * s.ofw * s.kh * s.kw
+    assert entry["rel_l2_vs_f64"] < 1e-6
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference interpreter not built here")
+@pytest.mark.parametrize("entry", SLICES, ids=lambda e: e["name"])
+def test_live_reference_ir_at_baseline_size(entry):
+    """Re-executes the reference IR live (this container only, ~5-9 s per slice)."""
+    mk, (s, x, w) = _slice(entry)
+    ref, n = oracle.ref_interp(entry["ref_csv10"], oracle.pad_input(s, x), w, (1, s.nOfm // 16, s.ofh, s.ofw, 16))
+    assert n == entry["iterations"]
+    assert np.array_equal(oracle.conv(s, x, w), ref)
