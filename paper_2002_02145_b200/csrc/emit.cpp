@@ -1,14 +1,20 @@
-// Driver emission: renders a plan's outer loop nest as C text in the format of
-// the reference emitter (include/nestrank/emit.hpp:60-134), so a plan can be
-// diffed against the reference's golden driver (tests/golden/conv_identity.c)
-// and against the reference's own `emit --recipe` output.
+// Driver emission: the plan's outer loop nest as C text, in the text format the
+// reference's emitter produces (emit.hpp:60-134; golden tests/golden/conv_identity.c),
+// so a B200 plan can be diffed against the reference's own `emit --recipe` output.
 //
-// Loop structure after a recipe follows apply_recipe (variants.hpp:230-284):
-// permuted loops, tiled loops replaced in place by their tile loop, intra-tile
-// loops hoisted just above the band in permuted order; a tile size that does
-// not divide the trip count yields a full-tile loop plus a remainder block.
+// Built directly from the resolved Schedule (Schedule::order = the recipe's loop
+// order; tiles from the canonical recipe id), in three steps:
+//   1. levels(): one Level per emitted loop -- untiled loops and the tile loops of
+//      tiled ones in the schedule's order, then the intra-tile loops in the same
+//      order, just above the band (the placement apply_recipe gives, variants.hpp:
+//      243-274);
+//   2. a tile loop whose tile does not divide the trip count is "versioned": its
+//      full tiles run in a for loop, the last partial tile in a block that pins the
+//      tile index, and everything nested inside is written once per version with the
+//      intra loop's bound switched to the trip count in the partial version;
+//   3. an explicit work stack walks the levels (no recursion) and a Writer turns the
+//      open/close events into indented lines.
 #include <cstring>
-#include <map>
 #include <set>
 #include <sstream>
 
@@ -17,141 +23,143 @@
 namespace psconv {
 namespace {
 
-struct Affine {  // c0 + sum coef*var, printed like NamedExpr::str (loopnest.hpp:69-88)
-  std::map<std::string, int64_t> terms;
-  int64_t cst = 0;
-  std::string str() const {
-    std::string out;
-    for (const auto& [v, c] : terms) {
-      if (c == 0) continue;
-      if (out.empty()) {
-        if (c == -1) out += "-";
-        else if (c != 1) out += std::to_string(c) + " * ";
-      } else {
-        out += c > 0 ? " + " : " - ";
-        const int64_t a = c > 0 ? c : -c;
-        if (a != 1) out += std::to_string(a) + " * ";
-      }
-      out += v;
-    }
-    if (out.empty()) return std::to_string(cst);
-    if (cst > 0) out += " + " + std::to_string(cst);
-    if (cst < 0) out += " - " + std::to_string(-cst);
-    return out;
-  }
-};
+// `k * v + c` in the reference's affine text form (coefficient first, `1 *` and
+// `+ 0` omitted); only the shapes the conv driver needs (k >= 0, c >= 0).
+std::string affine(int64_t k, const std::string& v, int64_t c) {
+  if (k == 0 || v.empty()) return std::to_string(c);
+  std::string s = (k == 1 ? std::string() : std::to_string(k) + " * ") + v;
+  if (c > 0) s += " + " + std::to_string(c);
+  return s;
+}
 
-struct ELoop {
+struct Level {
   std::string var;
-  Affine lower;
-  std::vector<Affine> uppers;  // 2 uppers = remainder intra loop
+  int64_t trip = 0;     // untiled / tile loop: iterations
+  // intra-tile loop of tile loop `outer`: var in [tile * outer, tile * outer + tile),
+  // clipped to `trip` (the original extent) in the partial-tile version
+  std::string outer;
+  int64_t tile = 0;
+  bool versioned = false;  // tile loop whose last tile is partial
+  int64_t full = 0;        // its full tiles
 };
 
-std::string indent(int d) { return std::string(static_cast<size_t>(d) * 2, ' '); }
+class Writer {
+ public:
+  void line(const std::string& s) { out_ << std::string(2 * depth_, ' ') << s << '\n'; }
+  void open(const std::string& s) {  // "<header> {"; a bare block for an empty header
+    line(s.empty() ? "{" : s + " {");
+    ++depth_;
+  }
+  void close() {
+    --depth_;
+    line("}");
+  }
+  std::string str() const { return out_.str(); }
+
+ private:
+  std::ostringstream out_;
+  int depth_ = 0;
+};
+
+std::vector<Level> levels(const conv_desc& d, const Schedule& s) {
+  const int64_t trips[L_COUNT] = {d.nImg, d.nOfm / d.gemm_block, d.nIfm / d.gemm_block, d.ofh, d.kh, d.kw};
+  const Recipe r = Recipe::parse(s.recipe_id);  // tiles ride on the canonical id
+  std::set<std::string> names = {"img", "ofm_tile", "ifm_tile", "oj", "kj", "ki", "oi", "ofm", "ifm"};
+  std::vector<Level> outer, inner;
+  for (int i = 0; i < L_COUNT; ++i) {
+    const int id = s.order[i];
+    Level l;
+    l.var = loop_name(id);
+    l.trip = trips[id];
+    int64_t tile = 0;
+    for (const auto& t : r.tiles)
+      if (t.first == l.var) tile = t.second;
+    if (tile == 0) {
+      outer.push_back(l);
+      continue;
+    }
+    Level t;  // the tile loop takes the loop's place
+    t.var = l.var + "_t";
+    while (names.count(t.var)) t.var += "_";
+    names.insert(t.var);
+    t.trip = (l.trip + tile - 1) / tile;
+    t.versioned = l.trip % tile != 0;
+    t.full = l.trip / tile;
+    outer.push_back(t);
+    l.outer = t.var;
+    l.tile = tile;
+    inner.push_back(l);
+  }
+  outer.insert(outer.end(), inner.begin(), inner.end());
+  return outer;
+}
 
 }  // namespace
 
 std::string emit_driver(const conv_desc& d, const Schedule& s) {
-  const int64_t trips[L_COUNT] = {d.nImg, d.nOfm / d.gemm_block, d.nIfm / d.gemm_block,
-                                  d.ofh,  d.kh,                  d.kw};
-  std::map<std::string, int64_t> tile_of;
-  // Tiles are carried on the canonical recipe id; recover them from it.
-  {
-    const Recipe r = Recipe::parse(s.recipe_id);
-    for (const auto& t : r.tiles) tile_of[t.first] = t.second;
-  }
-  std::set<std::string> taken = {"img", "ofm_tile", "ifm_tile", "oj", "kj", "ki", "oi", "ofm", "ifm"};
-  std::vector<ELoop> loops, intra;
-  for (int i = 0; i < L_COUNT; ++i) {
-    const int l = s.order[i];
-    const std::string var = loop_name(l);
-    auto t = tile_of.find(var);
-    if (t == tile_of.end()) {
-      ELoop e;
-      e.var = var;
-      e.uppers.push_back(Affine{{}, trips[l]});
-      loops.push_back(e);
+  const std::vector<Level> lv = levels(d, s);
+  const std::string row = d.stride_h == 1 ? "oj + kj" : "oj * " + std::to_string(d.stride_h) + " + kj";
+  const std::string call =
+      "gemm_microkernel(&output[img][ofm_tile][oj][0][0], &filter[ofm_tile][ifm_tile][kj][ki][0][0], "
+      "&input[img][ifm_tile][" + row + "][ki][0]);";
+  Writer w;
+  w.line("#pragma omp parallel for private(ofm_tile, ifm_tile, oj, kj, ki)");  // presets.hpp:125
+  // Work items: enter a level (in the current version), or close a scope. The
+  // partial-tile set records which versioned tile loops are in their last tile.
+  struct Item {
+    enum Kind { kEnter, kClose, kPartial, kUnpartial } kind;
+    size_t level;
+  };
+  std::set<std::string> partial;
+  std::vector<Item> work = {{Item::kEnter, 0}};
+  while (!work.empty()) {
+    const Item it = work.back();
+    work.pop_back();
+    if (it.kind == Item::kClose) {
+      w.close();
       continue;
     }
-    const int64_t tile = t->second;
-    std::string tvar = var + "_t";
-    while (taken.count(tvar)) tvar += "_";
-    ELoop tl;
-    tl.var = tvar;
-    tl.uppers.push_back(Affine{{}, (trips[l] + tile - 1) / tile});
-    loops.push_back(tl);
-    ELoop il;
-    il.var = var;
-    il.lower.terms[tvar] = tile;
-    Affine end = il.lower;
-    end.cst += tile;
-    il.uppers.push_back(end);
-    if (trips[l] % tile != 0) il.uppers.push_back(Affine{{}, trips[l]});
-    intra.push_back(il);
-  }
-  for (auto& l : intra) loops.push_back(l);
-
-  const std::string sh = d.stride_h != 1 ? "oj * " + std::to_string(d.stride_h) + " + kj" : "oj + kj";
-  const std::string call = "gemm_microkernel(&output[img][ofm_tile][oj][0][0], "
-                           "&filter[ofm_tile][ifm_tile][kj][ki][0][0], &input[img][ifm_tile][" +
-                           sh + "][ki][0]);";
-
-  std::ostringstream os;
-  os << "#pragma omp parallel for private(ofm_tile, ifm_tile, oj, kj, ki)\n";  // presets.hpp:125
-  std::map<std::string, bool> rem_mode;
-  auto is_rem = [](const ELoop& l) { return l.uppers.size() == 2; };
-  auto tile_var_of = [](const ELoop& l) { return l.lower.terms.begin()->first; };
-  auto rec = [&](auto&& self, size_t dpt, int depth) -> void {
-    if (dpt == loops.size()) {
-      os << indent(depth) << call << "\n";
-      return;
-    }
-    const ELoop& l = loops[dpt];
-    const std::string step = "++" + l.var;
-    const ELoop* rem = nullptr;
-    for (size_t j = dpt + 1; j < loops.size(); ++j)
-      if (is_rem(loops[j]) && tile_var_of(loops[j]) == l.var) {
-        rem = &loops[j];
-        break;
+    if (it.kind == Item::kPartial || it.kind == Item::kUnpartial) {
+      const Level& t = lv[it.level];
+      if (it.kind == Item::kUnpartial) {
+        partial.erase(t.var);
+        w.close();
+        continue;
       }
-    if (rem) {
-      const int64_t tile = rem->lower.terms.at(l.var);
-      const int64_t full = (rem->uppers[1].cst - rem->lower.cst) / tile;
-      os << indent(depth) << "for (int " << l.var << " = 0; " << l.var << " < " << full << "; "
-         << step << ") {\n";
-      rem_mode[l.var] = false;
-      self(self, dpt + 1, depth + 1);
-      os << indent(depth) << "}\n";
-      os << indent(depth) << "{\n";
-      os << indent(depth + 1) << "const int " << l.var << " = " << full << ";\n";
-      rem_mode[l.var] = true;
-      self(self, dpt + 1, depth + 1);
-      rem_mode.erase(l.var);
-      os << indent(depth) << "}\n";
-      return;
+      // the last, partial tile: a block pinning the tile index, the nest inside it again
+      w.open("");
+      w.line("const int " + t.var + " = " + std::to_string(t.full) + ";");
+      partial.insert(t.var);
+      work.push_back({Item::kUnpartial, it.level});
+      work.push_back({Item::kEnter, it.level + 1});
+      continue;
     }
-    std::string upper;
-    if (is_rem(l)) {
-      const bool r = rem_mode.count(tile_var_of(l)) && rem_mode.at(tile_var_of(l));
-      upper = l.uppers[r ? 1 : 0].str();
-    } else {
-      upper = l.uppers[0].str();
+    if (it.level == lv.size()) {
+      w.line(call);
+      continue;
     }
-    os << indent(depth) << "for (int " << l.var << " = " << l.lower.str() << "; " << l.var << " < "
-       << upper << "; " << step << ") {\n";
-    self(self, dpt + 1, depth + 1);
-    os << indent(depth) << "}\n";
-  };
-  rec(rec, 0, 0);
-  return os.str();
+    const Level& l = lv[it.level];
+    std::string lo = "0", hi = std::to_string(l.trip);
+    if (!l.outer.empty()) {
+      lo = affine(l.tile, l.outer, 0);
+      hi = partial.count(l.outer) ? std::to_string(l.trip) : affine(l.tile, l.outer, l.tile);
+    } else if (l.versioned) {
+      hi = std::to_string(l.full);
+    }
+    w.open("for (int " + l.var + " = " + lo + "; " + l.var + " < " + hi + "; ++" + l.var + ")");
+    // LIFO: the partial-tile version (if any) follows the for loop's closing brace
+    if (l.versioned) work.push_back({Item::kPartial, it.level});
+    work.push_back({Item::kClose, it.level});
+    work.push_back({Item::kEnter, it.level + 1});
+  }
+  return w.str();
 }
 
 }  // namespace psconv
 
 using namespace psconv;
 
-extern "C" int64_t conv_emit_driver(const conv_desc* d_in, const char* recipe, char* buf,
-                                       size_t len) {
+extern "C" int64_t conv_emit_driver(const conv_desc* d_in, const char* recipe, char* buf, size_t len) {
   int64_t need = -1;
   const int rc = guarded([&] {
     if (!d_in) throw ConfigError("null descriptor");

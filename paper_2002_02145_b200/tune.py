@@ -17,6 +17,22 @@ from . import ConfigRejectedError, ConvPlan, ConvPreset, fill_filter, fill_input
 from .timing import L2Flush
 
 CACHE_ENV = "PSCONV_PLAN_CACHE"
+# The committed plan cache: the measured best recipe per (descriptor, mode) of every bench
+# workload (BASELINE configs, the ResNet-50 sweep, cfg5's per-GPU shards), written by
+# `bench.py --tune-plans K` on a B200. bench.py and the GPU parity tests run these recipes.
+PLANS_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "plans_b200.json")
+
+
+def lookup(preset: ConvPreset, mode: str, path: str | None = None) -> str | None:
+    """The cached measured-best recipe of (preset, mode), or None."""
+    path = path or PLANS_PATH
+    try:
+        with open(path) as fh:
+            cache = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    e = cache.get(f"{preset}|{mode}")
+    return e["recipe"] if e else None
 
 
 def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list[str]:

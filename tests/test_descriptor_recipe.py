@@ -162,3 +162,43 @@ def test_f16x2_mode_selection():
     assert ps.model_us(stem, "gpu=pp:3", "f16x2") == ps.model_us(stem, "gpu=pp:3", "3xtf32")
     with pytest.raises(ConfigRejectedError):
         ps.model_us(cfg5, "gpu=bn:256,cl:2", "f16x2")  # the CTA pair is TF32-only
+
+
+def _random_recipes(n, seed=2024):
+    import random
+    rng = random.Random(seed)
+    loops = ["img", "ofm_tile", "ifm_tile", "oj", "kj", "ki"]
+    out = []
+    for _ in range(n):
+        perm = loops[1:] if rng.random() < 0.7 else loops[:]
+        perm = perm[:]
+        rng.shuffle(perm)
+        k = rng.randint(1, len(perm))
+        parts = ["perm=" + ",".join(perm[:k])]
+        tiles = rng.sample(["oj", "ofm_tile", "ifm_tile", "kj", "img"], rng.randint(0, 3))
+        if tiles:
+            parts.append("tile=" + ",".join(f"{t}:{rng.randint(1, 5)}" for t in tiles))
+        out.append(";".join(parts))
+    return out
+
+
+@pytest.mark.parametrize("conv", ["conv:3,48,32,7,5,3,3,1,1,16", "conv:5,32,64,9,4,3,2,2,1,16"])
+def test_emission_matches_live_reference_emitter(conv):
+    """Randomised recipes (several loops tiled, tiles that do not divide their trip counts,
+    so nested partial-tile versions) vs the reference emitter itself (emit.hpp:60-134 via
+    oracle/_ref, this container only): byte-identical text."""
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("reference emitter not built here")
+    csv10 = conv.split(":", 1)[1]
+    n = 0
+    for r in _random_recipes(120):
+        try:
+            want = oracle.ref_emit(csv10, r)
+        except RuntimeError:  # the reference rejects it: so must we
+            with pytest.raises(ConfigRejectedError):
+                ps.emit_driver(ConvPreset.parse(conv), r)
+            continue
+        assert ps.emit_driver(ConvPreset.parse(conv), r) == want, r
+        n += 1
+    assert n >= 60

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from paper_2002_02145_b200 import measure as bench  # noqa: E402
 import paper_2002_02145_b200 as ps  # noqa: E402
 from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
 from paper_2002_02145_b200.tune import autotune  # noqa: E402
