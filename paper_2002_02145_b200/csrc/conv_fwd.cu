@@ -112,12 +112,25 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// promo: L2 sector promotion of the TMA's fills. 256 B (default) suits dense boxes; boxes
+// that skip 64-B pixels (element strides > 1, the stride-2 layers' A) use 64 B so the skipped
+// pixels are not fetched from DRAM with the used ones.
 void encode(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
             const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr,
-            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
+            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B,
+            CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+  static const int promo_env = [] {  // A/B switch (profiling): 0 none, 64, 128, 256
+    const char* e = std::getenv("PSCONV_A_PROMO");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (promo != CU_TENSOR_MAP_L2_PROMOTION_L2_256B && promo_env >= 0)
+    promo = promo_env == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : promo_env == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+            : promo_env == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                               : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base),
                                  dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, promo,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw RuntimeError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
@@ -875,7 +888,8 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
       const cuuint32_t box[5] = {16, cuuint32_t(s.qb * d.stride_w), cuuint32_t(s.pb * d.stride_h),
                                  cuuint32_t(s.nb), cuuint32_t(a_group ? s.kps : 1)};
       const cuuint32_t estr[5] = {1, cuuint32_t(d.stride_w), cuuint32_t(d.stride_h), 1, 1};
-      encode(&ta, base, 5, dims, strides, box, estr);
+      encode(&ta, base, 5, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_64B,
+             d.stride_w > 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     }
   }
   // B: filter prepacked K-major [CRS][K][16c] (hi, and lo for 3xTF32)
@@ -962,8 +976,14 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.absmax_b = P->absmax;
     prm.ncat = P->ncat ? 1 : 0;
     if (s.tmem_a) {  // TMEM A ring after the accumulators (2 x bn) and the running sum (bn)
-      // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum
-      prm.a_slot_col = ((s.bn <= 64 ? 5 : 3) * s.bn + 31) / 32 * 32;
+      // accumulators (2 buffers; [D1|D2] of 2 bn columns at bn <= 64) + the running sum,
+      // which exists only when a tile's reduction is split into accumulation chunks: with
+      // one chunk per tile the ring gets those columns too (bn 64: 8 slots instead of 6,
+      // two whole stages of kps = 4, so the splitter fills stage s+1 while the MMAs read
+      // stage s -- with 6 slots the two serialised, measured by the CTA-0 clock trace)
+      const int chunk_st = ((s.chunk > 0 ? s.chunk : prm.ksteps) + s.kps - 1) / s.kps;
+      const bool sum = chunk_st < prm.nst;
+      prm.a_slot_col = (((s.bn <= 64 ? 4 : 2) + (sum ? 1 : 0)) * s.bn + 31) / 32 * 32;
       prm.a_slots = std::min(kMaxStages, (512 - prm.a_slot_col) / 32);
       if (prm.a_slots < s.kps) throw RuntimeError("internal: TMEM A ring smaller than a stage");
     }
@@ -1019,7 +1039,8 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   }();
   prm.debug = debug_env;
   static unsigned long long* trace_buf = nullptr;
-  if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, (8 * kTraceStages + 8) * 8));
+  if ((debug_env & 8) && !trace_buf) CUDA_OK(cudaMalloc(&trace_buf, kTraceWords * 8));
+  if (debug_env & 8) CUDA_OK(cudaMemsetAsync(trace_buf, 0, kTraceWords * 8, st));
   prm.debug = debug_env & ~8;  // 1 2 4: skip loads / MMAs / stores; 16: generic halo issuer
   prm.trace = (debug_env & 8) ? trace_buf : nullptr;
   prm.out = out;
@@ -1030,21 +1051,26 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     dispatch_cs<true>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
   else
     dispatch_cs<false>(s.cs, s.bn, P, prm, ta, tb, tblo, tout, st);
-  if (prm.trace) {  // profiling: dump CTA 0's per-stage clocks (producer | MMA issuer)
-    unsigned long long h[8 * kTraceStages + 8];
+  if (prm.trace) {  // profiling: dump CTA 0's clocks (producer | MMA issuer | splitter | epilogue)
+    std::vector<unsigned long long> h(kTraceWords);
     CUDA_OK(cudaStreamSynchronize(st));
-    CUDA_OK(cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost));
-    const unsigned long long t0 = h[8 * kTraceStages];
+    CUDA_OK(cudaMemcpy(h.data(), prm.trace, kTraceWords * 8, cudaMemcpyDeviceToHost));
+    const long long t0 = static_cast<long long>(h[8 * kTraceStages]);
+    auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i]) - t0 : -1LL; };
     std::fprintf(stderr, "events: setup %lld first-acc %lld last-store %lld stores-done %lld exit %lld\n",
-                 (long long)(h[8 * kTraceStages + 1] - t0), (long long)(h[8 * kTraceStages + 4] - t0),
-                 (long long)(h[8 * kTraceStages + 5] - t0), (long long)(h[8 * kTraceStages + 6] - t0),
-                 (long long)(h[8 * kTraceStages + 7] - t0));
-    for (int i = 0; i < kTraceStages; ++i)
-      std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld %8lld\n", i,
-                   (long long)(h[i * 4] - t0), (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
-                   (long long)(h[4 * kTraceStages + i * 4] - t0), (long long)(h[4 * kTraceStages + i * 4 + 3] - t0),
-                   (long long)(h[4 * kTraceStages + i * 4 + 1] - t0),
-                   (long long)(h[4 * kTraceStages + i * 4 + 2] - t0));
+                 rel(8 * kTraceStages + 1), rel(8 * kTraceStages + 4), rel(8 * kTraceStages + 5),
+                 rel(8 * kTraceStages + 6), rel(8 * kTraceStages + 7));
+    for (int i = 0; i < kTraceStages; ++i) {
+      if (!h[i * 4] && !h[4 * kTraceStages + i * 4] && !h[kTraceSplit + 2 * i]) continue;
+      std::fprintf(stderr, "trace %3d prod %8lld %8lld %8lld  mma %8lld %8lld %8lld %8lld  split %8lld %8lld\n", i,
+                   rel(i * 4), rel(i * 4 + 1), rel(i * 4 + 2), rel(4 * kTraceStages + i * 4),
+                   rel(4 * kTraceStages + i * 4 + 3), rel(4 * kTraceStages + i * 4 + 1),
+                   rel(4 * kTraceStages + i * 4 + 2), rel(kTraceSplit + 2 * i), rel(kTraceSplit + 2 * i + 1));
+    }
+    for (int c = 0; c < 32; ++c)
+      if (h[kTraceEpi + 2 * c])
+        std::fprintf(stderr, "epi %2d acc_full %8lld released %8lld\n", c, rel(kTraceEpi + 2 * c),
+                     rel(kTraceEpi + 2 * c + 1));
   }
 }
 

@@ -129,6 +129,10 @@ struct ConvParams {
   unsigned long long* trace;      // profiling only (PSCONV_DEBUG & 8): CTA 0 stage timestamps
 };
 constexpr int kTraceStages = 128;
+// trace buffer layout (CTA 0): [producer 4 x S][MMA 4 x S][events 8][splitter 2 x S][epilogue 2 x 32]
+constexpr int kTraceSplit = 8 * kTraceStages + 8;
+constexpr int kTraceEpi = kTraceSplit + 2 * kTraceStages;
+constexpr int kTraceWords = kTraceEpi + 64;
 // CTA-0 clock trace (PSCONV_DEBUG=8) is compiled in only with -DPSCONV_TRACE
 // (tools/build_variant.sh): the instrumented loops measured 5% slower on cfg5.
 #ifdef PSCONV_TRACE
@@ -471,9 +475,14 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
       ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
     const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
     for (int cg = 0; cg < p.cbg; ++cg) {
+      const int gs = cit * p.cbg + cg;
+      const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
+      if (tr) p.trace[4 * kTraceStages + gs * 4 + 0] = clock64();
       ptx::mbar_wait(&full[as], aph);  // PAIR: both CTAs' halos landed
+      if (tr) p.trace[4 * kTraceStages + gs * 4 + 3] = clock64();
       if (SPLIT3) ptx::mbar_wait(&split_full[as], aph);
       ptx::tc_fence_after();
+      if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
       if (ptx::elect_one()) {
         const uint64_t a0 = adesc0 + static_cast<uint32_t>(as) * astage;
         const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(BRES ? cg * 9 : 0) * bstep;
@@ -531,6 +540,7 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
         }
       }
       __syncwarp();
+      if (tr) p.trace[4 * kTraceStages + gs * 4 + 2] = clock64();
       if (!BRES)
         for (int t = 0; t < 9; ++t)  // warp-uniform copy of the B-ring position
           if (++bs == p.hb_stages) {
@@ -693,8 +703,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B align the carve-out (SWIZZLE_64B atoms are 512 B). The offset is the
   // same in both CTAs of a pair, which the pair MMA relies on.
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // (pointer arithmetic on the __shared__ array, not an integer round trip: the compiler
+  // keeps the shared address space and emits STS/LDS instead of generic ST.E/LD.E)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   auto stage_base = [&](int s) { return smem + s * p.stage_bytes; };
 
   uint8_t* out_stage = smem + p.ring_bytes;  // kOutStages x 8 KB (1024-B aligned)
@@ -743,6 +754,10 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   if (PAIR) ptx::cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: the next kernel in the stream may be scheduled now -- its CTAs take an SM as soon
+  // as ours leave it and run their prologue there; every global read or write it makes
+  // waits in its griddepcontrol.wait for this grid's completion and memory flush
+  ptx::griddep_launch_dependents();
   if (ev && threadIdx.x == 0) {
     ev[0] = t_entry;
     ev[1] = clock64();  // barriers initialised, TMEM allocated
@@ -1089,6 +1104,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         ptx::mbar_wait(&acc_full[buf], acc_phase);
 #endif
         if (ev && store_thread && cit == 0) ev[4] = clock64();
+        if (ev && threadIdx.x == 64 && cit < 32) p.trace[kTraceEpi + 2 * cit] = clock64();
         ptx::tc_fence_after();
         if (EPI == kEpiSplit && split && last) {
           // the unit's partial is complete: take a ticket; the last holder waits until the
@@ -1222,6 +1238,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         if (!last) ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
+        if (ev && threadIdx.x == 64 && cit < 32) p.trace[kTraceEpi + 2 * cit + 1] = clock64();
         if (ptx::elect_one()) {
           if (PAIR && !leader)
             ptx::mbar_arrive_remote(acc_empty_leader + 8u * buf);
@@ -1285,10 +1302,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       int slot = 0;
       uint32_t sph = 0;
+      int gs = 0;
       for (int u = cluster; u < p.units; u += nclusters) {
         const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
-        for (int it = un.ib; it < un.ie; ++it) {
+        for (int it = un.ib; it < un.ie; ++it, ++gs) {
+          const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && tid == 0 && gs < kTraceStages;
           ptx::mbar_wait(&full[stage], phase);
+          if (tr) p.trace[kTraceSplit + 2 * gs] = clock64();
           const int nk = min(p.kps, p.ksteps - it * p.kps);
           for (int j = 0; j < nk; ++j) {
             ptx::mbar_wait(&aslot_empty[slot], sph ^ 1);  // the MMAs of slot's last use retired
@@ -1347,17 +1367,21 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           ptx::mbar_arrive(&split_full[stage]);
+          if (tr) p.trace[kTraceSplit + 2 * gs + 1] = clock64();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
-    } else
+    } else {
+    int gs = 0;
     for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
-      for (int it = un.ib; it < un.ie; ++it) {
+      for (int it = un.ib; it < un.ie; ++it, ++gs) {
+        const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && tid == 0 && gs < kTraceStages;
         ptx::mbar_wait(&full[stage], phase);
+        if (tr) p.trace[kTraceSplit + 2 * gs] = clock64();
         // A tiles of the stage: kps x a_pitch bytes (packed box image, or 8 KB
         // tiles); the lo region mirrors it (offsets are multiples of 512 B, so
         // the swizzle phase matches). Loads are batched 4 deep for ILP.
@@ -1370,11 +1394,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           split_lo(a, alo, n4, tid);
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[stage]);
+        if (tr) p.trace[kTraceSplit + 2 * gs + 1] = clock64();
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
         }
       }
+    }
     }
   }
 

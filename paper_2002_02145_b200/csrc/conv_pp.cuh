@@ -77,8 +77,9 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
   using Cfg = PpCfg<BN, SPLIT3>;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_m128<BN, 128>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // (pointer arithmetic on the __shared__ array, not an integer round trip: the compiler
+  // keeps the shared address space and emits STS/LDS instead of generic ST.E/LD.E)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   // [ring: stages x stage_bytes][resident B (hi | lo)][out staging][barriers]
   const int ring = (p.stages * p.stage_bytes + 1023) / 1024 * 1024;
   uint8_t* bres = smem + ring;
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(PpCfg<BN, SPLIT3>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::griddep_launch_dependents();  // PDL: see conv_fwd_sm100
   const int tiles_pq = p.tiles_q * p.tiles_p;
 
   if (warp == 0) {

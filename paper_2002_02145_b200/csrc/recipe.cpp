@@ -374,9 +374,11 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   // 3xTF32 default: equal chunks of at most 16 k-steps, or 40 at bn 256 where
   // each chunk boundary stalls the MMA on the drain (measured cfg5: ch 72 / 36 /
   // 32 / 24 -> 1738 / 1775 / 1789 / 1815 us; 40 k-steps ~ 4.8e-6 relL2)
+  // At bn <= 64 (TMEM-resident A, not halo) one chunk of up to 40 k-steps frees the running
+  // sum's TMEM columns for two more A slots (conv_fwd.cu a_slot_col).
   int chunk_def = ksteps;
   if (split_mode(mode)) {
-    const int cmax = s.bn == 256 ? 40 : 16;
+    const int cmax = (s.bn == 256 || (s.bn <= 64 && !s.halo)) ? 40 : 16;
     const int nch = (ksteps + cmax - 1) / cmax;
     chunk_def = (ksteps + nch - 1) / nch;
   }

@@ -18,7 +18,22 @@ from paper_2002_02145_b200 import measure as bench  # noqa: E402
 import paper_2002_02145_b200 as ps  # noqa: E402
 from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
 from paper_2002_02145_b200.workloads import ALL, seeds  # noqa: E402
-from sweep import time_it  # noqa: E402
+
+
+def time_it(fn, flush, steps, warm, stream):
+    """Mean event time (ms) of fn with the L2 flushed before every launch."""
+    import statistics
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in ev:
+        flush()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
 
 
 def main():
@@ -35,7 +50,16 @@ def main():
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream()
     flush = L2Flush(dev)
-    recs = [json.loads(l) for l in open(args.sweep) if l.strip()]
+    recs = []
+    for line in open(args.sweep):
+        if not line.strip():
+            continue
+        r = json.loads(line)
+        if "modes" in r:  # bench.py per-layer records (one per layer, nested modes)
+            for m, x in r["modes"].items():
+                recs.append({"layer": r["layer"], "mode": m, "recipe": x["recipe"], "kernel_ms": x["kernel_ms"]})
+        else:
+            recs.append(r)
     fr = []
     for r in recs:
         if (only and r["layer"] not in only) or r["mode"] not in modes:

@@ -9,7 +9,7 @@
 #include "sm100_ptx.cuh"
 using namespace psconv;
 
-template <int N, int UNROLL, int NACC = 1>
+template <int N, int UNROLL, int NACC = 1, int M = 128>
 __global__ void k_rate(int iters, long long* out, int shift, int boff) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -28,7 +28,7 @@ __global__ void k_rate(int iters, long long* out, int shift, int boff) {
   ptx::tc_fence_after();
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = ptx::idesc_tf32_m128<N>();
+    const uint32_t idesc = ptx::idesc_tf32_m128<N, M>();
     // A may start `shift` 64-B rows into the swizzled tile (halo-mode operands)
     // shift < 0: walk the nine 3x3 halo taps (row offsets kj*58 + ki) two MMAs per tap
     // (compile-time offsets); boff: B tile offset in smem
@@ -68,23 +68,29 @@ __global__ void k_rate(int iters, long long* out, int shift, int boff) {
   }
 }
 
-template <int N, int U, int NACC = 1>
+template <int N, int U, int NACC = 1, int M = 128>
 void run(int grid, int shift = 0, int boff = 8192) {
   long long* out;
   cudaMalloc(&out, 16);
-  cudaFuncSetAttribute(k_rate<N, U, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  cudaFuncSetAttribute(k_rate<N, U, NACC, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   const int iters = 256 / U;
-  k_rate<N, U, NACC><<<grid, 128, 80 * 1024>>>(iters, out, shift, boff);
-  k_rate<N, U, NACC><<<grid, 128, 80 * 1024>>>(iters, out, shift, boff);
+  k_rate<N, U, NACC, M><<<grid, 128, 80 * 1024>>>(iters, out, shift, boff);
+  k_rate<N, U, NACC, M><<<grid, 128, 80 * 1024>>>(iters, out, shift, boff);
   long long h[2];
   cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
   printf("acc %d shift %d boff %d ", NACC, shift, boff);
+  printf("M=%d ", M);
   printf("grid %3d N=%3d unroll %d: issue %6.1f cyc/mma, complete %6.1f cyc/mma (ideal %d at 4096 flop/cyc)\n",
          grid, N, U, double(h[0]) / 256, double(h[1]) / 256, 128 * N * 8 * 2 / 4096);
   cudaFree(out);
 }
 
 int main() {
+  for (int grid : {1, 148}) {  // M = 64 (output channels on M, pixels on N): rate per SM
+    run<64, 8, 1, 64>(grid);
+    run<128, 8, 1, 64>(grid);
+    run<256, 8, 1, 64>(grid);
+  }
   for (int bo : {8192, 16384, 24576, 32768, 40960}) {
     run<64, 8>(1, 0, bo);
     run<64, 8>(1, 1, bo);
