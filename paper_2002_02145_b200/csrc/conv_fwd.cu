@@ -627,7 +627,7 @@ int launch_nst(const conv_plan* P) {
   const conv_desc& d = P->kd;
   const Schedule& s = P->sched;
   const int Cb = int(d.nIfm / 16);
-  if (s.halo) return (Cb % s.kps == 0 ? Cb / s.kps : Cb) * int(d.kh * d.kw);
+  if (s.halo) return (Cb % s.kps == 0 ? Cb / s.kps : Cb) * int(s.tc ? d.kh : d.kh * d.kw);
   return (Cb * int(d.kh * d.kw) + s.kps - 1) / s.kps;
 }
 
@@ -903,17 +903,21 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   // B viewed as [16c][K][R*S][Cb] (b128: [32c][K][R*S][Cb/2]); box {c, rows, 1, blocks}
   // (ncat: [B_hi;B_lo] rows per N tile -> 2K rows, boxes of 2 bn rows)
   const int kr = P->ncat ? 2 : 1;
+  // tap concat (recipe tc:1): the prepacked [..][R*S][K][..] rows are [..][R][S*K][..] -- a
+  // filter row's S taps are one slice of S*K rows (bn == K), loaded as one B box
+  const int tcs = s.tc ? S : 1;
   if (P->b128) {
-    const cuuint64_t dims[4] = {32, cuuint64_t(K) * kr, cuuint64_t(R) * S, cuuint64_t(Cb / 2)};
-    const cuuint64_t strides[3] = {128, cuuint64_t(K) * kr * 128, cuuint64_t(K) * kr * 128 * R * S};
-    const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs) * kr, 1, cuuint32_t(s.kps / 2)};
+    const cuuint64_t dims[4] = {32, cuuint64_t(K) * kr * tcs, cuuint64_t(R) * S / tcs, cuuint64_t(Cb / 2)};
+    const cuuint64_t strides[3] = {128, cuuint64_t(K) * kr * tcs * 128, cuuint64_t(K) * kr * 128 * R * S};
+    const cuuint32_t box[4] = {32, cuuint32_t(s.bn / s.cs) * kr * tcs, 1, cuuint32_t(s.kps / 2)};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     encode(&tb, b_hi, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
     encode(&tblo, b_lo, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
   } else {
-    const cuuint64_t dims[4] = {16, cuuint64_t(K) * kr, cuuint64_t(R) * S, cuuint64_t(Cb)};
-    const cuuint64_t strides[3] = {64, cuuint64_t(K) * kr * 64, cuuint64_t(K) * kr * 64 * R * S};
-    const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs) * kr, 1, cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
+    const cuuint64_t dims[4] = {16, cuuint64_t(K) * kr * tcs, cuuint64_t(R) * S / tcs, cuuint64_t(Cb)};
+    const cuuint64_t strides[3] = {64, cuuint64_t(K) * kr * tcs * 64, cuuint64_t(K) * kr * 64 * R * S};
+    const cuuint32_t box[4] = {16, cuuint32_t(s.bn / s.cs) * kr * tcs, 1,
+                               cuuint32_t(Cb % s.kps == 0 ? s.kps : 1)};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     encode(&tb, b_hi, 4, dims, strides, box, estr);
     encode(&tblo, b_lo, 4, dims, strides, box, estr);
@@ -1001,8 +1005,9 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
       prm.b_res = s.b_res;
       prm.b_lo_off = h.b_lo_off;
       prm.hb_ring_off = prm.stages * h.a_stage;
-      prm.ring_bytes = prm.hb_ring_off + (s.b_res ? int(R * S) * prm.cbg : prm.hb_stages) * h.b_stage;
-      prm.nst = prm.cbg * R * S;  // taps per tile (B stages)
+      prm.ring_bytes = prm.hb_ring_off + (s.b_res ? int(R * S / tcs) * prm.cbg : prm.hb_stages) * h.b_stage;
+      prm.nst = prm.cbg * R * S / tcs;  // taps (tap concat: filter rows) per tile = B stages
+      prm.tc = s.tc;
       if (prm.stages > kHaloB || prm.hb_stages < (s.b_res ? 1 : 2) || prm.hb_stages > kMaxStages - kHaloB)
         throw RuntimeError("internal: bad halo stage plan");
     }
@@ -1067,6 +1072,11 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
                    rel(4 * kTraceStages + i * 4 + 3), rel(4 * kTraceStages + i * 4 + 1),
                    rel(4 * kTraceStages + i * 4 + 2), rel(kTraceSplit + 2 * i), rel(kTraceSplit + 2 * i + 1));
     }
+    for (int r = 0; r < 16; ++r)
+      if (h[kTraceEpiR + 5 * r])
+        std::fprintf(stderr, "round %2d start %8lld loaded %8lld bar1 %8lld staged %8lld issued %8lld\n", r,
+                     rel(kTraceEpiR + 5 * r), rel(kTraceEpiR + 5 * r + 1), rel(kTraceEpiR + 5 * r + 2),
+                     rel(kTraceEpiR + 5 * r + 3), rel(kTraceEpiR + 5 * r + 4));
     for (int c = 0; c < 32; ++c)
       if (h[kTraceEpi + 2 * c])
         std::fprintf(stderr, "epi %2d acc_full %8lld released %8lld\n", c, rel(kTraceEpi + 2 * c),

@@ -82,6 +82,10 @@ struct ConvParams {
   // (one (kj, ki) filter box over the kps blocks) at hb_ring_off.
   int halo, hw, hr, a_tile;
   int hb_stages, hb_stage_bytes, hb_ring_off;
+  int tc;                         // halo tap concat (TF32, 3x3, bn == K <= 64): per filter row kj
+                                  // one N = 3 bn MMA of the shared A rows (halo pitch hw = 32:
+                                  // one output row per epilogue warp) into D = [D_0|D_1|D_2];
+                                  // out[r] = D_0[r] + D_1[r+1] + D_2[r+2] (warp shuffles)
   int b_res;                      // halo: the CTA's whole filter slice (R*S*cbg boxes of
                                   // hb_stage_bytes at hb_ring_off) loaded once and kept
                                   // resident (one N tile); no B ring
@@ -132,7 +136,8 @@ constexpr int kTraceStages = 128;
 // trace buffer layout (CTA 0): [producer 4 x S][MMA 4 x S][events 8][splitter 2 x S][epilogue 2 x 32]
 constexpr int kTraceSplit = 8 * kTraceStages + 8;
 constexpr int kTraceEpi = kTraceSplit + 2 * kTraceStages;
-constexpr int kTraceWords = kTraceEpi + 64;
+constexpr int kTraceEpiR = kTraceEpi + 64;   // per epilogue round (first 16): 5 timestamps
+constexpr int kTraceWords = kTraceEpiR + 80;
 // CTA-0 clock trace (PSCONV_DEBUG=8) is compiled in only with -DPSCONV_TRACE
 // (tools/build_variant.sh): the instrumented loops measured 5% slower on cfg5.
 #ifdef PSCONV_TRACE
@@ -181,7 +186,10 @@ struct KernelCfg {
   // alternate 32-column rounds: TF32 warps 2-5 and 6-9; 3xTF32 warps 2-5 and
   // 10-13 (the splitter is 6-9)
   static constexpr int kEpiGroups = EG;
-  static constexpr int kThreads = (SPLIT3 ? 320 : 192) + (kEpiGroups - 1) * 128;
+  // + one store warp: issues the epilogue's TMA stores from the staging slots the
+  // epilogue warps fill (mbarrier handshakes), so no epilogue warp waits on a store issue
+  static constexpr int kThreads = (SPLIT3 ? 320 : 192) + (kEpiGroups - 1) * 128 + 32;
+  static constexpr int kStoreWarp = kThreads / 32 - 1;
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
       kStageBudget + kOutStages * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
@@ -193,7 +201,8 @@ struct KernelCfg {
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
   static_assert(2 * (kABytes + kBBytes) * (SPLIT3 ? 2 : 1) <= kStageBudget, "two stages of one k-step");
   static_assert(kSmemBytes <= 227 * 1024, "smem");
-  static_assert(4 * kMaxStages * 8 + 4 * 8 + 4 <= kBarBytes, "barriers");  // full/split/empty/aslot + acc
+  static_assert(4 * kMaxStages * 8 + 4 * 8 + 8 + 2 * kOutStages * 8 + kOutStages * 4 <= kBarBytes,
+                "barriers");  // full/split/empty/aslot + acc + tmem slot/ticket + staging slots
   static_assert(kColsNeeded <= 512, "TMEM");
   // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
   // a cluster-scope release per k-step (MEMBAR.GPU, measured ~3x slower).
@@ -350,16 +359,18 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   constexpr int CS = Cfg::kCS;
   const bool skip_a = (p.debug & 1) != 0;
   const uint32_t a_tx = (skip_a ? 0u : static_cast<uint32_t>(p.kps * p.hr * p.hw * 64)) * CS;
-  const uint32_t b_tx = static_cast<uint32_t>(Cfg::kBBytes * p.kps * (SPLIT3 ? 2 : 1)) * CS;
+  // one B box (a tap, or with tap concat a filter row of S taps) over kps blocks, both CTAs
+  const uint32_t b_tx = static_cast<uint32_t>(p.hb_stage_bytes) * CS;
   const bool hncat = SPLIT3 && BN <= 64 && p.ncat != 0;  // 3xTF32 N-concat filter rows
   const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
-  const int taps = p.R * p.S;
+  const int taps = p.tc ? p.R : p.R * p.S;
+  const int brows = p.tc ? p.S * Cfg::kBRows : Cfg::kBRows;  // B rows of one CTA's box
   int as = 0, bs = 0, gs = 0;
   uint32_t aph = 0, bph = 0;
   if (p.b_res) {
     // resident filter slice: every (channel group, tap) box once, one barrier
     // (PAIR: each CTA loads its BN/2 rows, completing on the leader's barrier)
-    const int k0 = rank * Cfg::kBRows;  // single N tile (tiles_k == 1)
+    const int k0 = rank * brows;  // single N tile (tiles_k == 1)
     if (ptx::elect_one()) {
       if (!PAIR || leader) ptx::mbar_expect_tx(&full[kHaloB], b_tx * p.cbg * taps);
       for (int cg = 0; cg < p.cbg; ++cg)
@@ -381,8 +392,9 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
   for (int g = cluster; g < p.groups; g += nclusters) {
     const TileCoord tc = decode_group(p, g, rank, CS);
     const int hp = tc.tp * p.Pb - p.ph;
+    const int wq = tc.tq * p.Qb - p.pw;  // (whole rows: tq = 0; tap concat: Qb-wide column tiles)
     const int n0 = tc.tn;
-    const int k0 = tc.tk * BN + rank * Cfg::kBRows;
+    const int k0 = tc.tk * BN * (p.tc ? p.S : 1) + rank * brows;
     for (int cg = 0; cg < p.cbg; ++cg) {
       const int cb = cg * p.kps;
       ptx::mbar_wait(&empty[as], aph ^ 1);
@@ -390,10 +402,10 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
         uint8_t* sa = smem + as * p.stage_bytes;
         if (!PAIR) {
           ptx::mbar_expect_tx(&full[as], a_tx);
-          if (!skip_a) ptx::tma_load_5d(sa, tmap_in, &full[as], 0, -p.pw, hp, n0, cb);
+          if (!skip_a) ptx::tma_load_5d(sa, tmap_in, &full[as], 0, wq, hp, n0, cb);
         } else {
           if (leader) ptx::mbar_expect_tx(&full[as], a_tx);
-          if (!skip_a) ptx::tma_load_5d_cb(sa, tmap_in, full_leader + 8u * as, 0, -p.pw, hp, n0, cb);
+          if (!skip_a) ptx::tma_load_5d_cb(sa, tmap_in, full_leader + 8u * as, 0, wq, hp, n0, cb);
         }
       }
       __syncwarp();
@@ -438,17 +450,25 @@ __device__ __forceinline__ void halo_producer(const ConvParams& p, uint8_t* smem
 // thread waits for each tap's B-ring stage and releases it by a commit. The
 // generic issuer's per-tap bookkeeping (~200-400 cycles per tap, measured with
 // the clock trace) starves the tensor core at N = 64 (48-cycle MMAs).
-template <int BN, bool SPLIT3, bool PAIR, int KPS, bool BRES>
+// TC (tap concat, TF32, bn <= 64): per filter row kj ONE MMA of N = 3 bn over the three
+// ki taps' filter rows [W(kj,0); W(kj,1); W(kj,2)] with the A rows shifted by kj*hw only:
+// D_ki[r] = sum x[r + kj*hw] W(kj, ki), and the epilogue forms out[r] = sum_ki D_ki[r + ki].
+// N = 192 runs at the full tensor rate (96 cycles per K = 8) where three N = 64 MMAs take
+// 3 x 45-48 (tools/probe_mma_rate.cu).
+template <int BN, bool SPLIT3, bool PAIR, int KPS, bool BRES, bool TC = false>
 __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem, uint64_t* full,
                                              uint64_t* split_full, uint64_t* empty, uint64_t* acc_full,
                                              uint64_t* acc_empty, uint32_t tmem_base, int cluster,
                                              int nclusters, uint32_t idesc) {
   using Cfg = KernelCfg<BN, SPLIT3, PAIR>;
   constexpr int kAccBufs = Cfg::kAccBufs;
+  constexpr int kTaps = TC ? 3 : 9;                   // MMA groups per channel group
+  constexpr int kAccW = TC ? 3 * BN : Cfg::kAccW;     // accumulator columns per buffer
+  constexpr uint32_t kIdescTC = ptx::idesc_tf32_m128<(3 * BN <= 256 ? 3 * BN : BN), 128 * Cfg::kCS>();
   const uint64_t adesc0 = ptx::smem_desc_sw64(ptx::smem_u32(smem), 16, 512);
   const uint64_t bdesc0 = p.b128 ? ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024) : adesc0;
   const bool hncat = SPLIT3 && BN <= 64 && p.ncat != 0;  // [B_hi; B_lo] rows per block
-  const uint32_t bblk = static_cast<uint32_t>(Cfg::kBBytes * (hncat ? 2 : 1)) >> 4;
+  const uint32_t bblk = static_cast<uint32_t>(Cfg::kBBytes * (hncat ? 2 : 1) * (TC ? 3 : 1)) >> 4;
   const uint32_t b_even = p.b128 ? 4u : bblk;
   const uint32_t b_odd = p.b128 ? (2u * bblk - 4u) : bblk;
   constexpr uint32_t kIdesc2 = ptx::idesc_tf32_m128<(BN <= 128 ? 2 * BN : BN), 128 * Cfg::kCS>();
@@ -473,7 +493,7 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
       ptx::mbar_wait_cluster(&acc_empty[buf], acc_phase ^ 1);
     else
       ptx::mbar_wait(&acc_empty[buf], acc_phase ^ 1);
-    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * Cfg::kAccW);
+    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * kAccW);
     for (int cg = 0; cg < p.cbg; ++cg) {
       const int gs = cit * p.cbg + cg;
       const bool tr = kTrace && p.trace != nullptr && blockIdx.x == 0 && gs < kTraceStages;
@@ -485,13 +505,14 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
       if (tr) p.trace[4 * kTraceStages + gs * 4 + 1] = clock64();
       if (ptx::elect_one()) {
         const uint64_t a0 = adesc0 + static_cast<uint32_t>(as) * astage;
-        const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(BRES ? cg * 9 : 0) * bstep;
+        const uint64_t b0 = bdesc0 + bres + static_cast<uint32_t>(BRES ? cg * kTaps : 0) * bstep;
         uint32_t acc_in = cg == 0 ? 0u : 1u;
         int ts = bs;
         uint32_t tph = bph;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          uint64_t da = a0 + static_cast<uint32_t>(t / 3) * hw4 + static_cast<uint32_t>(t % 3) * 4u;
+        for (int t = 0; t < kTaps; ++t) {
+          uint64_t da = TC ? a0 + static_cast<uint32_t>(t) * hw4
+                           : a0 + static_cast<uint32_t>(t / 3) * hw4 + static_cast<uint32_t>(t % 3) * 4u;
           uint64_t db = b0 + static_cast<uint32_t>(BRES ? t : ts) * bstep;
           if (!BRES) {
             ptx::mbar_wait(&full[kHaloB + ts], tph);  // this tap's filter box landed
@@ -502,7 +523,11 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (!skip_mma) {
-                if (SPLIT3 && hncat) {
+                if (TC && PAIR) {
+                  ptx::mma_tf32_pair(d_tmem, da + h * 2, db + h * 2, kIdescTC, acc_in);  // -> D0|D1|D2
+                } else if (TC) {
+                  ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdescTC, acc_in);
+                } else if (SPLIT3 && hncat) {
                   ptx::mma_tf32(d_tmem, da + h * 2, db + h * 2, kIdesc2, acc_in);        // -> D1 | D2
                   ptx::mma_tf32(d_tmem, da + alo_off + h * 2, db + h * 2, idesc, 1u);   // A_lo B_hi
                 } else if (SPLIT3) {
@@ -542,7 +567,7 @@ __device__ __forceinline__ void halo_mma_fast(const ConvParams& p, uint8_t* smem
       __syncwarp();
       if (tr) p.trace[4 * kTraceStages + gs * 4 + 2] = clock64();
       if (!BRES)
-        for (int t = 0; t < 9; ++t)  // warp-uniform copy of the B-ring position
+        for (int t = 0; t < kTaps; ++t)  // warp-uniform copy of the B-ring position
           if (++bs == p.hb_stages) {
             bs = 0;
             bph ^= 1;
@@ -718,6 +743,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   uint64_t* aslot_empty = acc_empty + 2;         // TMEM A slot consumed by the MMA [kMaxStages]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aslot_empty + kMaxStages);
   volatile int* split_word = reinterpret_cast<volatile int*>(tmem_slot + 1);  // split-K ticket broadcast
+  uint64_t* out_full = aslot_empty + kMaxStages + 1;  // staging slot filled (128 epilogue threads)
+  uint64_t* out_free = out_full + kOutStages;         // staging slot read by its TMA store (store warp)
+  volatile int* out_skip = reinterpret_cast<volatile int*>(out_free + kOutStages);  // slot holds no tile
 
   const int warp = threadIdx.x >> 5;
   const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
@@ -741,13 +769,19 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
       ptx::mbar_init(&acc_empty[a], 4 * EG * CS);
     }
     for (int a = 0; a < (p.tmem_a ? p.a_slots : 0); ++a) ptx::mbar_init(&aslot_empty[a], 1);
+    for (int o = 0; o < kOutStages; ++o) {
+      ptx::mbar_init(&out_full[o], 128);
+      ptx::mbar_init(&out_free[o], 1);
+    }
     ptx::fence_mbar_init();
   }
+  // tap concat needs 2 x 3 bn accumulator columns (bn 64: 384 -> 512)
+  const uint32_t tmem_cols = (!SPLIT3 && BN <= 64 && p.tc) ? 512u : static_cast<uint32_t>(Cfg::kTmemCols);
   if (warp == 1) {
     if (PAIR)
-      ptx::tmem_alloc_pair(tmem_slot, Cfg::kTmemCols);
+      ptx::tmem_alloc_pair(tmem_slot, tmem_cols);
     else
-      ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+      ptx::tmem_alloc(tmem_slot, tmem_cols);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -874,13 +908,30 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
 #define PSCONV_HALO_FAST(K, R)                                                                         \
   halo_mma_fast<BN, SPLIT3, PAIR, K, R>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base, \
                                         cluster, nclusters, kIdesc)
-    if (fast && p.b_res && p.kps == 4) PSCONV_HALO_FAST(4, true);
+#define PSCONV_HALO_TC(K, R)                                                                                 \
+  halo_mma_fast<BN, SPLIT3, PAIR, K, R, true>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base, \
+                                              cluster, nclusters, kIdesc)
+    bool issued = false;
+    if constexpr (!SPLIT3 && BN <= 64) {
+      if (p.tc) {  // tap concat: always the lean issuer (3x3, one chunk)
+        if (p.b_res && p.kps == 4) PSCONV_HALO_TC(4, true);
+        else if (p.b_res && p.kps == 2) PSCONV_HALO_TC(2, true);
+        else if (p.b_res) PSCONV_HALO_TC(1, true);
+        else if (p.kps == 4) PSCONV_HALO_TC(4, false);
+        else if (p.kps == 2) PSCONV_HALO_TC(2, false);
+        else PSCONV_HALO_TC(1, false);
+        issued = true;
+      }
+    }
+    if (issued) {
+    } else if (fast && p.b_res && p.kps == 4) PSCONV_HALO_FAST(4, true);
     else if (fast && p.b_res && p.kps == 2) PSCONV_HALO_FAST(2, true);
     else if (fast && p.b_res && p.kps == 1) PSCONV_HALO_FAST(1, true);
     else if (fast && p.kps == 4) PSCONV_HALO_FAST(4, false);
     else if (fast && p.kps == 2) PSCONV_HALO_FAST(2, false);
     else if (fast && p.kps == 1) PSCONV_HALO_FAST(1, false);
 #undef PSCONV_HALO_FAST
+#undef PSCONV_HALO_TC
     else
       halo_mma<BN, SPLIT3, PAIR>(p, smem, full, split_full, empty, acc_full, acc_empty, tmem_base,
                                  cluster, nclusters, kIdesc);
@@ -1040,6 +1091,55 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   } else if (warp == 1) {
     // second CTA of a pair: its loads complete on the leader's barrier and the
     // leader issues the pair MMAs; nothing to do here.
+  } else if (warp == Cfg::kStoreWarp) {
+    // ------------------------------------------------------------ store warp
+    // Walks the epilogue's rounds in the same order (units, last chunk, 32-channel rounds
+    // of both groups): waits for a staging slot to be filled, issues its TMA tensor
+    // store(s) (reduce-add for `+=`), waits until the store has read the slot and hands it
+    // back. Slots of split-K writer units carry no tile (out_skip).
+    constexpr int DW = Cfg::kDrainW;
+    constexpr int kBlk = DW / 16;
+    constexpr int kRounds = kOutStages / EG / kBlk;  // staging slots per epilogue group
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&tmap_out);
+      int ost[2] = {0, 0};
+      uint32_t oph[2] = {0u, 0u};
+      const bool reduce = p.accumulate != 0;
+      for (int u = cluster; u < p.units; u += nclusters) {
+        const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
+        const TileCoord tc = decode_group(p, un.g, rank, CS);
+        if (!tc.live) continue;
+        const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
+        const int kb0 = tc.tk * (BN / 16);
+        for (int j = 0; j < BN / DW; ++j) {
+          const int g = EG == 2 ? (j & 1) : 0;
+          const int slot = g * kRounds + ost[g];
+          ptx::mbar_wait(&out_full[slot], oph[g]);
+          if (!out_skip[slot] && !(p.debug & 4)) {
+            const uint8_t* st = out_stage + slot * (kBlk * Cfg::kOutStageBytes);
+#pragma unroll
+            for (int blk = 0; blk < kBlk; ++blk) {
+              const int kb = kb0 + j * kBlk + blk;
+              if (reduce)
+                ptx::tma_reduce_add_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
+              else
+                ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
+            }
+            ptx::bulk_commit();
+            ptx::bulk_wait_read<0>();  // the slot's bytes are in flight to global memory
+          }
+          ptx::mbar_arrive(&out_free[slot]);
+          if (++ost[g] == kRounds) {
+            ost[g] = 0;
+            oph[g] ^= 1u;
+          }
+        }
+      }
+      if (ev) ev[5] = clock64();  // last store issued
+      ptx::bulk_wait_all();       // stores complete before smem is released
+      if (ev) ev[6] = clock64();
+    }
+    __syncwarp();
   } else if (warp < 6 || (EG == 2 && warp >= (SPLIT3 ? 10 : 6))) {
     // ------------------------------------------------------------ epilogue
     constexpr int DW = Cfg::kDrainW;
@@ -1052,10 +1152,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     const int lane = threadIdx.x & 31;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    // first thread of each group issues its TMA stores (own bulk groups, own
-    // staging blocks, own named barrier)
+    // first thread of each group: traces, the split-K ticket
     const bool store_thread = threadIdx.x == (egrp == 0 ? 64 : (SPLIT3 ? 320 : 192));
-    const int ebar = 1 + egrp;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
     // staged row of this lane: the tile row itself, or (halo) its pixel
@@ -1064,27 +1162,27 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     int srow = row;
     bool row_valid = true;
     if (p.halo) {
+      // (staging pitch = the tile's Qb columns: Q for whole-row tiles, 33 - kw with tap concat)
       const int pr = row / p.hw, q = row - pr * p.hw;
-      row_valid = q < p.Q && pr < p.Pb;
-      srow = pr * p.Q + q;
+      row_valid = q < p.Qb && pr < p.Pb;
+      srow = pr * p.Qb + q;
     }
     const uint32_t row_off = static_cast<uint32_t>(srow) * 64u;
     const uint32_t row_swz = (static_cast<uint32_t>(srow) >> 1) & 3u;  // SW64: chunk ^= bits[7:8]
-    int ostage = 0;                                                  // staging buffer toggle
-    if (store_thread) ptx::prefetch_tmap(&tmap_out);
+    int ostage = 0;      // this group's staging slot (round robin over kRounds)
+    uint32_t oph = 0u;   // its phase (toggles when ostage wraps)
     float out_scale = 1.f;
     if constexpr (F16) {
       ptx::griddep_wait();
       out_scale = 1.f / (pow2_scale(*p.absmax_a) * pow2_scale(*p.absmax_b));
     }
     int cit = 0;
+    [[maybe_unused]] int rtrace = 0;  // epilogue rounds traced (PSCONV_TRACE builds)
     for (int u = cluster; u < p.units; u += nclusters) {
       const Unit un = decode_unit<EPI == kEpiSplit>(p, u);
       const int unchunks =
           EPI != kEpiSplit || un.sp < 0 ? p.tile_chunks : (un.ie - un.ib + p.chunk_stages - 1) / p.chunk_stages;
       const TileCoord tc = decode_group(p, un.g, rank, CS);
-      const int q0 = tc.tq * p.Qb, p0 = tc.tp * p.Pb, n0 = tc.tn * p.Nb;
-      const int kb0 = tc.tk * (BN / 16);
       // split tile: ticket -> write the partial to the workspace, or (last ticket)
       // combine all partials in split order and store the tile (ConvParams::split_ctr)
       const bool split = EPI == kEpiSplit && un.sp >= 0 && tc.live;
@@ -1093,7 +1191,6 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
       float4* const ws = split ? reinterpret_cast<float4*>(p.split_ws) + static_cast<long long>(stile) * p.ksplit * (32 * BN)
                                : nullptr;
       bool fixer = false;
-      const bool reduce = p.accumulate != 0;  // `+=`: TMA reduce-add of the finished tile
       for (int c = 0; c < unchunks; ++c, ++cit) {
         const int buf = kAccBufs == 1 ? 0 : (cit & 1);
         const uint32_t acc_phase = (kAccBufs == 1 ? cit : (cit >> 1)) & 1;
@@ -1120,13 +1217,32 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
           fixer = *split_word == p.ksplit - 1;
           if (fixer) ptx::fence_acq_rel_gpu();
         }
-        const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * Cfg::kAccW);
+        constexpr bool kTcCap = !SPLIT3 && BN <= 64;  // tap concat instantiations
+        const int accw = (kTcCap && p.tc) ? 3 * BN : Cfg::kAccW;
+        const uint32_t tacc = lane_base + static_cast<uint32_t>(buf * accw);
         const uint32_t tsum = lane_base + static_cast<uint32_t>(Cfg::kSumCol);
 #pragma unroll 1
         for (int j = egrp; j < BN / DW; j += kGroups) {
+          const bool rtr = ev && threadIdx.x == 64 && rtrace < 16;
+          if (rtr) p.trace[kTraceEpiR + 5 * rtrace] = clock64();
           uint32_t v[DW];
           if constexpr (DW == 32) ptx::tmem_ld32(tacc + j * 32, v);
           else ptx::tmem_ld16(tacc + j * 16, v);
+          // tap concat: D = [D_0 | D_1 | D_2] (ki taps); out[r] = D_0[r] + D_1[r+1] + D_2[r+2]
+          // -- one output row per warp (halo pitch 32), so the row shifts are warp shuffles
+          // (lanes 30-31 read their own values: junk columns)
+          [[maybe_unused]] uint32_t t1[kTcCap ? DW : 1], t2[kTcCap ? DW : 1];
+          if constexpr (kTcCap) {
+            if (p.tc) {
+              if constexpr (DW == 32) {
+                ptx::tmem_ld32(tacc + BN + j * 32, t1);
+                ptx::tmem_ld32(tacc + 2 * BN + j * 32, t2);
+              } else {
+                ptx::tmem_ld16(tacc + BN + j * 16, t1);
+                ptx::tmem_ld16(tacc + 2 * BN + j * 16, t2);
+              }
+            }
+          }
           if constexpr (Cfg::kAccW == 2 * BN) {
             if (ncat) {  // D1 + D2 (A_hi B_lo in its own accumulator)
               uint32_t v2[DW];
@@ -1153,10 +1269,23 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
             ptx::tmem_wait_ld();
             ptx::reg_fence(v);
           }
+          if constexpr (kTcCap) {
+            if (p.tc) {
+              ptx::reg_fence(t1);
+              ptx::reg_fence(t2);
+#pragma unroll
+              for (int i = 0; i < DW; ++i)
+                v[i] = __float_as_uint(__uint_as_float(v[i]) +
+                                       __uint_as_float(__shfl_down_sync(0xFFFFFFFFu, t1[i], 1)) +
+                                       __uint_as_float(__shfl_down_sync(0xFFFFFFFFu, t2[i], 2)));
+            }
+          }
+          if (rtr) p.trace[kTraceEpiR + 5 * rtrace + 1] = clock64();
           if (!last) {
             if constexpr (DW == 32) ptx::tmem_st32(tsum + j * 32, v);
             else ptx::tmem_st16(tsum + j * 16, v);
           } else if (tc.live) {
+            bool store_round = true;  // false: a split-K writer unit (partial in the workspace)
             // fused epilogue on the finished sum: + bias[k], ReLU (the same
             // value for all lanes: broadcast loads through L1)
             if constexpr (F16) {  // undo the operand scales (exact powers of two)
@@ -1174,9 +1303,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                   __stcg(ws + un.sp * (32 * BN) + wbase + c4 * 128,
                          make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
                                      __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3])));
-                if (!fixer) continue;  // no staging, no store
+                if (!fixer) store_round = false;  // the slot is handed over empty
 #pragma unroll 1
-                for (int sp = 0; sp < p.ksplit; ++sp) {  // v accumulates (own partial re-read)
+                for (int sp = 0; sp < (store_round ? p.ksplit : 0); ++sp) {  // v accumulates (own partial re-read)
 #pragma unroll
                   for (int c4 = 0; c4 < DW / 4; ++c4) {
                     const float4 x = __ldcg(ws + sp * (32 * BN) + wbase + c4 * 128);
@@ -1204,10 +1333,11 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
             // rounds in flight
             constexpr int kBlk = DW / 16;
             constexpr int kRounds = kOutStages / kGroups / kBlk;  // per group
-            uint8_t* st = out_stage + (egrp * kRounds + ostage) * (kBlk * Cfg::kOutStageBytes);
-            if (store_thread) ptx::bulk_wait_read<kRounds - 1>();  // this round's buffers read out
-            ptx::named_bar(ebar, 128);
-            if (row_valid) {
+            const int slot = egrp * kRounds + ostage;
+            uint8_t* st = out_stage + slot * (kBlk * Cfg::kOutStageBytes);
+            ptx::mbar_wait(&out_free[slot], oph ^ 1u);  // the slot's previous store has read it
+            if (rtr) p.trace[kTraceEpiR + 5 * rtrace + 2] = clock64();
+            if (row_valid && store_round) {
 #pragma unroll
               for (int blk = 0; blk < kBlk; ++blk) {
 #pragma unroll
@@ -1220,20 +1350,16 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
               }
             }
             ptx::fence_proxy_async_smem();
-            ptx::named_bar(ebar, 128);
-            if (store_thread && !(p.debug & 4)) {
-#pragma unroll
-              for (int blk = 0; blk < kBlk; ++blk) {
-                const int kb = kb0 + j * kBlk + blk;
-                if (reduce)  // `+=` or a later split-K partial
-                  ptx::tma_reduce_add_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
-                else
-                  ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
-              }
-              ptx::bulk_commit();
+            if (store_thread) out_skip[slot] = store_round ? 0 : 1;
+            ptx::mbar_arrive(&out_full[slot]);  // the store warp issues the TMA store(s)
+            if (rtr) p.trace[kTraceEpiR + 5 * rtrace + 3] = clock64();
+            if (++ostage == kRounds) {
+              ostage = 0;
+              oph ^= 1u;
             }
-            ostage = ostage + 1 == kRounds ? 0 : ostage + 1;
+            if (rtr) p.trace[kTraceEpiR + 5 * rtrace + 4] = clock64();
           }
+          if (kTrace) ++rtrace;
         }
         if (!last) ptx::tmem_wait_st();
         ptx::tc_fence_before();
@@ -1261,9 +1387,6 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
         }
       }
     }
-    if (ev && store_thread) ev[5] = clock64();  // last store issued
-    if (store_thread) ptx::bulk_wait_all();  // stores complete before smem is released
-    if (ev && store_thread) ev[6] = clock64();
   } else if (SPLIT3 && warp < 10) {
     // ------------------------------------------------------------ splitter
     // lo = x - trunc_tf32(x), exact in fp32 (the MMA reads x itself as hi).
@@ -1411,9 +1534,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     if (PAIR)
-      ptx::tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+      ptx::tmem_dealloc_pair(tmem_base, tmem_cols);
     else
-      ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+      ptx::tmem_dealloc(tmem_base, tmem_cols);
   }
 #endif
 }

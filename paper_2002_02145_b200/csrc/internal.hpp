@@ -63,6 +63,7 @@ struct Recipe {
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int eg = 0;                                                 // epilogue warp groups, 0 = auto (1)
   int pp = 0;                                                 // parity-plane tap pairs: C real channels (<= 4)
+  int tc = 0;                                                 // halo: the kw taps of a row concatenated on N
   int cs = 0;                                                 // cluster size, 0 = default
   bool has_gpu = false;
   static Recipe parse(const std::string& text);  // throws ConfigError
@@ -91,6 +92,8 @@ struct Schedule {
                        // instead of only the last partial wave's (flag-ordered)
   int egroups = 1;     // epilogue warp groups draining alternate 32-channel rounds (1 or 2)
   int pp = 0;          // few-channel kernel (conv_pp.cuh): C <= 4 real channels, tap pairs per MMA
+  int tc = 0;          // halo tap concat (TF32, 3x3, bn == nOfm <= 64): one N = 3 bn MMA per filter row
+                       // (the three ki taps share the A rows; the epilogue adds D_ki shifted by ki rows)
   int raster[3];       // {0 img, 1 ofm_tile, 2 oj} outer -> inner
   int kord[3];         // {0 ifm_tile, 1 kj, 2 ki} outer -> inner
   std::string recipe_id;
@@ -108,7 +111,9 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg);  // throws 
 
 // Halo-mode geometry (conv_kernel.cuh ConvParams::halo): padded row pitch hw,
 // halo rows hr, byte sizes of one A stage (kps halo tiles + junk-row slack,
-// A_lo mirror in 3xTF32) and one B stage (one tap over kps blocks).
+// A_lo mirror in 3xTF32) and one B stage (one tap over kps blocks; tap concat: one
+// filter row's kw taps, kw * bn rows). Tap concat pitches the halo at 32 pixels so
+// that each epilogue warp holds one output row (qb <= 33 - kw valid columns).
 struct HaloGeom {
   int hw, hr, a_tile, a_lo_off, a_stage, b_lo_off, b_stage;
 };

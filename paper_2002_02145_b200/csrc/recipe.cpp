@@ -123,6 +123,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "halo") {
           r.halo = static_cast<int>(parse_int(val, "gpu halo"));
           if (r.halo != 0 && r.halo != 1) throw ConfigError("gpu halo must be 0 or 1");
+        } else if (key == "tc") {
+          r.tc = static_cast<int>(parse_int(val, "gpu tap concat"));
+          if (r.tc != 0 && r.tc != 1) throw ConfigError("gpu tc must be 0 or 1");
         } else if (key == "pp") {
           r.pp = static_cast<int>(parse_int(val, "gpu parity-plane channels"));
           if (r.pp < 1 || r.pp > 4) throw ConfigError("gpu pp must be in [1, 4] (real input channels)");
@@ -157,6 +160,7 @@ std::string Recipe::id() const {
          std::to_string(box_p) + "x" + std::to_string(box_n);
     if (cs) s += ",cl:" + std::to_string(cs);
     if (halo) s += ",halo:1";
+    if (tc) s += ",tc:1";
     if (gm >= 0) s += ",gm:" + std::to_string(gm);
     if (fold) s += ",fold:" + std::to_string(fold);
     if (ta >= 0) s += ",ta:" + std::to_string(ta);
@@ -321,7 +325,21 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
 
   int fix_p = tile_of.count("oj") ? static_cast<int>(std::min<int64_t>(tile_of["oj"], d.ofh)) : 0;
   int fix_n = tile_of.count("img") ? static_cast<int>(std::min<int64_t>(tile_of["img"], d.nImg)) : 0;
-  if (r.halo) {
+  if (r.tc) {
+    // tap concat (halo variant): a filter row's kw taps as one N = kw * bn MMA over
+    // shared A rows; the halo is pitched at 32 pixels -- one output row per epilogue
+    // warp, qb = 33 - kw columns -- so the epilogue's row shift by ki stays in a warp
+    if (mode != PSCONV_MODE_TF32) throw ConfigError("gpu tc (tap concat) is a TF32 option");
+    if (d.stride_h != 1 || d.stride_w != 1 || d.kh != 3 || d.kw != 3)
+      throw ConfigError("gpu tc needs a 3x3 stride-1 layer");
+    if (s.bn != K || s.bn > 64) throw ConfigError("gpu tc needs bn == nOfm <= 64 (one N tile, N = 3 bn <= 192)");
+    if (r.halo == 0 && r.has_gpu && r.box_q) throw ConfigError("gpu tc implies halo mode (no box)");
+    s.qb = static_cast<int>(std::min<int64_t>(33 - d.kw, d.ofw));
+    s.pb = static_cast<int>(std::min<int64_t>(4, d.ofh));
+    s.nb = 1;
+    s.halo = 1;
+    s.tc = 1;
+  } else if (r.halo) {
     // halo mode: whole output rows of one image at the padded pitch hw
     if (!halo_eligible(d))
       throw ConfigError("GPU tile: halo mode needs stride 1, a filter larger than 1x1 and ofw + kw - 1 <= 128");
@@ -354,6 +372,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.box_p = s.pb;
   canon.box_n = s.nb;
   canon.halo = s.halo;
+  canon.tc = s.tc;
   canon.fold = r.fold;
   canon.ta = r.ta;
   s.ta = r.ta;
@@ -471,15 +490,16 @@ bool halo_eligible(const conv_desc& d) {
 HaloGeom halo_geom(const conv_desc& d, const Schedule& s, int mode) {
   HaloGeom h{};
   const int mult = mode == PSCONV_MODE_3XTF32 ? 2 : 1;
-  h.hw = static_cast<int>(d.ofw + d.kw - 1);
+  h.hw = s.tc ? 32 : static_cast<int>(d.ofw + d.kw - 1);
   h.hr = s.pb + static_cast<int>(d.kh) - 1;
   h.a_tile = h.hr * h.hw * 64;
-  // the last block's shifted operands read up to (kh-1)*hw + kw-1 + 127 rows in
+  // the last block's shifted operands read up to (kh-1)*hw + kw-1 + 127 rows in (tap
+  // concat: the ki shift moves to the epilogue, the operands start at kj*hw)
   const int rows = (s.kps - 1) * h.hr * h.hw + static_cast<int>(d.kh - 1) * h.hw +
-                   static_cast<int>(d.kw - 1) + 128;
+                   (s.tc ? 0 : static_cast<int>(d.kw - 1)) + 128;
   h.a_lo_off = (rows * 64 + 1023) / 1024 * 1024;
   h.a_stage = h.a_lo_off * mult;
-  h.b_lo_off = s.kps * (s.bn / s.cs) * 64;
+  h.b_lo_off = s.kps * (s.bn / s.cs) * (s.tc ? static_cast<int>(d.kw) : 1) * 64;
   h.b_stage = h.b_lo_off * mult;
   return h;
 }
@@ -506,7 +526,7 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
       Schedule t = s;
       t.kps = k;
       const HaloGeom h = halo_geom(d, t, mode);
-      const int64_t bres = int64_t(d.kh * d.kw) * (Cb / k) * h.b_stage;
+      const int64_t bres = int64_t(s.tc ? d.kh : d.kh * d.kw) * (Cb / k) * h.b_stage;
       const int64_t left = kSmemStageBudget - bres;
       const int a = left > 0 ? static_cast<int>(std::min<int64_t>(8, left / h.a_stage)) : 0;
       if (a >= 2) {

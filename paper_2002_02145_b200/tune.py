@@ -81,6 +81,12 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     if (mode == "3xtf32" and preset.stride_h == preset.stride_w == 1 and preset.kh * preset.kw > 1
             and bn <= 64 and ksteps <= 40):
         alts.append({"bn": str(bn), "halo": "1", "ch": str(ksteps), "eg": "2"})
+    # TF32 tap concat (halo rows pitched at 32 px, one N = 3 bn MMA per filter row): the
+    # K <= 64 3x3 layers, where N = 64 MMAs run at 2/3 of the tensor rate
+    if (mode == "tf32" and preset.kh == preset.kw == 3 and preset.stride_h == preset.stride_w == 1
+            and preset.nOfm <= 64 and preset.nOfm % 16 == 0):
+        for extra in ({}, {"eg": "2"}, {"br": "0"}):
+            alts.append({"bn": str(preset.nOfm), "tc": "1", "cl": "1", **extra})
     # few-channel kernel (conv_pp.cuh) when at most 4 input channels are real: tap pairs
     # straight from the input's parity planes, no folded copy
     if (0 < c_logical <= 4 and preset.nIfm == 16 and preset.stride_h == preset.stride_w <= 2

@@ -723,3 +723,37 @@ def test_empty_image_range_is_a_noop(mode):
     plan.forward(x, w, y, img_begin=2, img_count=0)
     torch.cuda.synchronize()
     assert bool((y == 7.0).all())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    # cfg1's shape (2 column tiles of 30, 4-row tiles), resident filter, single CTA and pair
+    ("conv:4,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,tc:1,cl:1"),
+    ("conv:4,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,tc:1,cl:2"),
+    ("conv:4,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,tc:1,cl:2,kg:1"),
+    # B ring instead of the resident filter, two epilogue groups
+    ("conv:4,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,tc:1,cl:1,br:0"),
+    ("conv:4,64,64,56,56,3,3,1,1,16,1,1,56,56", 64, "gpu=bn:64,tc:1,cl:1,eg:2"),
+    # ragged tiles (21 rows = 5 x 4 + 1, 19 < 30 columns), Cb = 3, bn 32 / 16, unpadded
+    ("conv:3,32,48,21,19,3,3,1,1,16,1,1,21,19", 48, "gpu=bn:32,tc:1"),
+    ("conv:2,16,32,9,40,3,3,1,1,16,1,1,9,40", 32, "gpu=bn:16,tc:1,br:0"),
+    ("conv:2,64,32,10,33,3,3,1,1,16,0,0,12,35", 32, "gpu=bn:64,tc:1,cl:2"),
+])
+def test_tap_concat(conv, c_log, recipe):
+    """TF32 tap concat (recipe tc:1): per filter row one N = 3 bn MMA over shared halo rows
+    pitched at 32 pixels; the epilogue adds D_ki shifted by ki rows with warp shuffles."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("tc", conv, c_log, 23, "tf32", n, recipe)
+
+
+@pytest.mark.gpu
+def test_tap_concat_rejected_outside_its_domain():
+    for conv, mode, recipe in [
+        ("conv:2,64,64,8,8,3,3,1,1,16,1,1,8,8", "3xtf32", "gpu=bn:64,tc:1"),   # TF32 only
+        ("conv:2,128,64,8,8,3,3,1,1,16,1,1,8,8", "tf32", "gpu=bn:128,tc:1"),  # N = 3 bn > 192
+        ("conv:2,128,64,8,8,3,3,1,1,16,1,1,8,8", "tf32", "gpu=bn:64,tc:1"),   # two N tiles
+        ("conv:2,64,64,8,8,3,3,2,2,16,1,1,16,16", "tf32", "gpu=bn:64,tc:1"),  # stride 2
+        ("conv:2,64,64,8,8,5,5,1,1,16,2,2,8,8", "tf32", "gpu=bn:64,tc:1"),    # 5x5
+    ]:
+        with pytest.raises(ps.ConfigRejectedError):
+            ps.ConvPlan(ps.ConvPreset.parse(conv), mode=mode, device=0, recipe=recipe)
