@@ -148,8 +148,13 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // 3xTF32 at BN <= 64 outside halo mode (N-concat): per K half one N = 2 BN MMA
   // (A_hi x [B_hi;B_lo]) + one N = BN MMA (A_lo x B_hi) instead of three N = BN
   const bool ncat = x3 && s.bn <= 64 && std::max(1, s.cs) == 1;
-  const double mma_cyc = ncat ? 2.0 * (std::max(double(s.bn), 46.0) + std::max(s.bn / 2.0, 46.0))
-                              : 2.0 * mult * std::max(s.bn / 2.0, 46.0);
+  double mma_cyc = ncat ? 2.0 * (std::max(double(s.bn), 46.0) + std::max(s.bn / 2.0, 46.0))
+                        : 2.0 * mult * std::max(s.bn / 2.0, 46.0);
+  // tap concat (TF32 halo, tc:1): one N = 3 bn MMA per filter row covers three taps
+  if (s.tc) mma_cyc = 2.0 * std::max(1.5 * s.bn, 46.0) / 3.0;
+  // TMEM-resident A: the splitter's tcgen05.st traffic slows the TS MMAs that read the
+  // same tensor memory (tools/probe_kstep.cu: the N-concat k-step 192 -> ~296 cycles)
+  if (x3 && s.tmem_a) mma_cyc *= 1.5;
   // Operand delivery is bounded by TMA/L2 row requests, not bytes: ~0.75 rows
   // per cycle per SM with every SM loading, for 64-B and 128-B rows alike
   // (tools/probe_tma_issue.cu). A rows are 64 B (NCHW16c pixels); filter rows
@@ -161,12 +166,19 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
     // halo mode: the (Pb + R - 1) x (Q + S - 1) halo of a channel block is loaded
     // once for its R*S taps; the filter is resident (b_res: loaded once per CTA)
     // or streamed per tap through the B ring
-    const double halo_rows = double(s.pb + g.R - 1) * (g.Q + g.S - 1) / (double(g.R) * g.S);
+    const double hw = s.tc ? 32.0 : double(g.Q + g.S - 1);
+    const double halo_rows = double(s.pb + g.R - 1) * hw / (double(g.R) * g.S);
     rows = halo_rows + (s.b_res ? 0.0 : b_rows * (x3 ? 2 : 1) * (b128 ? 0.5 : 1.0));
     a_bytes = halo_rows * 64.0;
   }
   const double deliver_b = a_bytes + (s.halo && s.b_res ? 0.0 : b_rows * 64.0 * (x3 ? 2 : 1));
-  const double del_cyc = rows / m.row_requests_per_cycle;
+  // strided layers: every A row is an isolated 64-B pixel; boxes taking few pixels per
+  // image spread the requests over many DRAM pages and the row delivery slows (r02 tuner
+  // rows, l3 ds 1x1/s2: box 1x1x128 1.7x slower than 2x2x32)
+  const double ppi = double(s.qb) * s.pb;  // pixels per image in the box
+  const double a_rows = s.halo ? rows : double(s.qb) * s.pb * s.nb;
+  const double a_eff = (d.stride_h > 1 || d.stride_w > 1) ? 0.5 + 0.5 * std::min(1.0, ppi / 4.0) : 1.0;
+  const double del_cyc = (rows + a_rows * (1.0 / a_eff - 1.0)) / m.row_requests_per_cycle;
   // operand reads per k-step: 2 K-halves x (A 4 KB + B rows x 32 B) per MMA; with
   // TMEM-resident A (3xTF32) the MMAs read only B and the splitter reads A once
   const double tc_reads = 2.0 * mult * ((s.tmem_a ? 0.0 : 4096.0) + b_rows * 32.0);
@@ -188,6 +200,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
     const bool fast = g.R == 3 && g.S == 3 && (s.chunk <= 0 || s.chunk >= ksteps);
     stage_cyc = fast ? (s.b_res ? 300.0 / 9.0 : 60.0) : 300.0;
   }
+  // the CTA pair synchronises its two CTAs per stage (the leader waits for both CTAs'
+  // loads): ~200 cycles a stage, which only the wide-N (MMA-bound) layers hide
+  if (cs == 2) stage_cyc += 100.0;
   kstep_cyc = std::max(kstep_cyc, del_cyc) + stage_cyc / std::max(1, s.kps);
   const int chunk = s.chunk > 0 ? s.chunk : static_cast<int>(ksteps);
   const double nchunks = std::ceil(double(ksteps) / chunk);
@@ -204,13 +219,22 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // (kt:1 splits every tile: no whole-tile waves)
   const int64_t waves = s.split_all && ks > 1 ? 0 : groups / clusters, rem = groups - waves * clusters;
   const int kt = rem > 0 ? ks : 1;
-  const double tile_cyc = double(ksteps) * kstep_cyc + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
+  // Epilogue throughput (CTA-0 clock traces, r02): ~1000 cycles per 32-channel round
+  // (TMEM load, staging, store-warp handoff; ~1300 with the tap-concat's three loads),
+  // EG groups in parallel, ~+500 per round for every non-last 3xTF32 chunk (running
+  // sum); double-buffered, so a tile costs max(mainloop, epilogue). The CTA pair couples
+  // both CTAs' epilogues on one accumulator release (~1.3x when it binds).
+  const double rounds = std::max(1.0, s.bn / 32.0);
+  const double epi_tile = rounds * ((s.tc ? 1300.0 : 1000.0) + (nchunks - 1.0) * 500.0) /
+                          (s.egroups == 2 ? 1.2 : 1.0) * (cs == 2 ? 1.6 : 1.0);
+  const double main_tile = double(ksteps) * kstep_cyc;
+  const double tile_cyc = std::max(main_tile, epi_tile) + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
   // (a split unit also refills the pipeline (~1500 cycles) and writes its
   // 128 x BN fp32 partial to the workspace; the last unit of the tile then reads
   // all kt partials back in split order before its store (~64 B/cycle each way;
   // r01 A/B fit of the refill, conv_kernel.cuh ConvParams::split_ctr)
-  const double split_cyc = 1500.0 + (1.0 + ks) * 128.0 * s.bn * 4.0 / 64.0;
-  const double unit_cyc = double(ksteps) / kt * kstep_cyc +
+  const double split_cyc = 3000.0 + (1.0 + ks) * 128.0 * s.bn * 4.0 / 64.0;
+  const double unit_cyc = std::max(double(ksteps) / kt * kstep_cyc, epi_tile) +
                           (drain_exposed ? nchunks / kt * drain_cyc : drain_cyc) + (kt > 1 ? split_cyc : 0.0);
   double tail_units = std::ceil(double(rem) * kt / clusters);
   // a partial wave of whole tiles runs faster than a full one (fewer SMs share
@@ -235,7 +259,9 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
                                               tn == 1);
   double in_reads = 1.0;
   if (ofm_outer && tk > 1 && in_b + flt_b > m.l2_bytes) in_reads = double(tk);
-  b.hbm_bytes = in_b * in_reads + flt_b + out_b;
+  // (1x1 strided layers touch 1 / (sh * sw) of the input)
+  const double touched = (g.R == 1 && g.S == 1) ? 1.0 / (d.stride_h * d.stride_w) : 1.0;
+  b.hbm_bytes = in_b * touched * in_reads + flt_b + out_b;
   // split-K: every unit of a split tile writes its partial to the workspace and the
   // last reads them all back (mostly in L2, partly written back to HBM)
   if (kt > 1) b.hbm_bytes += 0.5 * out_b * double(s.split_all ? groups : rem) / groups * kt;
@@ -292,6 +318,25 @@ std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
           // the halo tile does not fit at this bn
         }
       }
+  // tap concat (TF32, 3x3 stride 1, nOfm <= 64: one N = 3 nOfm MMA per filter row),
+  // single CTA and pair, one or two epilogue groups
+  if (mode == PSCONV_MODE_TF32 && d.kh == 3 && d.kw == 3 && d.stride_h == 1 && d.stride_w == 1 &&
+      d.nOfm <= 64)
+    for (const char* perm : kPerms)
+      for (int cs : {1, 2})
+        for (int eg : {1, 2}) {
+          Recipe r = Recipe::parse(std::string("perm=") + perm);
+          r.has_gpu = true;
+          r.bn = static_cast<int>(d.nOfm);
+          r.tc = 1;
+          r.cs = cs;
+          r.eg = eg == 2 ? 2 : 0;
+          try {
+            Schedule s = resolve_schedule(d, r, mode);
+            if (seen.insert(s.recipe_id).second) out.push_back(s);
+          } catch (const ConfigError&) {
+          }
+        }
   return out;
 }
 
