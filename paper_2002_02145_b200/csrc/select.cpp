@@ -29,6 +29,21 @@
 namespace psconv {
 
 namespace {
+#ifndef EPI_FIX
+#define EPI_FIX 800.0
+#endif
+#ifndef EPI_ROUND
+#define EPI_ROUND 700.0
+#endif
+#ifndef EPI_TC
+#define EPI_TC 1000.0
+#endif
+#ifndef EPI_EG
+#define EPI_EG 1.2
+#endif
+#ifndef EPI_PAIR
+#define EPI_PAIR 1.3
+#endif
 
 // B200 machine model. Peaks: defaults from an earlier pod's MEASURED_PEAKS.json;
 // the Python layer loads this pod's file at import (conv_select_set_machine:
@@ -225,8 +240,8 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // sum); double-buffered, so a tile costs max(mainloop, epilogue). The CTA pair couples
   // both CTAs' epilogues on one accumulator release (~1.3x when it binds).
   const double rounds = std::max(1.0, s.bn / 32.0);
-  const double epi_tile = rounds * ((s.tc ? 1300.0 : 1000.0) + (nchunks - 1.0) * 500.0) /
-                          (s.egroups == 2 ? 1.2 : 1.0) * (cs == 2 ? 1.6 : 1.0);
+  const double epi_tile = (EPI_FIX + rounds * ((s.tc ? EPI_TC : EPI_ROUND) + (nchunks - 1.0) * 250.0)) /
+                          (s.egroups == 2 ? EPI_EG : 1.0) * (cs == 2 ? EPI_PAIR : 1.0);
   const double main_tile = double(ksteps) * kstep_cyc;
   const double tile_cyc = std::max(main_tile, epi_tile) + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
   // (a split unit also refills the pipeline (~1500 cycles) and writes its
