@@ -2,7 +2,7 @@ cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_sw.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_sw.log
 for lib in libpsconv_base.so libpsconv.so; do
   echo "== $lib"
-  PSCONV_LIB_NAME=$lib python tools/ab_sweep.py profiles/r02_sweep_tuned.jsonl --steps 10
+  PSCONV_LIB_NAME=$lib python tools/ab_sweep.py profiles/r02_sweep_first.jsonl --steps 10
 done > gpurun_out/ab_sw.log 2>&1
 python tools/ab_cmp.py gpurun_out/ab_sw.log
 grep geomean gpurun_out/ab_sw.log
