@@ -135,14 +135,18 @@ int conv_plan_create(const conv_desc* d, int mode, int device, const char* recip
                      conv_plan** out);
 
 /* Backward-data plan (neighbouring ops): for the FORWARD
- * descriptor d (stride 1), a plan whose conv_fwd / conv_fwd_host computes
- * dX = dL/dInput from dY = dL/dOutput and the forward filter:
+ * descriptor d, a plan whose conv_fwd / conv_fwd_host computes dX = dL/dInput
+ * from dY = dL/dOutput and the forward filter:
  *   in  = dY  [N][nOfm/16][ofh][ofw][16]   (NKPQ16k of the forward output)
  *   flt = W   KCRS16c16k of the forward layer (transposed and flipped inside)
  *   out = dX  [N][nIfm/16][ifh][ifw][16]   (NCHW16c of the forward input)
- * i.e. the transposed convolution conv(dY, W^T flipped, pad = k - 1 - pad) on the
- * same kernel; conv_plan_recipe reports the transposed layer's schedule.
- * Returns 0 / 2 (stride > 1) / 1. */
+ * Stride 1: the transposed convolution conv(dY, W^T flipped, pad = k - 1 - pad) on
+ * the same kernel. Stride s > 1: dX splits into stride_h x stride_w output phases
+ * (h mod stride_h, w mod stride_w); each is a stride-1 transposed conv over dY with
+ * the phase's forward taps (r = stride_h*u + rho) and asymmetric implied padding,
+ * stored through a strided view of dX (phases without taps, e.g. 3 of 4 for a 1x1
+ * stride-2 layer, are zero-filled). conv_plan_recipe lists the phases' schedules.
+ * Returns 0 / 2 (a phase would need negative padding, e.g. 2x2 / stride 2 / pad 1) / 1. */
 int conv_plan_create_bwd_data(const conv_desc* d, int mode, int device, const char* recipe_or_null,
                               conv_plan** out);
 /* Backward-weight plan: for the FORWARD descriptor d (stride 1,

@@ -194,8 +194,9 @@ class ConvPlan:
 
     def __init__(self, preset: ConvPreset, mode="3xtf32", device: int = 0,
                  recipe: str | None = None, bwd_data: bool = False):
-        """bwd_data=True: the backward-data plan of the (stride-1) forward layer `preset`;
-        forward(dy, w, dx) then computes dX from dY (NKPQ16k) and the forward filter."""
+        """bwd_data=True: the backward-data plan of the forward layer `preset`; forward(dy, w,
+        dx) then computes dX from dY (NKPQ16k) and the forward filter (strided layers: one
+        stride-1 transposed conv per output phase, C ABI conv_plan_create_bwd_data)."""
         if isinstance(mode, str):
             mode = _MODES[mode.lower()]
         self.preset = ConvPreset(**{f.name: getattr(preset, f.name) for f in fields(preset)}).validate()

@@ -50,6 +50,16 @@ struct conv_plan {
   bool bwd_data = false;
   conv_desc fwd{};                // the forward layer's descriptor
   float* wtrans = nullptr;
+  // strided backward data (stride s > 1): dX splits into sh x sw output phases (a, b) =
+  // (h mod sh, w mod sw). Phase (a, b) is a stride-1 transposed conv over dY whose taps are
+  // the forward taps r = sh*u + rho_h, s = sw*v + rho_w (flipped), with asymmetric implied
+  // padding; a child plan runs it and stores through a strided view of dX (out_sh/out_sw
+  // over the parent extent out_H x out_W). Phases without taps are zero-filled.
+  std::vector<conv_plan*> phase_plans;  // parent: one child per phase with taps
+  std::vector<std::pair<int, int>> zero_phases;
+  int ph_a = 0, ph_b = 0, ph_rho_h = 0, ph_rho_w = 0;  // child: its phase and first taps
+  int out_sh = 1, out_sw = 1;
+  int64_t out_H = 0, out_W = 0;
   // backward-weight plan (conv_plan_create_bwd_weight): d is the role-swapped conv
   // (images = forward input channels, channels = batch, filter = dY); scratch for
   // the transposed input, dY as that conv's KCRS16c16k filter, and its output
@@ -536,10 +546,13 @@ __global__ void fold_filter_kernel(const float* __restrict__ flt, float* __restr
 }
 
 // Backward data: the forward filter KCRS16c16k [Kb][Cb][R][S][16c][16k] becomes the
-// filter of the transposed conv, [Cb][Kb][R][S][16k][16c] with the taps flipped:
-// W'[c][k][r][s] = W[k][c][R-1-r][S-1-s].
+// filter of the transposed conv, [Cb][Kb][U][V][16k][16c] with the taps flipped:
+// W'[c][k][u][v] = W[k][c][sh*(U-1-u) + rho_h][sw*(V-1-v) + rho_w] -- for stride 1
+// (U, V = R, S, rho = 0) W[k][c][R-1-u][S-1-v]; for a phase of a strided layer the
+// forward taps of that phase (r = rho_h mod sh, s = rho_w mod sw).
 __global__ void bwd_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int64_t n_elems,
-                                  int Kb, int Cb, int R, int S) {
+                                  int Kb, int Cb, int R, int S, int U, int V, int sh, int sw, int rho_h,
+                                  int rho_w) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_elems;
        e += int64_t(gridDim.x) * blockDim.x) {
     int64_t t = e;
@@ -547,21 +560,40 @@ __global__ void bwd_filter_kernel(const float* __restrict__ w, float* __restrict
     t >>= 4;
     const int k16 = int(t & 15);  // its input channel (forward output k)
     t >>= 4;
-    const int s = int(t % S);
-    t /= S;
-    const int r = int(t % R);
-    t /= R;
+    const int v = int(t % V);
+    t /= V;
+    const int u = int(t % U);
+    t /= U;
     const int kb = int(t % Kb);
     const int cb = int(t / Kb);
-    out[e] = w[((((int64_t(kb) * Cb + cb) * R + (R - 1 - r)) * S + (S - 1 - s)) * 16 + c16) * 16 + k16];
+    const int r = sh * (U - 1 - u) + rho_h, s = sw * (V - 1 - v) + rho_w;
+    out[e] = w[((((int64_t(kb) * Cb + cb) * R + r) * S + s) * 16 + c16) * 16 + k16];
   }
 }
 
 void launch_bwd_filter(const conv_plan* P, const float* flt, cudaStream_t st) {
-  const int64_t n = P->fwd.nOfm * P->fwd.nIfm * P->fwd.kh * P->fwd.kw;
-  bwd_filter_kernel<<<grid_for(n), 256, 0, st>>>(flt, P->wtrans, n, int(P->fwd.nOfm / 16),
-                                                 int(P->fwd.nIfm / 16), int(P->fwd.kh), int(P->fwd.kw));
+  const conv_desc& f = P->fwd;
+  const int U = int(P->d.kh), V = int(P->d.kw);
+  const int64_t n = f.nOfm * f.nIfm * U * V;
+  bwd_filter_kernel<<<grid_for(n), 256, 0, st>>>(flt, P->wtrans, n, int(f.nOfm / 16), int(f.nIfm / 16),
+                                                 int(f.kh), int(f.kw), U, V, int(f.stride_h),
+                                                 int(f.stride_w), P->ph_rho_h, P->ph_rho_w);
   CUDA_OK(cudaGetLastError());
+}
+
+// dX positions of a phase without filter taps (h = a mod sh, w = b mod sw): zero
+__global__ void zero_phase_kernel(float* __restrict__ out, int64_t n_px, int H, int W, int Ha, int Wb,
+                                  int sh, int sw, int a, int b) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_px * 4;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e >> 2;  // (img, cb, i, j) of the phase; 4 float4 per 16-channel pixel
+    const int j = int(t % Wb);
+    t /= Wb;
+    const int i = int(t % Ha);
+    t /= Ha;  // img * Cb + cb
+    const int64_t px = (t * H + int64_t(sh) * i + a) * W + int64_t(sw) * j + b;
+    reinterpret_cast<float4*>(out + px * 16)[e & 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 void launch_fold_filter(const conv_plan* P, const float* flt, cudaStream_t st) {
@@ -820,6 +852,24 @@ void launch_pp(const conv_plan* P, const float* in, const float* flt, float* out
 void launch_range(const conv_plan* P, const float* in, const float* flt, float* out, int64_t img_count,
                   cudaStream_t st, unsigned flags, const float* bias = nullptr) {
   const bool prepacked = (flags & PSCONV_FLAG_PREPACKED) != 0;
+  if (!P->phase_plans.empty() || !P->zero_phases.empty()) {
+    // strided backward data: one stride-1 transposed conv per output phase, each storing
+    // through its strided view of dX (out + the phase's first pixel); tap-less phases zeroed
+    const conv_desc& f = P->fwd;
+    const int H = int(f.ifh), W = int(f.ifw), sh = int(f.stride_h), sw = int(f.stride_w);
+    for (const conv_plan* c : P->phase_plans)
+      launch_range(c, in, flt, out + (int64_t(c->ph_a) * W + c->ph_b) * 16, img_count, st, flags, bias);
+    if (!(flags & PSCONV_FLAG_ACCUMULATE))
+      for (const auto& ab : P->zero_phases) {
+        const int Ha = (H - ab.first + sh - 1) / sh, Wb = (W - ab.second + sw - 1) / sw;
+        const int64_t n_px = img_count * (f.nIfm / 16) * Ha * Wb;
+        zero_phase_kernel<<<grid_for(n_px * 4), 256, 0, st>>>(out, n_px, H, W, Ha, Wb, sh, sw, ab.first,
+                                                              ab.second);
+        CUDA_OK(cudaGetLastError());
+      }
+    if (!prepacked) P->prepacked = false;
+    return;
+  }
   if (P->pp) {
     if (bias || (flags & PSCONV_FLAG_RELU)) throw ConfigError("gpu pp kernel: no fused bias/ReLU epilogue");
     return launch_pp(P, in, flt, out, img_count, st, flags);
@@ -856,11 +906,15 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
   // output viewed as [img_count][Kb][P][Q][16] from the first image; the box is
   // the pixel tile (no stride factor); stores outside the layer are clipped
   {
+    // (a phase of a strided backward-data plan stores every out_sw-th pixel of every
+    // out_sh-th row of the parent's out_H x out_W output)
     const float* base = out;
+    const cuuint64_t oH = P->out_H ? cuuint64_t(P->out_H) : cuuint64_t(Pp);
+    const cuuint64_t oW = P->out_W ? cuuint64_t(P->out_W) : cuuint64_t(Q);
     const cuuint64_t dims[5] = {16, cuuint64_t(Q), cuuint64_t(Pp), cuuint64_t(Kb),
                                 cuuint64_t(img_count)};
-    const cuuint64_t strides[4] = {64, cuuint64_t(Q) * 64, cuuint64_t(Pp) * Q * 64,
-                                   cuuint64_t(Kb) * Pp * Q * 64};
+    const cuuint64_t strides[4] = {64 * cuuint64_t(P->out_sw), oW * 64 * P->out_sh, oH * oW * 64,
+                                   cuuint64_t(Kb) * oH * oW * 64};
     const cuuint32_t box[5] = {16, cuuint32_t(s.qb), cuuint32_t(s.pb), 1, cuuint32_t(s.nb)};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     encode(&tout, base, 5, dims, strides, box, estr);
@@ -1087,25 +1141,14 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
 }  // namespace
 }  // namespace psconv
 
-using namespace psconv;
-
-extern "C" {
-
-int psconv_device_sm_count(int device) {
-  int n = 0;
-  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  return n;
-}
-
-int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* recipe,
-                     conv_plan** out) {
-  return guarded([&] {
-    if (!d_in || !out) throw ConfigError("null argument");
-    *out = nullptr;
+namespace psconv {
+namespace {
+// Plan construction for a validated descriptor (conv_plan_create) or for an internal
+// phase conv of a strided backward-data plan, whose implied bottom padding is asymmetric
+// (the TMA zero-fills the rows past dY; conv_plan_create_bwd_data).
+conv_plan* create_plan(const conv_desc& d, int mode, int device, const char* recipe) {
     if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32 && mode != PSCONV_MODE_F16X2)
       throw ConfigError("unknown mode " + std::to_string(mode));
-    conv_desc d = *d_in;
-    validate_desc(d);
     Recipe r;
     Schedule s;
     conv_desc kd = d;
@@ -1210,7 +1253,30 @@ int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* re
         throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
       }
     }
-    *out = P;
+    return P;
+}
+}  // namespace
+}  // namespace psconv
+
+using namespace psconv;
+
+extern "C" {
+
+int psconv_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+
+int conv_plan_create(const conv_desc* d_in, int mode, int device, const char* recipe,
+                     conv_plan** out) {
+  return guarded([&] {
+    if (!d_in || !out) throw ConfigError("null argument");
+    *out = nullptr;
+    conv_desc d = *d_in;
+    validate_desc(d);
+    *out = create_plan(d, mode, device, recipe);
   });
 }
 
@@ -1221,45 +1287,103 @@ int conv_plan_create_bwd_data(const conv_desc* d_in, int mode, int device, const
     *out = nullptr;
     conv_desc f = *d_in;
     validate_desc(f);
-    if (f.stride_h != 1 || f.stride_w != 1)
-      throw ConfigError("backward data: only stride-1 layers are supported (stride " +
-                        std::to_string(f.stride_h) + "x" + std::to_string(f.stride_w) + ")");
-    if (f.kh - 1 - f.pad_h < 0 || f.kw - 1 - f.pad_w < 0)
-      throw ConfigError("backward data: padding larger than kernel - 1");
-    // dX = conv(dY, W^T flipped): images stay, channels swap, the output is the
-    // forward input extent, padding kernel - 1 - pad
-    conv_desc t{};
-    t.nImg = f.nImg;
-    t.nOfm = f.nIfm;
-    t.nIfm = f.nOfm;
-    t.ofh = f.ifh;
-    t.ofw = f.ifw;
-    t.kh = f.kh;
-    t.kw = f.kw;
-    t.stride_h = t.stride_w = 1;
-    t.gemm_block = f.gemm_block;
-    t.pad_h = f.kh - 1 - f.pad_h;
-    t.pad_w = f.kw - 1 - f.pad_w;
-    t.ifh = f.ofh;
-    t.ifw = f.ofw;
-    conv_plan* P = nullptr;
-    const int rc = conv_plan_create(&t, mode, device, recipe, &P);
-    if (rc != PSCONV_OK) {
-      if (rc == PSCONV_ERR_CONFIG) throw ConfigError(conv_last_error());
-      throw RuntimeError(conv_last_error());
+    const int64_t sh = f.stride_h, sw = f.stride_w;
+    // Output phase (a, b) of dX: h = sh*i + a reads dY rows p = i + c_a - u through the
+    // forward taps r = sh*u + rho_a, rho_a = (a + pad_h) mod sh, u < U_a = ceil((kh - rho_a)
+    // / sh), c_a = (a + pad_h - rho_a) / sh -- i.e. the stride-1 conv of dY with the taps
+    // flipped (u' = U_a - 1 - u) and top padding U_a - 1 - c_a (the bottom padding is
+    // whatever the phase needs: rows past dY are TMA zero fill). Stride 1: one phase,
+    // padding kh - 1 - pad_h (the plain transposed conv).
+    std::vector<conv_plan*> kids;
+    std::vector<std::pair<int, int>> zeros;
+    auto cleanup = [&] {
+      for (conv_plan* c : kids) conv_plan_destroy(c);
+    };
+    try {
+      for (int64_t a = 0; a < sh; ++a)
+        for (int64_t b = 0; b < sw; ++b) {
+          const int64_t Ha = (f.ifh - a + sh - 1) / sh, Wb = (f.ifw - b + sw - 1) / sw;
+          if (Ha <= 0 || Wb <= 0) continue;
+          const int64_t rh = (a + f.pad_h) % sh, rw = (b + f.pad_w) % sw;
+          const int64_t U = f.kh > rh ? (f.kh - rh + sh - 1) / sh : 0;
+          const int64_t V = f.kw > rw ? (f.kw - rw + sw - 1) / sw : 0;
+          if (U == 0 || V == 0) {
+            zeros.emplace_back(int(a), int(b));
+            continue;
+          }
+          const int64_t ch = (a + f.pad_h - rh) / sh, cw = (b + f.pad_w - rw) / sw;
+          conv_desc t{};
+          t.nImg = f.nImg;
+          t.nOfm = f.nIfm;
+          t.nIfm = f.nOfm;
+          t.ofh = Ha;
+          t.ofw = Wb;
+          t.kh = U;
+          t.kw = V;
+          t.stride_h = t.stride_w = 1;
+          t.gemm_block = f.gemm_block;
+          t.pad_h = U - 1 - ch;
+          t.pad_w = V - 1 - cw;
+          t.ifh = f.ofh;
+          t.ifw = f.ofw;
+          if (t.pad_h < 0 || t.pad_w < 0)
+            throw ConfigError("backward data: this stride / padding combination needs a negative phase "
+                              "padding (unsupported)");
+          if (sh == 1 && sw == 1) validate_desc(t);  // the plain transposed conv is a valid layer
+          conv_plan* c = create_plan(t, mode, device, recipe);
+          kids.push_back(c);
+          c->bwd_data = true;
+          c->fwd = f;
+          c->ph_a = int(a);
+          c->ph_b = int(b);
+          c->ph_rho_h = int(rh);
+          c->ph_rho_w = int(rw);
+          if (sh > 1 || sw > 1) {
+            c->out_sh = int(sh);
+            c->out_sw = int(sw);
+            c->out_H = f.ifh;
+            c->out_W = f.ifw;
+          }
+          DeviceGuard guard(device);
+          const cudaError_t e = cudaMalloc(&c->wtrans, size_t(f.nOfm) * f.nIfm * U * V * sizeof(float));
+          if (e != cudaSuccess) throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+      if (sh == 1 && sw == 1) {
+        *out = kids.at(0);
+        return;
+      }
+      // strided: a parent plan holding the phases; its descriptor is the whole transposed
+      // layer (dY in, dX out: the sizes conv_fwd / conv_fwd_host check and stage)
+      auto* P = new conv_plan();
+      P->d = f;
+      P->d.nOfm = f.nIfm;
+      P->d.nIfm = f.nOfm;
+      P->d.ofh = f.ifh;
+      P->d.ofw = f.ifw;
+      P->d.ifh = f.ofh;
+      P->d.ifw = f.ofw;
+      P->kd = P->d;
+      P->mode = mode;
+      P->device = device;
+      P->num_sms = kids.empty() ? 0 : kids[0]->num_sms;
+      P->bwd_data = true;
+      P->fwd = f;
+      P->user_flt_elems = f.nOfm * f.nIfm * f.kh * f.kw;
+      P->phase_plans = kids;
+      P->zero_phases = zeros;
+      std::string id;
+      for (const conv_plan* c : kids)
+        id += (id.empty() ? "" : " | ") + std::string("phase ") + std::to_string(c->ph_a) + "," +
+              std::to_string(c->ph_b) + ": " + c->sched.recipe_id;
+      for (const auto& z : zeros)
+        id += (id.empty() ? "" : " | ") + std::string("phase ") + std::to_string(z.first) + "," +
+              std::to_string(z.second) + ": zero";
+      P->sched.recipe_id = id;
+      *out = P;
+    } catch (...) {
+      cleanup();
+      throw;
     }
-    P->bwd_data = true;
-    P->fwd = f;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(device);
-    const cudaError_t e = cudaMalloc(&P->wtrans, size_t(f.nOfm) * f.nIfm * f.kh * f.kw * sizeof(float));
-    cudaSetDevice(prev);
-    if (e != cudaSuccess) {
-      conv_plan_destroy(P);
-      throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    }
-    *out = P;
   });
 }
 
@@ -1353,6 +1477,7 @@ int conv_bwd_weight(const conv_plan* P, const float* x, const float* dy, float* 
 
 void conv_plan_destroy(conv_plan* p) {
   if (!p) return;
+  for (conv_plan* c : p->phase_plans) conv_plan_destroy(c);
   if (p->pipe) {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -1399,6 +1524,8 @@ int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len) {
   int64_t need = -1;
   const int rc = guarded([&] {
     if (!p) throw ConfigError("null plan");
+    if (!p->phase_plans.empty() || !p->zero_phases.empty())
+      throw ConfigError("a strided backward-data plan is one transposed conv per output phase: no single driver nest");
     const std::string txt = emit_driver(p->d, p->sched);
     need = static_cast<int64_t>(txt.size());
     if (buf && len) {
@@ -1411,7 +1538,13 @@ int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len) {
 }
 
 int conv_plan_launches(const conv_plan* p) {
-  return p ? 2 : 0;  // filter prepack + conv
+  if (!p) return 0;
+  if (!p->phase_plans.empty() || !p->zero_phases.empty()) {
+    int n = int(p->zero_phases.size());
+    for (const conv_plan* c : p->phase_plans) n += conv_plan_launches(c);
+    return n;
+  }
+  return 2 + (p->bwd_data ? 1 : 0);  // (backward data: filter transform +) filter prepack + conv
 }
 
 int conv_fwd_ex(const conv_plan* P, const float* in, const float* flt, float* out, const float* bias,
@@ -1452,7 +1585,11 @@ int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
     if (!P || !flt) throw ConfigError("null argument");
     if (reinterpret_cast<uintptr_t>(flt) & 15) throw ConfigError("filter must be 16-byte aligned");
     DeviceGuard guard(P->device);
-    launch_prepack(P, flt, static_cast<cudaStream_t>(stream));
+    for (conv_plan* c : P->phase_plans) {  // strided backward data: every phase's filter
+      launch_prepack(c, flt, static_cast<cudaStream_t>(stream));
+      c->prepacked = true;
+    }
+    if (P->phase_plans.empty() && P->zero_phases.empty()) launch_prepack(P, flt, static_cast<cudaStream_t>(stream));
     P->prepacked = true;
   });
 }

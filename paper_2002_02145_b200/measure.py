@@ -193,7 +193,13 @@ class LayerBench:
     # -- single launch after an L2 flush -------------------------------------------------
     def single(self, plan, flush, steps, warmup, prepack_in_step=True):
         """Per-step (repack + conv) and conv-only event times in ms (lists); L2 flushed before
-        every step. With prepack_in_step=False the step is the conv alone (prepacked filter)."""
+        every step. With prepack_in_step=False the step is the conv alone (prepacked filter).
+
+        Two passes of `steps` each: the step pass records events only around the whole step
+        (an event between the repack and the conv launch would serialise them: the conv's
+        prologue overlaps the repack through PDL, so a middle event adds ~6 us to a step of a
+        small layer, tools/step_overhead.py), then the kernel pass times the conv alone on the
+        prepacked filter."""
         torch, st = self.torch, self.stream
 
         def one():
@@ -206,17 +212,22 @@ class LayerBench:
         for _ in range(warmup):
             one()
         torch.cuda.synchronize()
-        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(steps)]
-        for e0, e1, e2 in ev:
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(steps)]
+        for e0, e1 in ev:
             flush()
             e0.record(st)
-            if prepack_in_step:
-                plan.prepack(self.w, st)
+            one()
             e1.record(st)
-            plan.forward(self.x, None, self.y, self.b0, self.n, st, prepacked=True)
-            e2.record(st)
         torch.cuda.synchronize()
-        return [a.elapsed_time(c) for a, _, c in ev], [b.elapsed_time(c) for _, b, c in ev]
+        step = [a.elapsed_time(b) for a, b in ev]
+        plan.prepack(self.w, st)
+        for e0, e1 in ev:
+            flush()
+            e0.record(st)
+            plan.forward(self.x, None, self.y, self.b0, self.n, st, prepacked=True)
+            e1.record(st)
+        torch.cuda.synchronize()
+        return step, [a.elapsed_time(b) for a, b in ev]
 
     # -- steady state: rotating sets, back-to-back launches -------------------------------
     def _rotating_sets(self):

@@ -316,32 +316,43 @@ def test_tmem_resident_a(conv, c_log, recipe):
 
 
 def _bwd_data_ref(p, dy, w):
-    """dX[n][c][h][w] = sum_{k,r,s} dY[n][k][h+p-r][w+p-s] W[k][c][r][s] (float64, NCHW16c)."""
+    """dX[n][c][h][w] = sum over (p, q, r, s) with h = p*sh + r - pad_h, w = q*sw + s - pad_w of
+    dY[n][k][p][q] W[k][c][r][s] (float64, NCHW16c) -- the adjoint of the forward conv."""
     N, K, C = p.nImg, p.nOfm, p.nIfm
     P, Q, R, S, H, W_ = p.ofh, p.ofw, p.kh, p.kw, p.ifh, p.ifw
+    sh, sw = p.stride_h, p.stride_w
     dyl = dy.reshape(N, K // 16, P, Q, 16).transpose(0, 1, 4, 2, 3).reshape(N, K, P, Q).astype(np.float64)
     wl = w.reshape(K // 16, C // 16, R, S, 16, 16).transpose(0, 5, 1, 4, 2, 3).reshape(K, C, R, S)
     dx = np.zeros((N, C, H, W_))
     for r in range(R):
         for s in range(S):
-            for h in range(H):
-                pp = h + p.pad_h - r
-                if not 0 <= pp < P:
-                    continue
-                # columns: q = w + pad - s
-                ws = [x for x in range(W_) if 0 <= x + p.pad_w - s < Q]
-                qs = [x + p.pad_w - s for x in ws]
-                dx[:, :, h, ws] += np.einsum("nkq,kc->ncq", dyl[:, :, pp, qs], wl[:, :, r, s])
+            ps_ = [pp for pp in range(P) if 0 <= pp * sh + r - p.pad_h < H]
+            qs = [q for q in range(Q) if 0 <= q * sw + s - p.pad_w < W_]
+            if not ps_ or not qs:
+                continue
+            hs = [pp * sh + r - p.pad_h for pp in ps_]
+            ws = [q * sw + s - p.pad_w for q in qs]
+            dx[:, :, np.ix_(hs, ws)[0], np.ix_(hs, ws)[1]] += np.einsum(
+                "nkpq,kc->ncpq", dyl[:, :, ps_][:, :, :, qs], wl[:, :, r, s])
     return dx.reshape(N, C // 16, 16, H, W_).transpose(0, 1, 3, 4, 2).ravel()
+
+
+BWD_DATA = ["conv:2,64,32,12,12,3,3,1,1,16,1,1,12,12",
+            "conv:2,32,48,9,11,5,5,1,1,16,2,2,9,11",
+            "conv:3,128,64,7,7,1,1,1,1,16",
+            # strided: one stride-1 transposed conv per output phase (sh x sw of them)
+            "conv:2,64,32,14,14,3,3,2,2,16,1,1,28,28",   # 3x3/s2 (ResNet-50 l2..l4 first 3x3)
+            "conv:2,32,48,7,7,3,3,2,2,16,1,1,13,13",     # odd extent: phases of 7 and 6 rows
+            "conv:2,64,32,7,7,1,1,2,2,16,0,0,14,14",     # 1x1/s2 downsample: 3 phases zero
+            "conv:2,64,16,8,8,7,7,2,2,16,3,3,16,16",     # 7x7/s2 (stem-shaped)
+            "conv:2,32,32,5,9,3,1,2,1,16,1,0,10,9"]      # stride only in h
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["3xtf32", "tf32", "f16x2"])
-@pytest.mark.parametrize("conv", ["conv:2,64,32,12,12,3,3,1,1,16,1,1,12,12",
-                                  "conv:2,32,48,9,11,5,5,1,1,16,2,2,9,11",
-                                  "conv:3,128,64,7,7,1,1,1,1,16"])
+@pytest.mark.parametrize("conv", BWD_DATA)
 def test_backward_data(conv, mode):
-    """§8f row f4: dX of a stride-1 layer as the transposed conv on the same kernel."""
+    """§8f row f4: dX as the transposed conv on the same kernel (strided layers: per phase)."""
     p = ps.ConvPreset.parse(conv)
     rng = np.random.default_rng(3)
     dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
@@ -356,9 +367,42 @@ def test_backward_data(conv, mode):
 
 
 @pytest.mark.gpu
-def test_backward_data_rejects_strided():
+def test_backward_data_strided_paths():
+    """Strided backward data through the other entry points: accumulate (+=, zero phases left
+    alone), a prepacked filter, an image range, and the host-buffer path."""
+    p = ps.ConvPreset.parse("conv:4,64,32,7,7,1,1,2,2,16,0,0,14,14")
+    rng = np.random.default_rng(5)
+    dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
+    w = rng.uniform(-1, 1, p.filter_elems()).astype(np.float32)
+    base = rng.uniform(-1, 1, p.input_elems()).astype(np.float32)
+    ref = _bwd_data_ref(p, dy, w)
+    plan = ps.ConvPlan(p, mode="3xtf32", device=0, bwd_data=True)
+    assert plan.recipe.count("phase") == 4 and plan.launches == 3 + 3
+    dyd, wd = torch.from_numpy(dy).cuda(), torch.from_numpy(w).cuda()
+    dx = torch.from_numpy(base.copy()).cuda()
+    plan.forward(dyd, wd, dx, accumulate=True)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(dx.cpu().numpy(), ref + base) <= 1e-5
+    plan.prepack(wd)
+    per = p.input_elems() // p.nImg
+    dx = torch.full((p.input_elems(),), float("nan"), device="cuda:0")
+    plan.forward(dyd, None, dx, img_begin=1, img_count=2, prepacked=True)
+    torch.cuda.synchronize()
+    got = dx.cpu().numpy()[per:3 * per]
+    assert oracle.rel_l2(got, ref[per:3 * per]) <= 1e-5
+    hx = np.full(p.input_elems(), np.nan, dtype=np.float32)
+    plan.forward_host(dy, w, hx)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(hx, ref) <= 1e-5
     with pytest.raises(ps.ConfigRejectedError):
-        ps.ConvPlan(ps.ConvPreset.parse(BASELINE["cfg3"][0]), bwd_data=True)
+        plan.emit()
+
+
+@pytest.mark.gpu
+def test_backward_data_rejects_negative_phase_pad():
+    # 2x2 / stride 2 / pad 1: phase 1's taps start one row past its first output row
+    with pytest.raises(ps.ConfigRejectedError):
+        ps.ConvPlan(ps.ConvPreset.parse("conv:1,16,16,4,4,2,2,2,2,16,1,1,6,6"), bwd_data=True)
 
 
 @pytest.mark.gpu
