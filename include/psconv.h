@@ -149,17 +149,25 @@ int conv_plan_create(const conv_desc* d, int mode, int device, const char* recip
  * Returns 0 / 2 (a phase would need negative padding, e.g. 2x2 / stride 2 / pad 1) / 1. */
 int conv_plan_create_bwd_data(const conv_desc* d, int mode, int device, const char* recipe_or_null,
                               conv_plan** out);
-/* Backward-weight plan: for the FORWARD descriptor d (stride 1,
- * nImg a multiple of 16), dW = dL/dFilter from the forward input X and dY:
- *   dW[k][c][r][s] = sum_{n,p,q} X[n][c][p+r-pad][q+s-pad] * dY[n][k][p][q]
- * computed as a forward conv on the same kernel with the roles swapped -- the
- * input channels become images, the batch the reduction channels, dY the filter
- * (P x Q taps) and R x S the output extent -- split-K over the long reduction
- * (kt:1, units reduce-added). tf32 / 3xtf32 modes. Returns 0 / 2 / 1. */
+/* Backward-weight plan: for the FORWARD descriptor d (any
+ * stride / padding), dW = dL/dFilter from the forward input X and dY:
+ *   dW[k][c][r][s] = sum_{n,p,q} X[n][c][p*sh+r-pad_h][q*sw+s-pad_w] * dY[n][k][p][q]
+ * computed by a pixel-major implicit GEMM (per tap, the reduction runs over the
+ * pixels; both operands are read by TMA straight from NCHW16c / NKPQ16k as MN-major
+ * tf32 tiles), split over pixel ranges with the partials added in split order
+ * (bitwise reproducible). tf32 / 3xtf32 modes. recipe_or_null: NULL, or
+ * "gpu=sw:S,kn:K,cn:C,nt:T,box:QxP,sp:SPLITS,st:STAGES,ch:K8" overriding the tile
+ * roles (sw), channels / taps per tile, pixel box, splits, ring depth, 3xTF32
+ * accumulation chunk. Returns 0 / 2 / 1. */
 int conv_plan_create_bwd_weight(const conv_desc* d, int mode, int device, const char* recipe_or_null,
                                 conv_plan** out);
+/* The backward-weight geometry conv_plan_create_bwd_weight would choose on a GPU with
+ * num_sms SMs (host only, no device): its recipe plus tiles / units / stage bytes. 0 / 2. */
+int conv_wgrad_describe(const conv_desc* d, int mode, int num_sms, const char* recipe_or_null, char* buf,
+                        size_t len);
 /* Runs a backward-weight plan: x = X (NCHW16c), dy = dY (NKPQ16k), dw = dW
- * (KCRS16c16k, overwritten), all device arrays of the forward layer's sizes. */
+ * (KCRS16c16k, overwritten), all device arrays of the forward layer's sizes.
+ * Stream-ordered, no allocation (the split workspace is the plan's). */
 int conv_bwd_weight(const conv_plan* p, const float* x, const float* dy, float* dw, void* cuda_stream);
 void conv_plan_destroy(conv_plan* p);
 

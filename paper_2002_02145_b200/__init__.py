@@ -155,9 +155,10 @@ def _ptr(t) -> int:
 
 
 class WgradPlan:
-    """Backward-weight plan of a stride-1 forward layer (C ABI conv_plan_create_bwd_weight):
-    forward(x, dy, dw) computes dW (KCRS16c16k) from X (NCHW16c) and dY (NKPQ16k) as the
-    role-swapped forward conv on the same kernel, split-K over the N*P*Q reduction."""
+    """Backward-weight plan of a forward layer (C ABI conv_plan_create_bwd_weight):
+    forward(x, dy, dw) computes dW (KCRS16c16k) from X (NCHW16c) and dY (NKPQ16k) with the
+    pixel-major wgrad kernel (MN-major tf32 operands straight from the activation layouts,
+    split over pixel ranges, partials added in split order)."""
 
     def __init__(self, preset: "ConvPreset", mode="3xtf32", device: int = 0, recipe: str | None = None):
         if isinstance(mode, str):
@@ -173,8 +174,19 @@ class WgradPlan:
 
     @property
     def recipe(self) -> str:
-        """The role-swapped conv's schedule."""
+        """The wgrad kernel's geometry (gpu=sw:,kn:,cn:,nt:,box:,sp:,st:,ch:)."""
         return lib.conv_plan_recipe(self._h).decode()
+
+    @staticmethod
+    def describe(preset: "ConvPreset", mode="3xtf32", num_sms: int = 148, recipe: str | None = None) -> str:
+        """The geometry a plan would choose on a GPU with num_sms SMs (host only)."""
+        if isinstance(mode, str):
+            mode = _MODES[mode.lower()]
+        d = preset.to_c()
+        buf = ctypes.create_string_buffer(512)
+        _check(lib.conv_wgrad_describe(ctypes.byref(d), mode, num_sms, recipe.encode() if recipe else None,
+                                       buf, len(buf)))
+        return buf.value.decode()
 
     def forward(self, x, dy, dw, stream=None) -> None:
         _check(lib.conv_bwd_weight(self._h, _ptr(x), _ptr(dy), _ptr(dw), _stream_ptr(stream)))
@@ -186,7 +198,11 @@ class WgradPlan:
             lib.conv_plan_destroy(self._h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
 
 class ConvPlan:

@@ -55,6 +55,8 @@ _sigs = {
     "conv_plan_create_bwd_weight": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                                     ctypes.POINTER(c_vp)]),
     "conv_bwd_weight": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "conv_wgrad_describe": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                           ctypes.c_char_p, ctypes.c_size_t]),
     "conv_model_stats": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_char_p,
                                          ctypes.POINTER(ctypes.c_double)]),
     "ranker_train": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,

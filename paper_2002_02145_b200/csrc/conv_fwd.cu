@@ -18,6 +18,7 @@
 #include "conv_pp.cuh"
 #include "internal.hpp"
 #include "seeded.hpp"
+#include "wgrad_kernel.cuh"
 
 static_assert(psconv::kSmemStageBudget == psconv::kStageBudget, "stage budget");
 static_assert(psconv::kSmemMaxStages == psconv::kMaxStages, "max stages");
@@ -60,13 +61,11 @@ struct conv_plan {
   int ph_a = 0, ph_b = 0, ph_rho_h = 0, ph_rho_w = 0;  // child: its phase and first taps
   int out_sh = 1, out_sw = 1;
   int64_t out_H = 0, out_W = 0;
-  // backward-weight plan (conv_plan_create_bwd_weight): d is the role-swapped conv
-  // (images = forward input channels, channels = batch, filter = dY); scratch for
-  // the transposed input, dY as that conv's KCRS16c16k filter, and its output
+  // backward-weight plan (conv_plan_create_bwd_weight): d is the forward layer; the
+  // pixel-major wgrad kernel's geometry and its split partial workspace (wgrad_kernel.cuh)
   bool bwd_weight = false;
-  float* wg_x = nullptr;
-  float* wg_dy = nullptr;
-  float* wg_dw = nullptr;
+  psconv::WgradParams wg{};
+  float* wg_ws = nullptr;
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
   // conv_fwd_host staging (lazily created): double-buffered device chunks,
@@ -229,47 +228,6 @@ __global__ void prepack_filter_f16_kernel(const float* __restrict__ flt, uint16_
   const __half l = __float2half_rn(x - __half2float(h));
   out[g + c16] = *reinterpret_cast<const uint16_t*>(&h);
   out[g + 16 + c16] = *reinterpret_cast<const uint16_t*>(&l);
-}
-
-// ---- backward weight: layout moves around the role-swapped forward conv
-// X [N][C/16][HW][16c] -> Xt [C][N/16][HW][16n]: one 16x16 (n, c) tile per pixel
-// through shared memory (coalesced 64-B rows both ways)
-__global__ void wgrad_transpose_x_kernel(const float* __restrict__ x, float* __restrict__ xt, int N, int Cb,
-                                         int64_t HW) {
-  __shared__ float tile[16][17];
-  const int t = threadIdx.x;
-  const int Nb = N / 16;
-  for (int64_t b = blockIdx.x; b < int64_t(Nb) * Cb * HW; b += gridDim.x) {
-    const int64_t pix = b % HW;
-    const int cb = int((b / HW) % Cb), nb = int(b / HW / Cb);
-    __syncthreads();
-    tile[t >> 4][t & 15] = x[((int64_t(nb * 16 + (t >> 4)) * Cb + cb) * HW + pix) * 16 + (t & 15)];
-    __syncthreads();
-    xt[((int64_t(cb * 16 + (t >> 4)) * Nb + nb) * HW + pix) * 16 + (t & 15)] = tile[t & 15][t >> 4];
-  }
-}
-// dY [N][K/16][PQ][16k] -> the swapped conv's filter KCRS16c16k [K/16][N/16][PQ][16n][16k]
-__global__ void wgrad_dy_filter_kernel(const float* __restrict__ dy, float* __restrict__ f, int N, int Kb,
-                                       int64_t PQ) {
-  const int64_t n_el = int64_t(N) * Kb * PQ * 16;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
-    const int ki = int(e & 15), ni = int((e >> 4) & 15);
-    const int64_t r = e >> 8;  // (kb, nb, pq)
-    const int64_t pq = r % PQ;
-    const int nb = int((r / PQ) % (N / 16)), kb = int(r / PQ / (N / 16));
-    f[e] = dy[((int64_t(nb * 16 + ni) * Kb + kb) * PQ + pq) * 16 + ki];
-  }
-}
-// the swapped conv's output [C][K/16][RS][16k] -> dW KCRS16c16k [K/16][C/16][RS][16c][16k]
-__global__ void wgrad_dw_kernel(const float* __restrict__ o, float* __restrict__ dw, int C, int Kb, int RS) {
-  const int64_t n_el = int64_t(C) * Kb * RS * 16;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
-    const int ki = int(e & 15), ci = int((e >> 4) & 15);
-    const int64_t r = e >> 8;  // (kb, cb, rs)
-    const int rs = int(r % RS);
-    const int cb = int((r / RS) % (C / 16)), kb = int(r / RS / (C / 16));
-    dw[e] = o[((int64_t(cb * 16 + ci) * Kb + kb) * RS + rs) * 16 + ki];
-  }
 }
 
 // NCHW16c element e (relative to image img_begin) <- value(seed, logical NCHW index)
@@ -1258,6 +1216,242 @@ conv_plan* create_plan(const conv_desc& d, int mode, int device, const char* rec
 }  // namespace
 }  // namespace psconv
 
+namespace psconv {
+namespace {
+// ---------------------------------------------------------------- backward weight
+// Geometry of the pixel-major wgrad kernel (wgrad_kernel.cuh) for the forward layer f:
+// tile roles / sizes by a small cost model (MMA cycles at the measured N floor, operand
+// bytes per K=8 step at ~64 B/cycle/SM of L2->SMEM delivery, pixel-box and tap waste), the
+// pixel box per stage (rows multiple of 8, >= 3-4 ring slots), and the split of the pixel
+// range so that the units fill the SMs once. A recipe "gpu=sw:S,kn:K,cn:C,nt:T,box:QxP,
+// sp:SPLITS,st:STAGES,ch:K8" overrides any of the choices.
+struct WgPick {
+  int swap = -1, kn = 0, cn = 0, ntap = 0, qb = 0, pb = 0, splits = 0, stages = 0, chunk = -1;
+};
+WgPick parse_wgrad_recipe(const char* recipe) {
+  WgPick w;
+  if (!recipe || !*recipe) return w;
+  std::string r(recipe);
+  const auto pos = r.find("gpu=");
+  if (pos == std::string::npos) throw ConfigError("backward-weight recipe: expected 'gpu=key:value,...'");
+  std::string body = r.substr(pos + 4);
+  size_t i = 0;
+  while (i < body.size()) {
+    size_t j = body.find(',', i);
+    if (j == std::string::npos) j = body.size();
+    const std::string kv = body.substr(i, j - i);
+    const auto c = kv.find(':');
+    if (c == std::string::npos) throw ConfigError("backward-weight recipe: bad item '" + kv + "'");
+    const std::string k = kv.substr(0, c), v = kv.substr(c + 1);
+    auto num = [&](const std::string& t) {
+      char* e = nullptr;
+      const long x = std::strtol(t.c_str(), &e, 10);
+      if (t.empty() || *e || x < 0) throw ConfigError("backward-weight recipe: bad value '" + kv + "'");
+      return int(x);
+    };
+    if (k == "sw") w.swap = num(v);
+    else if (k == "kn") w.kn = num(v);
+    else if (k == "cn") w.cn = num(v);
+    else if (k == "nt") w.ntap = num(v);
+    else if (k == "sp") w.splits = num(v);
+    else if (k == "st") w.stages = num(v);
+    else if (k == "ch") w.chunk = num(v);
+    else if (k == "box") {
+      const auto x = v.find('x');
+      if (x == std::string::npos) throw ConfigError("backward-weight recipe: box:QxP");
+      w.qb = num(v.substr(0, x));
+      w.pb = num(v.substr(x + 1));
+    } else {
+      throw ConfigError("backward-weight recipe: unknown key '" + k + "'");
+    }
+    i = j + 1;
+  }
+  return w;
+}
+
+std::string wgrad_recipe(const WgradParams& g) {
+  return "gpu=sw:" + std::to_string(g.swap) + ",kn:" + std::to_string(g.kn) + ",cn:" + std::to_string(g.cn) +
+         ",nt:" + std::to_string(g.ntap) + ",box:" + std::to_string(g.Qb) + "x" + std::to_string(g.Pb) +
+         ",sp:" + std::to_string(g.splits) + ",st:" + std::to_string(g.stages) + ",ch:" + std::to_string(g.chunk_k8);
+}
+
+constexpr int kWgSmemBudget = 227 * 1024 - 6144;  // ring; the rest: alignment, barriers, row/tap tables
+
+WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* recipe) {
+  const WgPick want = parse_wgrad_recipe(recipe);
+  const bool split3 = mode == PSCONV_MODE_3XTF32;
+  const int C = int(f.nIfm), K = int(f.nOfm), RS = int(f.kh * f.kw);
+  const int Cb = C / 16, Kb = K / 16;
+  const int P = int(f.ofh), Q = int(f.ofw);
+  const int mult = split3 ? 2 : 1;
+  auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
+  // pixel box for a per-row stage footprint: least waste, then most rows
+  auto pick_box = [&](int row_bytes, int min_stages, int& qb, int& pb) {
+    const int rows_max = std::max(8, (kWgSmemBudget / min_stages / row_bytes) / 8 * 8);
+    double best = 1e30;
+    qb = pb = 0;
+    for (int q = 1; q <= Q + 7; ++q) {
+      if (q > Q && q != (Q + 7) / 8 * 8) continue;
+      for (int pp = 1; pp <= P; ++pp) {
+        const int rows = q * pp;
+        if (rows % 8 || rows > rows_max || rows > 256) continue;
+        const double waste = double(cdiv(Q, q) * q * cdiv(P, pp) * pp) / (double(P) * Q);
+        const double score = waste * (1.0 + 2.0 / rows);  // per-stage fixed cost ~ 2 rows
+        if (score < best - 1e-12) {
+          best = score;
+          qb = q;
+          pb = pp;
+        }
+      }
+    }
+    if (!qb) throw ConfigError("backward weight: no pixel box fits");
+  };
+  struct Cand {
+    int swap, kn, cn, ntap, bn;
+    double cost;
+  };
+  std::vector<Cand> cands;
+  const int mma_mult = split3 ? 3 : 1;
+  auto consider = [&](int swap, int kn, int cn, int ntap) {
+    const int bn = swap ? kn : ntap * cn;
+    const int m = swap ? ntap * cn : kn;
+    if (m != 128 || bn < 32 || bn > 256 || bn % 32) return;
+    if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 256) return;
+    if (split3 && bn > 128) return;
+    if (cn > std::max(32, (C + 31) / 32 * 32) || kn > std::max(32, (K + 31) / 32 * 32)) return;
+    if (want.swap >= 0 && want.swap != swap) return;
+    if (want.kn && want.kn != kn) return;
+    if (want.cn && want.cn != cn) return;
+    if (want.ntap && want.ntap != ntap) return;
+    const int64_t tiles = cdiv(K, kn) * cdiv(C, cn) * cdiv(RS, ntap);
+    const double mma = std::max(bn / 2.0, bn <= 64 ? 45.0 : 0.0) * mma_mult;
+    const double deliver = (128.0 + bn) * 8 * 4 / 64.0;
+    const double smem = split3 ? (128.0 + bn) * 8 * 4 * 6 / 128.0 : 0.0;  // TMA + split r/w + 3 MMA reads
+    const double k8 = std::max(mma, std::max(deliver, smem));
+    cands.push_back({swap, kn, cn, ntap, bn, double(tiles) * k8});
+  };
+  for (int kn : {32, 64, 128, 256})
+    for (int cn : {32, 64, 128, 256})
+      for (int nt : {1, 2, 3, 4, 7, 8, 9}) {
+        consider(0, kn, cn, nt);
+        consider(1, kn, cn, nt);
+      }
+  if (cands.empty()) throw ConfigError("backward weight: no tile geometry for this layer / recipe");
+  const Cand* best = &cands[0];
+  for (const Cand& c : cands)
+    if (c.cost < best->cost * (1 - 1e-9) || (c.cost <= best->cost * (1 + 1e-9) && c.bn > best->bn)) best = &c;
+  WgradParams g{};
+  g.N = int(f.nImg);
+  g.Cb = Cb;
+  g.Kb = Kb;
+  g.H = int(f.ifh);
+  g.W = int(f.ifw);
+  g.P = P;
+  g.Q = Q;
+  g.R = int(f.kh);
+  g.S = int(f.kw);
+  g.sh = int(f.stride_h);
+  g.sw = int(f.stride_w);
+  g.ph = int(f.pad_h);
+  g.pw = int(f.pad_w);
+  g.swap = best->swap;
+  g.kn = best->kn;
+  g.cn = best->cn;
+  g.ntap = best->ntap;
+  g.bn = best->bn;
+  g.tiles_k = int(cdiv(K, g.kn));
+  g.tiles_c = int(cdiv(C, g.cn));
+  g.tiles_t = int(cdiv(RS, g.ntap));
+  g.tiles = g.tiles_k * g.tiles_c * g.tiles_t;
+  const int row_bytes = (g.ntap * g.cn + g.kn) * 4 * mult;
+  if (want.qb) {
+    g.Qb = want.qb;
+    g.Pb = want.pb;
+    if ((g.Qb * g.Pb) % 8 || g.Qb * g.Pb > 256 || g.Qb < 1 || g.Pb < 1)
+      throw ConfigError("backward-weight recipe: box rows (QxP) must be a multiple of 8, at most 256");
+  } else {
+    pick_box(row_bytes, split3 ? 3 : 4, g.Qb, g.Pb);
+  }
+  g.rows = g.Qb * g.Pb;
+  g.tiles_q = int(cdiv(Q, g.Qb));
+  g.tiles_p = int(cdiv(P, g.Pb));
+  const int64_t nstage = int64_t(g.N) * g.tiles_p * g.tiles_q;
+  if (nstage >= (int64_t(1) << 31)) throw ConfigError("backward weight: too many pixel stages");
+  g.nstage = int(nstage);
+  g.x_bytes = g.ntap * g.cn * g.rows * 4;
+  g.y_bytes = g.kn * g.rows * 4;
+  g.stage_bytes = (g.x_bytes + g.y_bytes) * mult;
+  g.stages = want.stages ? want.stages : std::min(kWgMaxStages, kWgSmemBudget / g.stage_bytes);
+  if (g.stages < 2 || g.stages > kWgMaxStages || g.stages * g.stage_bytes > kWgSmemBudget)
+    throw ConfigError("backward weight: the stage ring does not fit shared memory");
+  // one unit per SM: split the pixel stages so that splits x tiles ~ the SM count (at least
+  // 2 stages per unit); more units than SMs only when the tiles alone exceed them
+  int splits = want.splits;
+  if (!splits) splits = int(std::max<int64_t>(1, std::min<int64_t>(num_sms / g.tiles, nstage / 2)));
+  splits = int(std::min<int64_t>(splits, nstage));
+  g.stage_per_split = int(cdiv(nstage, splits));
+  g.splits = int(cdiv(nstage, g.stage_per_split));
+  g.units = g.splits * g.tiles;
+  // 3xTF32 accumulation chunks (~32 K=8 steps: error ~6e-8 per step)
+  g.chunk_k8 = split3 ? (want.chunk >= 0 ? want.chunk : 32) : 0;
+  if (split3 && g.chunk_k8 > 0 && g.chunk_k8 < g.rows / 8) g.chunk_k8 = g.rows / 8;
+  return g;
+}
+
+template <int BN, bool SPLIT3>
+void launch_wgrad_kernel(const conv_plan* P, const WgradParams& g, cudaStream_t st) {
+  using Cfg = WgCfg<BN, SPLIT3>;
+  const int smem = g.stages * g.stage_bytes + 6144;
+  static SmemAttr attr_once;  // the largest ring any plan may use (set once per device)
+  CUDA_OK(attr_once.ensure(wgrad_sm100<BN, SPLIT3>, kWgSmemBudget + 6144, P->device));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(g.units, P->num_sms));
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = std::getenv("PSCONV_NO_PDL") ? 0 : 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_sm100<BN, SPLIT3>, g));
+}
+
+void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw, cudaStream_t st) {
+  WgradParams g = P->wg;
+  g.x = x;
+  g.dy = dy;
+  static const int debug_env = [] {  // profiling switch, results wrong when set
+    const char* e = std::getenv("PSCONV_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  g.debug = debug_env & 3;
+  const bool split3 = P->mode == PSCONV_MODE_3XTF32;
+#define PSCONV_WG(B) (split3 ? launch_wgrad_kernel<B, true>(P, g, st) : launch_wgrad_kernel<B, false>(P, g, st))
+  switch (g.bn) {
+    case 32: PSCONV_WG(32); break;
+    case 64: PSCONV_WG(64); break;
+    case 128: PSCONV_WG(128); break;
+    case 192: launch_wgrad_kernel<192, false>(P, g, st); break;
+    case 256: launch_wgrad_kernel<256, false>(P, g, st); break;
+    default: throw RuntimeError("internal: wgrad bn");
+  }
+#undef PSCONV_WG
+  const int64_t n = int64_t(g.Kb) * 16 * g.Cb * 16 * g.R * g.S;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_for(n));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_reduce_kernel, g, dw));
+}
+}  // namespace
+}  // namespace psconv
+
 using namespace psconv;
 
 extern "C" {
@@ -1394,64 +1588,53 @@ int conv_plan_create_bwd_weight(const conv_desc* d_in, int mode, int device, con
     *out = nullptr;
     conv_desc f = *d_in;
     validate_desc(f);
-    if (f.stride_h != 1 || f.stride_w != 1)
-      throw ConfigError("backward weight: only stride-1 layers are supported");
-    if (f.nImg % 16) throw ConfigError("backward weight: nImg must be a multiple of 16 (it becomes the reduction channels)");
+    if (f.gemm_block != 16) throw ConfigError("backward weight: gemm_block must be 16");
     if (mode == PSCONV_MODE_F16X2) throw ConfigError("backward weight: tf32 / 3xtf32 modes only");
-    // dW[k][c][r][s] = sum_{n,p,q} X[n][c][r+p-pad][s+q-pad] dY[n][k][p][q]: the forward
-    // conv with images = input channels, channels = batch, filter = dY (P x Q taps),
-    // output extent R x S, same padding
-    conv_desc t{};
-    t.nImg = f.nIfm;
-    t.nOfm = f.nOfm;
-    t.nIfm = f.nImg;
-    t.ofh = f.kh;
-    t.ofw = f.kw;
-    t.kh = f.ofh;
-    t.kw = f.ofw;
-    t.stride_h = t.stride_w = 1;
-    t.gemm_block = f.gemm_block;
-    t.pad_h = f.pad_h;
-    t.pad_w = f.pad_w;
-    t.ifh = f.ifh;
-    t.ifw = f.ifw;
-    conv_plan* P = nullptr;
-    auto create = [&](const char* r) {
-      const int rc = conv_plan_create(&t, mode, device, r, &P);
-      if (rc != PSCONV_OK) {
-        if (rc == PSCONV_ERR_CONFIG) throw ConfigError(conv_last_error());
-        throw RuntimeError(conv_last_error());
-      }
-    };
-    create(recipe && *recipe ? recipe : nullptr);
-    if (!(recipe && std::strstr(recipe, "ks:"))) {
-      // few tiles (C*R*S x K outputs) over a reduction of N*P*Q: split every tile
-      // into ks units (~2 per SM), partial sums reduce-added into the zeroed output
-      const Schedule& s = P->sched;
-      const int64_t tiles = ((t.ofw + s.qb - 1) / s.qb) * ((t.ofh + s.pb - 1) / s.pb) *
-                            ((t.nImg + s.nb - 1) / s.nb) * (t.nOfm / s.bn);
-      const int ks = int(std::min<int64_t>(64, std::max<int64_t>(1, (2 * P->num_sms + tiles - 1) / tiles)));
-      if (ks > 1) {
-        const std::string r2 = s.recipe_id + ",ks:" + std::to_string(ks) + ",kt:1";
-        conv_plan_destroy(P);
-        P = nullptr;
-        create(r2.c_str());
-      }
-    }
-    P->bwd_weight = true;
+    if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32)
+      throw ConfigError("unknown mode " + std::to_string(mode));
+    (void)wgrad_geom(f, mode, 148, recipe);  // recipe / geometry errors before any device call
+    int ndev = 0;
+    CUDA_OK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ConfigError("invalid device " + std::to_string(device));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+      throw RuntimeError("psconv kernels are built for sm_100a; device is sm_" + std::to_string(prop.major) +
+                         std::to_string(prop.minor));
+    const WgradParams g = wgrad_geom(f, mode, prop.multiProcessorCount, recipe);
+    auto* P = new conv_plan();
+    P->d = f;
+    P->kd = f;
     P->fwd = f;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(device);
-    cudaError_t e = cudaMalloc(&P->wg_x, size_t(f.nImg) * f.nIfm * f.ifh * f.ifw * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&P->wg_dy, size_t(f.nImg) * f.nOfm * f.ofh * f.ofw * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&P->wg_dw, size_t(f.nOfm) * f.nIfm * f.kh * f.kw * sizeof(float));
-    cudaSetDevice(prev);
+    P->mode = mode;
+    P->device = device;
+    P->num_sms = prop.multiProcessorCount;
+    P->bwd_weight = true;
+    P->wg = g;
+    P->sched.recipe_id = wgrad_recipe(g);
+    DeviceGuard guard(device);
+    const cudaError_t e = cudaMalloc(&P->wg_ws, size_t(g.units) * 128 * g.bn * sizeof(float));
     if (e != cudaSuccess) {
-      conv_plan_destroy(P);
+      delete P;
       throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
+    P->wg.ws = P->wg_ws;
     *out = P;
+  });
+}
+
+int conv_wgrad_describe(const conv_desc* d_in, int mode, int num_sms, const char* recipe, char* buf, size_t len) {
+  return guarded([&] {
+    if (!d_in || !buf || !len) throw ConfigError("null argument");
+    conv_desc f = *d_in;
+    validate_desc(f);
+    if (mode != PSCONV_MODE_3XTF32 && mode != PSCONV_MODE_TF32) throw ConfigError("backward weight: tf32 / 3xtf32 modes only");
+    const WgradParams g = wgrad_geom(f, mode, num_sms > 0 ? num_sms : 148, recipe);
+    const std::string t = wgrad_recipe(g) + " tiles:" + std::to_string(g.tiles) + " units:" +
+                          std::to_string(g.units) + " stage_bytes:" + std::to_string(g.stage_bytes);
+    const size_t n = std::min(t.size(), len - 1);
+    std::memcpy(buf, t.data(), n);
+    buf[n] = 0;
   });
 }
 
@@ -1459,19 +1642,10 @@ int conv_bwd_weight(const conv_plan* P, const float* x, const float* dy, float* 
   return guarded([&] {
     if (!P || !x || !dy || !dw) throw ConfigError("null argument");
     if (!P->bwd_weight) throw ConfigError("not a backward-weight plan (conv_plan_create_bwd_weight)");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dw)) & 15)
+      throw ConfigError("tensor pointers must be 16-byte aligned");
     DeviceGuard guard(P->device);
-    const conv_desc& t = P->d;  // the role-swapped conv
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int N = int(t.nIfm), C = int(t.nImg), Kb = int(t.nOfm / 16);
-    const int64_t HW = t.ifh * t.ifw, PQ = t.kh * t.kw;
-    const int64_t xb = int64_t(N / 16) * (C / 16) * HW;
-    wgrad_transpose_x_kernel<<<int(std::min<int64_t>(xb, 148 * 32)), 256, 0, st>>>(x, P->wg_x, N, C / 16, HW);
-    wgrad_dy_filter_kernel<<<grid_for(int64_t(N) * Kb * PQ * 16), 256, 0, st>>>(dy, P->wg_dy, N, Kb, PQ);
-    CUDA_OK(cudaGetLastError());
-    launch_range(P, P->wg_x, P->wg_dy, P->wg_dw, C, st, 0u);
-    wgrad_dw_kernel<<<grid_for(int64_t(C) * Kb * t.ofh * t.ofw * 16), 256, 0, st>>>(P->wg_dw, dw, C, Kb,
-                                                                                  int(t.ofh * t.ofw));
-    CUDA_OK(cudaGetLastError());
+    launch_wgrad(P, x, dy, dw, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1499,7 +1673,7 @@ void conv_plan_destroy(conv_plan* p) {
     delete h;
     cudaSetDevice(prev);
   }
-  if (p->flt_pack) {
+  if (p->flt_pack || p->wg_ws) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
@@ -1509,9 +1683,7 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->split_ctr);
     cudaFree(p->split_ws);
     cudaFree(p->absmax);
-    cudaFree(p->wg_x);
-    cudaFree(p->wg_dy);
-    cudaFree(p->wg_dw);
+    cudaFree(p->wg_ws);
     cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }
@@ -1526,6 +1698,7 @@ int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len) {
     if (!p) throw ConfigError("null plan");
     if (!p->phase_plans.empty() || !p->zero_phases.empty())
       throw ConfigError("a strided backward-data plan is one transposed conv per output phase: no single driver nest");
+    if (p->bwd_weight) throw ConfigError("a backward-weight plan has no forward driver nest");
     const std::string txt = emit_driver(p->d, p->sched);
     need = static_cast<int64_t>(txt.size());
     if (buf && len) {
@@ -1539,6 +1712,7 @@ int64_t conv_plan_emit(const conv_plan* p, char* buf, size_t len) {
 
 int conv_plan_launches(const conv_plan* p) {
   if (!p) return 0;
+  if (p->bwd_weight) return 2;  // wgrad kernel + split reduction
   if (!p->phase_plans.empty() || !p->zero_phases.empty()) {
     int n = int(p->zero_phases.size());
     for (const conv_plan* c : p->phase_plans) n += conv_plan_launches(c);
@@ -1584,6 +1758,7 @@ int conv_plan_prepack(conv_plan* P, const float* flt, void* stream) {
   return guarded([&] {
     if (!P || !flt) throw ConfigError("null argument");
     if (reinterpret_cast<uintptr_t>(flt) & 15) throw ConfigError("filter must be 16-byte aligned");
+    if (P->bwd_weight) throw ConfigError("a backward-weight plan has no filter to prepack");
     DeviceGuard guard(P->device);
     for (conv_plan* c : P->phase_plans) {  // strided backward data: every phase's filter
       launch_prepack(c, flt, static_cast<cudaStream_t>(stream));

@@ -1,0 +1,477 @@
+// Backward-weight kernel: pixel-major implicit GEMM on tcgen05 with
+// MN-major tf32 operands gathered straight from the activation layouts.
+//
+//   dW[k][c][r][s] = sum_{n,p,q} dY[n][k][p][q] * X[n][c][p*sh + r - ph][q*sw + s - pw]
+//
+// For every tap (r, s) this is a GEMM over the pixels (n, p, q): the reduction index is the
+// pixel, so both operands are "MN-major" -- one pixel = one reduction row of 32 channels
+// (two 16-channel blocks of NCHW16c / NKPQ16k side by side, 128 B). kind::tf32 accepts
+// MN-major operands only in the SWIZZLE_128B_BASE32B smem layout (4-row atoms of 128-B
+// rows, 32-B chunks XOR-ed with the row; tools/probe_mn.cu). TMA cannot build it from 64-B
+// channel blocks: a box whose inner dimension (64 B) is narrower than the 128-B swizzle
+// span is stored one inner row per 128-B smem row, half empty, and a second box cannot start
+// 64 B in (misaligned; tools/probe_tma_sw32.cu). So producer warps gather the operands
+// with 16-byte cp.async copies, each placed at its swizzled position (out-of-image pixels and
+// channels past C / K: zero fill through src-size 0), one cp.async group per stage; a
+// producer thread signals a stage after its own copies of it completed (wait_group) and a
+// proxy fence -- the MMAs read it through the async proxy.
+//
+// Stage = a Qb x Pb pixel box of one image: rows = Qb * Pb reduction rows (multiple of 8).
+//   X side:  ntap taps x cn channels = ntap * cn / 32 MN groups (tap-shifted windows)
+//   dY side: kn channels = kn / 32 MN groups
+// Every MN group is `rows` 128-B rows (LBO = rows * 128 B, SBO = 512 B: 4-row atoms).
+//
+// Tile = 128 (M) x bn (N) accumulator in TMEM:
+//   swap 0: M = 128 output channels k (dY), N = ntap taps x cn input channels (X)
+//   swap 1: M = ntap x cn = 128 (X: taps x input channels), N = kn output channels (dY)
+//           (layers with K < 128, e.g. ResNet-50's K = 64 convs)
+// Work unit = (pixel split, tile); units are split-major so the CTAs running at one time
+// share a pixel range (its X / dY slice is read from HBM once, the other tiles hit L2).
+// Each unit writes its 128 x bn partial to a workspace; wgrad_reduce_kernel adds the splits
+// in split order (bitwise reproducible) and scatters into KCRS16c16k.
+//
+// Warp roles: 0-3 epilogue (TMEM lane quadrant = warp; TMEM -> registers -> workspace),
+// 4 TMEM owner + MMA issuer, 5.. producers (kWgProdWarps). 3xTF32: the producers also write lo = x -
+// trunc_tf32(x) of every chunk they copied into the stage's lo half; the MMAs D += A_hi B_hi
+// + A_lo B_hi + A_hi B_lo (kind::tf32 truncates fp32 operands, so A_hi / B_hi are the raw
+// tiles), accumulated in chunks of `chunk_k8` K=8 steps (the TMEM accumulation error grows
+// with the chain length) that the epilogue sums in fp32 registers;
+// double-buffered accumulators keep the MMA busy meanwhile.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "sm100_ptx.cuh"
+
+namespace psconv {
+
+constexpr int kWgMaxStages = 8;
+constexpr int kWgProdWarps = 8;  // producer warps (cp.async gatherers)
+
+struct WgradParams {
+  int N, Cb, Kb, H, W, P, Q, R, S, sh, sw, ph, pw;
+  int swap;                         // see above
+  int kn, cn, ntap, bn;             // channels / taps per tile, MMA N
+  int tiles_k, tiles_c, tiles_t, tiles;
+  int Qb, Pb, rows;                 // pixel box per stage (rows = Qb * Pb, multiple of 8)
+  int tiles_q, tiles_p;             // boxes per image
+  int nstage;                       // N * tiles_p * tiles_q pixel stages
+  int splits, units, stage_per_split;
+  int stages;                       // ring depth
+  int x_bytes, y_bytes;             // per stage (hi), X region first
+  int stage_bytes;                  // x + y (x2 for 3xTF32: hi | lo)
+  int chunk_k8;                     // 3xTF32: K=8 steps per accumulation chunk (0: whole unit)
+  int debug;                        // profiling (PSCONV_DEBUG): 1 skip copies, 2 skip MMAs
+  const float* x;                   // NCHW16c forward input
+  const float* dy;                  // NKPQ16k output gradient
+  float* ws;                        // partials [unit][128][bn]
+};
+
+namespace ptx {
+// MN-major SWIZZLE_128B_BASE32B descriptor (layout type 1): lbo = MN-group pitch, sbo = the
+// pitch of 4-row reduction atoms (512 B when contiguous)
+__device__ __forceinline__ uint64_t smem_desc_mn32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (1ull << 61);
+}
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_tf32_mn() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+// 16-byte global -> shared copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace ptx
+
+template <int BN, bool SPLIT3>
+struct WgCfg {
+  static constexpr int kThreads = 32 * (5 + kWgProdWarps);  // 4 epilogue + 1 MMA + producer warps
+  static constexpr int kAccCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  static constexpr uint32_t kTmemCols = 2 * kAccCols;  // two accumulators (power of 2, >= 64)
+};
+
+__device__ __forceinline__ void wg_stage_coords(const WgradParams& p, int g, int& n, int& p0, int& q0) {
+  const int per_img = p.tiles_p * p.tiles_q;
+  n = g / per_img;
+  const int r = g - n * per_img;
+  p0 = (r / p.tiles_q) * p.Pb;
+  q0 = (r % p.tiles_q) * p.Qb;
+}
+
+// The producer thread's share of one stage: its chunk column k8 (half = k8 / 4 selects the
+// 16-channel block of the 32-channel group, c16 = k8 % 4 the 16-B piece of it) of rows
+// row0 + kRowStep * m, in every MN group of the stage. The per-row pixel offsets live in a
+// shared-memory table (built once per CTA), the per-tap shifts in another (per unit); per
+// (row, tap) one bounds test and one pointer, then a pointer step + cp.async per block pair.
+// Compact loops on purpose: an unrolled version stalled on instruction fetch (ncu: BSYNC
+// no_instruction) and ran at ~0.16 IPC per producer warp.
+struct WgRowTab {
+  int xoff;  // X: (pi * sh * W + qi * sw) * 16 floats from the box origin
+  int xhw;   // X: (pi * sh) << 16 | qi * sw
+  int yoff;  // dY: (pi * Q + qi) * 16
+  int ypq;   // dY: pi << 16 | qi
+};
+struct WgTapTab {
+  int off;  // (r * W + s) * 16 floats
+  int rs;   // r << 16 | s
+};
+
+template <int PW>
+struct WgProducer {
+  static constexpr int kRowStep = PW * 4;  // 8 chunk columns per 128-B row
+  int k8, row0;
+  uint32_t doff0;  // byte offset of the chunk inside its MN group at m = 0 (row & 3 is the
+                   // same for every m: the row step is a multiple of 4, one swizzle phase)
+
+  __device__ __forceinline__ void init(int tid) {
+    k8 = tid & 7;
+    row0 = tid >> 3;
+    const int chunk32 = (k8 >> 1) ^ (row0 & 3);  // logical 32-B chunk (half*2 + c16/2), swizzled
+    doff0 = static_cast<uint32_t>(row0 * 128 + chunk32 * 32 + (k8 & 1) * 16);
+  }
+
+  // issue the stage's copies into the slot at shared address `sb`
+  __device__ __forceinline__ void issue(const WgradParams& p, const WgRowTab* rows, const WgTapTab* taps, uint32_t sb,
+                                        int n, int p0, int q0, int kt, int ct) const {
+    const uint32_t grp = static_cast<uint32_t>(p.rows) * 128u;
+    const int half = k8 >> 2, c16 = k8 & 3;
+    const int npx = p.cn / 32, npy = p.kn / 32;
+    // block pairs j whose block (first + 2 j) exists; past C / K: zeros
+    const int cb0 = ct * (p.cn / 16) + half, kb0 = kt * (p.kn / 16) + half;
+    const int jx = max(0, min(npx, (p.Cb - cb0 + 1) / 2)), jy = max(0, min(npy, (p.Kb - kb0 + 1) / 2));
+    const int64_t xpair = static_cast<int64_t>(2) * p.H * p.W * 16;  // floats between block pairs
+    const int64_t ypair = static_cast<int64_t>(2) * p.P * p.Q * 16;
+    const int hb = p0 * p.sh - p.ph, wb = q0 * p.sw - p.pw;  // input origin of the box (tap 0, 0)
+    const float* xs = p.x + ((static_cast<int64_t>(n) * p.Cb + cb0) * p.H + hb) * p.W * 16 + wb * 16 + c16 * 4;
+    const float* ys = p.dy + ((static_cast<int64_t>(n) * p.Kb + kb0) * p.P + p0) * p.Q * 16 + q0 * 16 + c16 * 4;
+    const int pmax = p.P - p0, qmax = p.Q - q0;
+    const uint32_t ybase = sb + static_cast<uint32_t>(p.x_bytes);
+#pragma unroll 1
+    for (int row = row0, m = 0; row < p.rows; row += kRowStep, ++m) {
+      const WgRowTab rt = rows[row];
+      const uint32_t dm = doff0 + static_cast<uint32_t>(m * kRowStep * 128);
+      const int hr = hb + (rt.xhw >> 16), wr = wb + (rt.xhw & 0xFFFF);
+#pragma unroll 1
+      for (int t = 0; t < p.ntap; ++t) {
+        const WgTapTab tp = taps[t];
+        const int h = hr + (tp.rs >> 16), w = wr + (tp.rs & 0xFFFF);
+        const bool ok = static_cast<unsigned>(h) < static_cast<unsigned>(p.H) &&
+                        static_cast<unsigned>(w) < static_cast<unsigned>(p.W);
+        const float* src = ok ? xs + (rt.xoff + tp.off) : p.x;
+        const int64_t step = ok ? xpair : 0;
+        const uint32_t d = sb + static_cast<uint32_t>(t * npx) * grp + dm;
+        // independent addresses per copy: a running pointer made every copy wait for the
+        // previous cp.async to read its operands (ncu: long scoreboard on the increment)
+#pragma unroll 4
+        for (int j = 0; j < npx; ++j)
+          ptx::cp_async16(d + j * grp, src + j * step, (ok && j < jx) ? 16u : 0u);
+      }
+      const bool ok = (rt.ypq >> 16) < pmax && (rt.ypq & 0xFFFF) < qmax;
+      const float* src = ok ? ys + rt.yoff : p.dy;
+      const int64_t step = ok ? ypair : 0;
+      const uint32_t d = ybase + dm;
+#pragma unroll 4
+      for (int j = 0; j < npy; ++j) ptx::cp_async16(d + j * grp, src + j * step, (ok && j < jy) ? 16u : 0u);
+    }
+  }
+
+  // 3xTF32: lo = x - trunc_tf32(x) of this thread's chunks of the (landed) stage
+  __device__ __forceinline__ void split(const WgradParams& p, uint8_t* slot) const {
+    const uint32_t grp = static_cast<uint32_t>(p.rows) * 128u;
+    const int groups = p.ntap * (p.cn / 32) + p.kn / 32;
+    const uint32_t lo = static_cast<uint32_t>(p.x_bytes + p.y_bytes);
+#pragma unroll 1
+    for (int row = row0, m = 0; row < p.rows; row += kRowStep, ++m) {
+      uint32_t o = doff0 + static_cast<uint32_t>(m * kRowStep * 128);
+#pragma unroll 2
+      for (int g = 0; g < groups; ++g, o += grp) {
+        const float4 v = *reinterpret_cast<const float4*>(slot + o);
+        float4 l;
+        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        *reinterpret_cast<float4*>(slot + lo + o) = l;
+      }
+    }
+  }
+};
+
+template <int BN, bool SPLIT3>
+__global__ void __launch_bounds__(WgCfg<BN, SPLIT3>::kThreads, 1) wgrad_sm100(const __grid_constant__ WgradParams p) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using Cfg = WgCfg<BN, SPLIT3>;
+  constexpr uint32_t kIdesc = ptx::idesc_tf32_mn<BN>();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int kStages = p.stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * p.stage_bytes);
+  uint64_t* full = bars;                     // stage landed (+ split): every producer thread
+  uint64_t* empty = bars + kWgMaxStages;     // MMAs done with the slot
+  uint64_t* acc_full = bars + 2 * kWgMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // per-row pixel offsets of the box (256 max) and the unit's tap shifts (9 max x 2 buffers)
+  WgRowTab* rowtab = reinterpret_cast<WgRowTab*>(smem + kStages * p.stage_bytes + 256);
+  WgTapTab* taptab = reinterpret_cast<WgTapTab*>(rowtab + 256);
+  const int warp = threadIdx.x >> 5;
+  for (int row = threadIdx.x; row < p.rows; row += blockDim.x) {
+    const int pi = row / p.Qb, qi = row - (row / p.Qb) * p.Qb;
+    WgRowTab t;
+    t.xoff = (pi * p.sh * p.W + qi * p.sw) * 16;
+    t.xhw = ((pi * p.sh) << 16) | (qi * p.sw);
+    t.yoff = (pi * p.Q + qi) * 16;
+    t.ypq = (pi << 16) | qi;
+    rowtab[row] = t;
+  }
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 32 * kWgProdWarps);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  ptx::griddep_launch_dependents();
+
+  const int per_split = p.stage_per_split;
+  // chunks per unit: 3xTF32 splits the reduction into accumulation chunks of chunk_k8 K=8
+  // steps (whole stages); TF32 accumulates the unit in one chunk
+  const int k8_stage = p.rows / 8;
+  const int chunk_st = (SPLIT3 && p.chunk_k8 > 0) ? max(1, p.chunk_k8 / k8_stage) : (1 << 30);
+
+  if (warp >= 5) {
+    // ------------------------------------------------------------ producers (cp.async)
+    WgProducer<kWgProdWarps> pr;
+    pr.init(threadIdx.x - 160);
+    int tt_cur = -1, tbuf = 0;
+    ptx::griddep_wait();  // X / dY come from earlier kernels in the stream (PDL)
+    const uint32_t s0 = ptx::smem_u32(smem);
+    // a stage is signalled once `lag` younger stages are in flight (cp.async groups)
+    const int lag = kStages > 3 ? 3 : kStages - 1;
+    int stage = 0, pending = 0, sig_stage = 0;
+    uint32_t phase = 0;
+    auto signal_oldest = [&]() {
+      if (SPLIT3) pr.split(p, smem + sig_stage * p.stage_bytes);
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&full[sig_stage]);
+      if (++sig_stage == kStages) sig_stage = 0;
+    };
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int split = u / p.tiles, tile = u - split * p.tiles;
+      const int ct = tile % p.tiles_c, tt = (tile / p.tiles_c) % p.tiles_t, kt = tile / (p.tiles_c * p.tiles_t);
+      const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
+      if (tt != tt_cur) {  // the unit's taps (double-buffered: the other warps may still read)
+        tt_cur = tt;
+        tbuf ^= 1;
+        const int i = threadIdx.x - 160;
+        if (i < p.ntap) {
+          // taps past R*S (a partial last tap group) copy the last tap again; the reduce
+          // kernel never reads those accumulator rows / columns
+          const int tap = min(tt * p.ntap + i, p.R * p.S - 1);
+          const int r = tap / p.S, sx = tap - r * p.S;
+          WgTapTab tp;
+          tp.off = (r * p.W + sx) * 16;
+          tp.rs = (r << 16) | sx;
+          taptab[tbuf * 16 + i] = tp;
+        }
+        ptx::named_bar(1, 32 * kWgProdWarps);
+      }
+      for (int g = g0; g < g1; ++g) {
+        int n, p0, q0;
+        wg_stage_coords(p, g, n, p0, q0);
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (!(p.debug & 1))
+          pr.issue(p, rowtab, taptab + tbuf * 16, s0 + static_cast<uint32_t>(stage * p.stage_bytes), n, p0, q0, kt,
+                   ct);
+        ptx::cp_async_commit();
+        if (++pending > lag) {
+          if (lag == 3)
+            ptx::cp_async_wait<3>();
+          else if (lag == 2)
+            ptx::cp_async_wait<2>();
+          else
+            ptx::cp_async_wait<1>();
+          signal_oldest();
+          --pending;
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    ptx::cp_async_wait<0>();
+    while (pending-- > 0) signal_oldest();
+  } else if (warp == 4) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t lbo = static_cast<uint32_t>(p.rows) * 128u;
+    const uint32_t s0 = ptx::smem_u32(smem);
+    const uint32_t a_off = p.swap ? 0u : static_cast<uint32_t>(p.x_bytes);
+    const uint32_t b_off = p.swap ? static_cast<uint32_t>(p.x_bytes) : 0u;
+    const uint32_t lo_off = static_cast<uint32_t>(p.x_bytes + p.y_bytes);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int split = u / p.tiles;
+      const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
+      int in_chunk = 0;
+      for (int g = g0; g < g1; ++g) {
+        if (in_chunk == 0) {  // a fresh accumulator (chunk) begins
+          ptx::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+          ptx::tc_fence_after();
+        }
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const bool first = in_chunk == 0;
+        const bool last = ++in_chunk == chunk_st || g + 1 == g1;
+        if (ptx::elect_one()) {
+          const uint32_t base = s0 + static_cast<uint32_t>(stage * p.stage_bytes);
+          const uint32_t d = tmem_base + static_cast<uint32_t>(acc * Cfg::kAccCols);
+          const int nk8 = (p.debug & 2) ? 0 : k8_stage;
+          for (int j = 0; j < nk8; ++j) {
+            const uint32_t a = base + a_off + j * 1024u, b = base + b_off + j * 1024u;
+            const uint64_t ad = ptx::smem_desc_mn32(a, lbo, 512), bd = ptx::smem_desc_mn32(b, lbo, 512);
+            ptx::mma_tf32(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
+            if (SPLIT3) {
+              ptx::mma_tf32(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
+              ptx::mma_tf32(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+            }
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (last) ptx::mma_commit(&acc_full[acc]);
+        }
+        __syncwarp();
+        if (last) {
+          in_chunk = 0;
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 0-3)
+    const int row = warp * 32 + (threadIdx.x & 31);
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int split = u / p.tiles;
+      const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
+      float* dst = p.ws + (static_cast<int64_t>(u) * 128 + row) * p.bn;
+      if constexpr (SPLIT3 && BN <= 128) {
+        const int nchunks = (g1 - g0 + chunk_st - 1) / chunk_st;
+        float sum[BN];
+#pragma unroll
+        for (int i = 0; i < BN; ++i) sum[i] = 0.f;
+        for (int c = 0; c < nchunks; ++c) {
+          ptx::mbar_wait_sleep(&acc_full[acc], acc_phase);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            ptx::tmem_ld32(lane_base + acc * Cfg::kAccCols + c0, v);
+            ptx::tmem_wait_ld();
+            ptx::reg_fence(v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum[c0 + i] += __uint_as_float(v[i]);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (ptx::elect_one()) ptx::mbar_arrive(&acc_empty[acc]);  // one arrival per warp
+          __syncwarp();
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 4)
+          *reinterpret_cast<float4*>(dst + c0) = make_float4(sum[c0], sum[c0 + 1], sum[c0 + 2], sum[c0 + 3]);
+      } else {
+        // one chunk per unit (TF32): stream the accumulator to the workspace in 32-column pieces
+        ptx::mbar_wait_sleep(&acc_full[acc], acc_phase);
+        ptx::tc_fence_after();
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          ptx::tmem_ld32(lane_base + acc * Cfg::kAccCols + c0, v);
+          ptx::tmem_wait_ld();
+          ptx::reg_fence(v);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c0 + i) =
+                make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                            __uint_as_float(v[i + 3]));
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (ptx::elect_one()) ptx::mbar_arrive(&acc_empty[acc]);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+#endif
+}
+
+// dW (KCRS16c16k) = the split partials of every tile added in split order.
+__global__ void wgrad_reduce_kernel(const __grid_constant__ WgradParams p, float* __restrict__ dw) {
+  ptx::griddep_wait();
+  const int C = p.Cb * 16, RS = p.R * p.S;
+  const int64_t n_el = int64_t(p.Kb) * 16 * C * RS;
+  const int64_t tile_elems = int64_t(128) * p.bn;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = e;
+    const int k16 = int(t & 15);
+    t >>= 4;
+    const int c16 = int(t & 15);
+    t >>= 4;
+    const int tap = int(t % RS);
+    t /= RS;
+    const int cb = int(t % p.Cb);
+    const int kb = int(t / p.Cb);
+    const int k = kb * 16 + k16, c = cb * 16 + c16;
+    const int tt = tap / p.ntap, tl = tap - tt * p.ntap, ct = c / p.cn, cl = c - ct * p.cn;
+    const int kt = k / p.kn, kl = k - kt * p.kn;
+    const int tile = (kt * p.tiles_t + tt) * p.tiles_c + ct;
+    const int xi = tl * p.cn + cl;  // X-side index within the tile (taps x channels)
+    const int64_t off = p.swap ? int64_t(xi) * p.bn + kl : int64_t(kl) * p.bn + xi;
+    const float* src = p.ws + int64_t(tile) * tile_elems + off;
+    float s = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) s += src[int64_t(sp) * p.tiles * tile_elems];
+    dw[e] = s;
+  }
+}
+
+}  // namespace psconv

@@ -202,3 +202,33 @@ def test_emission_matches_live_reference_emitter(conv):
         assert ps.emit_driver(ConvPreset.parse(conv), r) == want, r
         n += 1
     assert n >= 60
+
+
+def test_wgrad_geometry_all_resnet_shapes():
+    """Backward-weight geometry (conv_wgrad_describe, host only) for every bench layer in both
+    modes: an M = 128 tile, a legal MMA N, whole K=8 steps per pixel box, and a ring that fits."""
+    import re
+
+    from paper_2002_02145_b200.workloads import ALL
+    for name, (conv, _c, _i) in ALL.items():
+        p = ps.ConvPreset.parse(conv)
+        for mode in ("tf32", "3xtf32"):
+            d = ps.WgradPlan.describe(p, mode)
+            kv = dict(re.findall(r"(\w+):([\dx]+)", d))
+            sw, kn, cn, nt = (int(kv[k]) for k in ("sw", "kn", "cn", "nt"))
+            m = nt * cn if sw else kn
+            bn = kn if sw else nt * cn
+            assert m == 128, (name, mode, d)
+            assert bn in (32, 64, 128, 192, 256) and (mode == "tf32" or bn <= 128), (name, mode, d)
+            qb, pb = (int(v) for v in kv["box"].split("x"))
+            assert (qb * pb) % 8 == 0 and qb * pb <= 256, (name, mode, d)
+            assert int(kv["stage_bytes"]) * int(kv["st"]) <= 227 * 1024 - 6144, (name, mode, d)
+
+
+def test_wgrad_recipe_override_and_errors():
+    p = ps.ConvPreset.parse("conv:8,128,64,10,10,3,3,1,1,16,1,1,10,10")
+    d = ps.WgradPlan.describe(p, "tf32", recipe="gpu=sw:0,kn:128,cn:64,nt:3,box:10x4,sp:5,st:3")
+    assert d.startswith("gpu=sw:0,kn:128,cn:64,nt:3,box:10x4,sp:5,st:3")
+    for bad in ("gpu=box:7x1", "gpu=zz:1", "gpu=nt:3,cn:64,sw:0", "sw:0"):
+        with pytest.raises(ps.ConfigRejectedError):
+            ps.WgradPlan.describe(p, "3xtf32", recipe=bad)

@@ -683,33 +683,46 @@ def test_f16x2_accumulate_bias_relu():
 
 
 def _wgrad_ref(p, x, dy):
-    """dW[k][c][r][s] = sum_{n,p,q} X[n][c][p+r-pad][q+s-pad] dY[n][k][p][q] in float64,
+    """dW[k][c][r][s] = sum_{n,p,q} X[n][c][p*sh+r-pad][q*sw+s-pad] dY[n][k][p][q] in float64,
     returned in KCRS16c16k."""
     N, K, C = p.nImg, p.nOfm, p.nIfm
     P, Q, R, S, H, W_ = p.ofh, p.ofw, p.kh, p.kw, p.ifh, p.ifw
+    sh, sw = p.stride_h, p.stride_w
     xl = x.reshape(N, C // 16, H, W_, 16).transpose(0, 1, 4, 2, 3).reshape(N, C, H, W_).astype(np.float64)
     dyl = dy.reshape(N, K // 16, P, Q, 16).transpose(0, 1, 4, 2, 3).reshape(N, K, P, Q).astype(np.float64)
-    xp = np.zeros((N, C, H + 2 * p.pad_h, W_ + 2 * p.pad_w))
+    hp = max(H + 2 * p.pad_h, (P - 1) * sh + R)
+    wp = max(W_ + 2 * p.pad_w, (Q - 1) * sw + S)
+    xp = np.zeros((N, C, hp, wp))
     xp[:, :, p.pad_h:p.pad_h + H, p.pad_w:p.pad_w + W_] = xl
     dw = np.zeros((K, C, R, S))
     for r in range(R):
         for s in range(S):
-            dw[:, :, r, s] = np.einsum("nkpq,ncpq->kc", dyl, xp[:, :, r:r + P, s:s + Q])
+            win = xp[:, :, r:r + (P - 1) * sh + 1:sh, s:s + (Q - 1) * sw + 1:sw]
+            dw[:, :, r, s] = np.einsum("nkpq,ncpq->kc", dyl, win)
     return dw.reshape(K // 16, 16, C // 16, 16, R, S).transpose(0, 2, 4, 5, 3, 1).ravel()
+
+
+WGRAD = [
+    ("conv:16,48,32,10,10,3,3,1,1,16,1,1,10,10", None),            # K = 48: odd blocks, zero fill
+    ("conv:32,64,16,12,12,1,1,1,1,16,0,0,12,12", None),            # C = 16: one block
+    ("conv:16,16,16,9,9,5,5,1,1,16,2,2,9,9", None),                # K = C = 16
+    ("conv:64,64,64,14,14,3,3,1,1,16,1,1,14,14", None),            # ResNet-style 3x3, K = 64
+    ("conv:5,128,96,13,11,3,3,1,1,16,1,1,13,11", None),            # ragged N, C = 96, 13x11
+    ("conv:4,256,128,7,7,3,3,2,2,16,1,1,14,14", None),             # 3x3 / stride 2
+    ("conv:6,128,64,14,14,1,1,2,2,16,0,0,28,28", None),            # 1x1 / stride 2 (downsample)
+    ("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32", None),             # 7x7 / stride 2 (stem-shaped)
+    ("conv:8,128,64,10,10,3,3,1,1,16,1,1,10,10", "gpu=sw:0,kn:128,cn:64,nt:2,box:10x4,sp:5"),
+    ("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10", "gpu=sw:1,kn:64,cn:64,nt:2,box:8x1,sp:3,st:3,ch:8"),
+    ("conv:8,256,128,8,8,3,3,1,1,16,1,1,8,8", "gpu=sw:0,kn:128,cn:128,nt:1,box:8x2"),
+]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
-@pytest.mark.parametrize("conv,recipe", [
-    ("conv:16,48,32,10,10,3,3,1,1,16,1,1,10,10", None),
-    ("conv:32,64,16,12,12,1,1,1,1,16,0,0,12,12", None),
-    ("conv:16,16,16,9,9,5,5,1,1,16,2,2,9,9", None),
-    ("conv:64,64,64,14,14,3,3,1,1,16,1,1,14,14", None),          # ResNet-style 3x3 at small N
-    ("conv:16,48,32,10,10,3,3,1,1,16,1,1,10,10", "gpu=bn:16,ks:5,kt:1"),
-])
+@pytest.mark.parametrize("conv,recipe", WGRAD)
 def test_backward_weight(conv, recipe, mode):
-    """dW = conv_bwd_weight(X, dY): the role-swapped forward conv (images = input channels,
-    channels = batch, filter = dY) split-K over N*P*Q, against float64."""
+    """dW = conv_bwd_weight(X, dY): the pixel-major wgrad kernel (MN-major tf32 operands,
+    pixel-range splits added in split order), against float64."""
     p = ps.ConvPreset.parse(conv)
     rng = np.random.default_rng(26)
     x = rng.uniform(-1, 1, p.input_elems()).astype(np.float32)
@@ -717,6 +730,8 @@ def test_backward_weight(conv, recipe, mode):
     ref = _wgrad_ref(p, x, dy)
     dev = torch.device("cuda:0")
     dw = torch.full((p.filter_elems(),), float("nan"), device=dev)
+    if recipe and mode == "tf32" and ",ch:" in recipe:
+        recipe = recipe[:recipe.index(",ch:")]
     plan = ps.WgradPlan(p, mode=mode, device=0, recipe=recipe)
     plan.forward(torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev), dw)
     torch.cuda.synchronize()
@@ -727,11 +742,36 @@ def test_backward_weight(conv, recipe, mode):
     assert err <= TOL[mode], f"relL2 {err:.3e} ({plan.recipe})"
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_backward_weight_resnet_layer(mode):
+    """ResNet-50 l1 3x3 shape at N = 32 (the K = 64 swapped-role tiles, 56x56 boxes) and
+    bitwise run-to-run reproducibility (fixed split order)."""
+    p = ps.ConvPreset.parse("conv:32,64,64,56,56,3,3,1,1,16,1,1,56,56")
+    rng = np.random.default_rng(27)
+    x = rng.uniform(-1, 1, p.input_elems()).astype(np.float32)
+    dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
+    ref = _wgrad_ref(p, x, dy)
+    dev = torch.device("cuda:0")
+    xd, dyd = torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev)
+    plan = ps.WgradPlan(p, mode=mode, device=0)
+    outs = []
+    for _ in range(2):
+        dw = torch.full((p.filter_elems(),), float("nan"), device=dev)
+        plan.forward(xd, dyd, dw)
+        torch.cuda.synchronize()
+        outs.append(dw.cpu().numpy())
+    assert oracle.rel_l2(outs[0], ref) <= TOL[mode], plan.recipe
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_backward_weight_rejects():
     with pytest.raises(ps.ConfigRejectedError):
-        ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"))   # nImg % 16
+        ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"), mode="f16x2")
     with pytest.raises(ps.ConfigRejectedError):
-        ps.WgradPlan(ps.ConvPreset.parse("conv:16,64,64,5,5,3,3,2,2,16,1,1,10,10"))    # stride 2
+        ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"), recipe="gpu=box:7x1")
+    with pytest.raises(ps.ConfigRejectedError):
+        ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"), recipe="gpu=zz:1")
 
 
 @pytest.mark.gpu
