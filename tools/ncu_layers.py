@@ -3,8 +3,8 @@ layer): runs every (layer, mode) of a sweep file once with its tuned recipe (pre
 in order, so that one ncu session can attribute the conv kernel launches to layers.
 
   ncu --metrics <M> --clock-control none -k regex:"conv_(fwd|pp)_sm100" --csv \\
-      --log-file gpurun_out/ncu_layers.csv python tools/ncu_layers.py run profiles/r01_sweep.jsonl
-  python tools/ncu_layers.py table profiles/r01_sweep.jsonl gpurun_out/ncu_layers.csv > profiles/r01_ncu_layers.md
+      --log-file gpurun_out/ncu_layers.csv python tools/ncu_layers.py run profiles/r02_sweep.jsonl
+  python tools/ncu_layers.py table profiles/r02_sweep.jsonl gpurun_out/ncu_layers.csv > profiles/r02_ncu_layers.md
 (M: see METRICS; cold caches and serialised launches, so absolute times run above the bench's)
 """
 import csv
@@ -18,7 +18,22 @@ sys.path.insert(0, ROOT)
 METRICS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
            "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "dram__bytes_read.sum", "dram__bytes_write.sum",
-           "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+           "lts__t_sectors_srcunit_tex_op_read.sum"]
+
+
+def records(sweep):
+    """(layer, mode) records of a sweep file: r01 rows are per (layer, mode); r02 rows per layer
+    with a "modes" map."""
+    out = []
+    for r in map(json.loads, open(sweep)):
+        if "modes" in r:
+            for mode, m in r["modes"].items():
+                out.append({"layer": r["layer"], "mode": mode, "recipe": m["recipe"],
+                            "mb_compulsory": r["mb_compulsory"]})
+        else:
+            out.append(r)
+    return out
 
 
 def run(sweep):
@@ -26,7 +41,7 @@ def run(sweep):
     import paper_2002_02145_b200 as ps
     from paper_2002_02145_b200.workloads import ALL, seeds
     dev = torch.device("cuda:0")
-    for r in map(json.loads, open(sweep)):
+    for r in records(sweep):
         conv, c_log, cid = ALL[r["layer"]]
         p = ps.ConvPreset.parse(conv)
         x = torch.empty(p.input_elems(), device=dev)
@@ -45,7 +60,7 @@ def run(sweep):
 
 
 def table(sweep, ncu_csv):
-    recs = [json.loads(l) for l in open(sweep)]
+    recs = records(sweep)
     rows = [r for r in csv.reader(open(ncu_csv)) if len(r) > 10 and r[0].isdigit()]
     # long format: one row per (launch id, metric)
     by_id = {}
@@ -57,17 +72,19 @@ def table(sweep, ncu_csv):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "hz": 1,
              "msecond": 1e-3, "Hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "%": 1}
     print("# Per-layer ncu (1 B200, `tools/ncu_layers.py`; cold caches, serialised launches, clock-control none)\n")
-    print("| layer | mode | kernel us | SM GHz | tensor pipe % | DRAM MB | DRAM GB/s | DRAM % of peak | compulsory MB |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("| layer | mode | kernel us | SM GHz | tensor pipe % | DRAM MB | DRAM / compulsory | DRAM GB/s | DRAM % of peak "
+          "| compulsory MB | L2->SM MB |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|")
     for i, r in zip(ids, recs):
         m = by_id[i]
         v = {k: m[k][0] * scale.get(m[k][1], 1) for k in m}
         t = v["gpu__time_duration.sum"]
         mb = (v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]) / 1e6
+        l2 = v.get("lts__t_sectors_srcunit_tex_op_read.sum", 0.0) * 32 / 1e6
         print(f"| {r['layer']} | {r['mode']} | {t * 1e6:.1f} | {v['sm__cycles_elapsed.avg.per_second'] / 1e9:.2f} | "
               f"{v['sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed']:.1f} | {mb:.1f} | "
-              f"{mb / 1e3 / t:.0f} | {v['dram__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
-              f"{r['mb_compulsory']} |")
+              f"{mb / r['mb_compulsory']:.3f} | {mb / 1e3 / t:.0f} | "
+              f"{v['dram__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | {r['mb_compulsory']} | {l2:.0f} |")
 
 
 if __name__ == "__main__":
