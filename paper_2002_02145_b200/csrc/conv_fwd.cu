@@ -66,6 +66,8 @@ struct conv_plan {
   bool bwd_weight = false;
   psconv::WgradParams wg{};
   float* wg_ws = nullptr;
+  float* wg_x32 = nullptr;  // TMA path: X / dY relaid into 32-channel blocks (+ 3xTF32 lo halves)
+  float* wg_y32 = nullptr;
   mutable bool prepacked = false;  // flt_pack holds the filter given to conv_plan_prepack
   int64_t flt_elems = 0;
   // conv_fwd_host staging (lazily created): double-buffered device chunks,
@@ -1226,7 +1228,7 @@ namespace {
 // range so that the units fill the SMs once. A recipe "gpu=sw:S,kn:K,cn:C,nt:T,box:QxP,
 // sp:SPLITS,st:STAGES,ch:K8" overrides any of the choices.
 struct WgPick {
-  int swap = -1, kn = 0, cn = 0, ntap = 0, qb = 0, pb = 0, splits = 0, stages = 0, chunk = -1;
+  int swap = -1, kn = 0, cn = 0, ntap = 0, qb = 0, pb = 0, splits = 0, stages = 0, chunk = -1, tma = -1;
 };
 WgPick parse_wgrad_recipe(const char* recipe) {
   WgPick w;
@@ -1256,7 +1258,10 @@ WgPick parse_wgrad_recipe(const char* recipe) {
     else if (k == "sp") w.splits = num(v);
     else if (k == "st") w.stages = num(v);
     else if (k == "ch") w.chunk = num(v);
-    else if (k == "box") {
+    else if (k == "tma") {
+      w.tma = num(v);
+      if (w.tma > 1) throw ConfigError("backward-weight recipe: tma:0|1");
+    } else if (k == "box") {
       const auto x = v.find('x');
       if (x == std::string::npos) throw ConfigError("backward-weight recipe: box:QxP");
       w.qb = num(v.substr(0, x));
@@ -1272,7 +1277,8 @@ WgPick parse_wgrad_recipe(const char* recipe) {
 std::string wgrad_recipe(const WgradParams& g) {
   return "gpu=sw:" + std::to_string(g.swap) + ",kn:" + std::to_string(g.kn) + ",cn:" + std::to_string(g.cn) +
          ",nt:" + std::to_string(g.ntap) + ",box:" + std::to_string(g.Qb) + "x" + std::to_string(g.Pb) +
-         ",sp:" + std::to_string(g.splits) + ",st:" + std::to_string(g.stages) + ",ch:" + std::to_string(g.chunk_k8);
+         ",sp:" + std::to_string(g.splits) + ",st:" + std::to_string(g.stages) + ",ch:" + std::to_string(g.chunk_k8) +
+         ",tma:" + std::to_string(g.tma);
 }
 
 constexpr int kWgSmemBudget = 227 * 1024 - 6144;  // ring; the rest: alignment, barriers, row/tap tables
@@ -1395,15 +1401,22 @@ WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* re
   // 3xTF32 accumulation chunks (~32 K=8 steps: error ~6e-8 per step)
   g.chunk_k8 = split3 ? (want.chunk >= 0 ? want.chunk : 32) : 0;
   if (split3 && g.chunk_k8 > 0 && g.chunk_k8 < g.rows / 8) g.chunk_k8 = g.rows / 8;
+  g.Cb2 = (Cb + 1) / 2;
+  g.Kb2 = (Kb + 1) / 2;
+  // TMA path: one relayout pass over X and dY buys dense TMA boxes (about twice the cp.async
+  // gather's L2->SM rate); the gather stays for boxes TMA cannot express (> 256 px per dim)
+  g.tma = want.tma >= 0 ? want.tma : 1;
+  if (g.tma && (g.Qb * g.sw > 256 || g.Pb * g.sh > 256))
+    throw ConfigError("backward weight: tma:1 needs Qb*stride_w and Pb*stride_h <= 256");
   return g;
 }
 
-template <int BN, bool SPLIT3>
-void launch_wgrad_kernel(const conv_plan* P, const WgradParams& g, cudaStream_t st) {
-  using Cfg = WgCfg<BN, SPLIT3>;
+template <int BN, bool SPLIT3, bool TMA>
+void launch_wgrad_kernel(const conv_plan* P, const WgradParams& g, const CUtensorMap* tm, cudaStream_t st) {
+  using Cfg = WgCfg<BN, SPLIT3, TMA>;
   const int smem = g.stages * g.stage_bytes + 6144;
   static SmemAttr attr_once;  // the largest ring any plan may use (set once per device)
-  CUDA_OK(attr_once.ensure(wgrad_sm100<BN, SPLIT3>, kWgSmemBudget + 6144, P->device));
+  CUDA_OK(attr_once.ensure(wgrad_sm100<BN, SPLIT3, TMA>, kWgSmemBudget + 6144, P->device));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(g.units, P->num_sms));
   cfg.blockDim = dim3(Cfg::kThreads);
@@ -1414,7 +1427,30 @@ void launch_wgrad_kernel(const conv_plan* P, const WgradParams& g, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = std::getenv("PSCONV_NO_PDL") ? 0 : 1;
-  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_sm100<BN, SPLIT3>, g));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_sm100<BN, SPLIT3, TMA>, g, tm[0], tm[1], tm[2], tm[3]));
+}
+
+template <int BN, bool SPLIT3>
+void launch_wgrad_bn(const conv_plan* P, const WgradParams& g, const CUtensorMap* tm, cudaStream_t st) {
+  if (g.tma)
+    launch_wgrad_kernel<BN, SPLIT3, true>(P, g, tm, st);
+  else
+    launch_wgrad_kernel<BN, SPLIT3, false>(P, g, tm, st);
+}
+
+void launch_relayout(const float* in, float* out, bool lo, int Cb, int Cb2, int64_t N, int64_t HW, cudaStream_t st) {
+  const int64_t pieces = N * Cb2 * HW * 8;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_for(pieces));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_relayout_kernel, in, out, lo ? out + pieces * 4 : nullptr, Cb, Cb2, HW,
+                             pieces));
 }
 
 void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw, cudaStream_t st) {
@@ -1427,13 +1463,44 @@ void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw
   }();
   g.debug = debug_env & 3;
   const bool split3 = P->mode == PSCONV_MODE_3XTF32;
-#define PSCONV_WG(B) (split3 ? launch_wgrad_kernel<B, true>(P, g, st) : launch_wgrad_kernel<B, false>(P, g, st))
+  CUtensorMap tm[4];
+  std::memset(tm, 0, sizeof tm);
+  if (g.tma) {
+    const int64_t HW = int64_t(g.H) * g.W, PQ = int64_t(g.P) * g.Q;
+    launch_relayout(x, P->wg_x32, split3, g.Cb, g.Cb2, g.N, HW, st);
+    launch_relayout(dy, P->wg_y32, split3, g.Kb, g.Kb2, g.N, PQ, st);
+    const cuuint32_t ex[5] = {1, cuuint32_t(g.sw), cuuint32_t(g.sh), 1, 1};
+    const cuuint32_t e1[5] = {1, 1, 1, 1, 1};
+    {  // X32 [N][Cb2][H][W][32]: box {32, Qb*sw, Pb*sh, cn/32, 1}
+      const cuuint64_t dims[5] = {32, cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.Cb2), cuuint64_t(g.N)};
+      const cuuint64_t strides[4] = {128, cuuint64_t(g.W) * 128, cuuint64_t(HW) * 128, cuuint64_t(g.Cb2) * HW * 128};
+      const cuuint32_t box[5] = {32, cuuint32_t(g.Qb * g.sw), cuuint32_t(g.Pb * g.sh), cuuint32_t(g.cn / 32), 1};
+      encode(&tm[0], P->wg_x32, 5, dims, strides, box, ex, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+             g.sw > 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      tm[1] = tm[0];
+      if (split3)
+        encode(&tm[1], P->wg_x32 + int64_t(g.N) * g.Cb2 * HW * 32, 5, dims, strides, box, ex,
+               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+               g.sw > 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    }
+    {  // dY32 [N][Kb2][P][Q][32]: box {32, Qb, Pb, kn/32, 1}
+      const cuuint64_t dims[5] = {32, cuuint64_t(g.Q), cuuint64_t(g.P), cuuint64_t(g.Kb2), cuuint64_t(g.N)};
+      const cuuint64_t strides[4] = {128, cuuint64_t(g.Q) * 128, cuuint64_t(PQ) * 128, cuuint64_t(g.Kb2) * PQ * 128};
+      const cuuint32_t box[5] = {32, cuuint32_t(g.Qb), cuuint32_t(g.Pb), cuuint32_t(g.kn / 32), 1};
+      encode(&tm[2], P->wg_y32, 5, dims, strides, box, e1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      tm[3] = tm[2];
+      if (split3)
+        encode(&tm[3], P->wg_y32 + int64_t(g.N) * g.Kb2 * PQ * 32, 5, dims, strides, box, e1,
+               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+  }
+#define PSCONV_WG(B) (split3 ? launch_wgrad_bn<B, true>(P, g, tm, st) : launch_wgrad_bn<B, false>(P, g, tm, st))
   switch (g.bn) {
     case 32: PSCONV_WG(32); break;
     case 64: PSCONV_WG(64); break;
     case 128: PSCONV_WG(128); break;
-    case 192: launch_wgrad_kernel<192, false>(P, g, st); break;
-    case 256: launch_wgrad_kernel<256, false>(P, g, st); break;
+    case 192: launch_wgrad_bn<192, false>(P, g, tm, st); break;
+    case 256: launch_wgrad_bn<256, false>(P, g, tm, st); break;
     default: throw RuntimeError("internal: wgrad bn");
   }
 #undef PSCONV_WG
@@ -1613,8 +1680,17 @@ int conv_plan_create_bwd_weight(const conv_desc* d_in, int mode, int device, con
     P->wg = g;
     P->sched.recipe_id = wgrad_recipe(g);
     DeviceGuard guard(device);
-    const cudaError_t e = cudaMalloc(&P->wg_ws, size_t(g.units) * 128 * g.bn * sizeof(float));
+    cudaError_t e = cudaMalloc(&P->wg_ws, size_t(g.units) * 128 * g.bn * sizeof(float));
+    if (e == cudaSuccess && g.tma) {
+      const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;  // hi (raw) | lo
+      e = cudaMalloc(&P->wg_x32, size_t(copies) * f.nImg * g.Cb2 * 32 * f.ifh * f.ifw * sizeof(float));
+      if (e == cudaSuccess)
+        e = cudaMalloc(&P->wg_y32, size_t(copies) * f.nImg * g.Kb2 * 32 * f.ofh * f.ofw * sizeof(float));
+    }
     if (e != cudaSuccess) {
+      cudaFree(P->wg_ws);
+      cudaFree(P->wg_x32);
+      cudaFree(P->wg_y32);
       delete P;
       throw RuntimeError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
@@ -1684,6 +1760,8 @@ void conv_plan_destroy(conv_plan* p) {
     cudaFree(p->split_ws);
     cudaFree(p->absmax);
     cudaFree(p->wg_ws);
+    cudaFree(p->wg_x32);
+    cudaFree(p->wg_y32);
     cudaFree(p->wtrans);
     cudaSetDevice(prev);
   }

@@ -62,6 +62,8 @@ struct WgradParams {
   int stage_bytes;                  // x + y (x2 for 3xTF32: hi | lo)
   int chunk_k8;                     // 3xTF32: K=8 steps per accumulation chunk (0: whole unit)
   int debug;                        // profiling (PSCONV_DEBUG): 1 skip copies, 2 skip MMAs
+  int tma;                          // 1: TMA path over the relaid X / dY (else cp.async gather)
+  int Cb2, Kb2;                     // TMA path: 32-channel blocks of the relaid X / dY
   const float* x;                   // NCHW16c forward input
   const float* dy;                  // NKPQ16k output gradient
   float* ws;                        // partials [unit][128][bn]
@@ -90,9 +92,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 }  // namespace ptx
 
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, bool TMA = false>
 struct WgCfg {
-  static constexpr int kThreads = 32 * (5 + kWgProdWarps);  // 4 epilogue + 1 MMA + producer warps
+  // 4 epilogue + 1 MMA + producer warps (the TMA path: one producer warp)
+  static constexpr int kThreads = 32 * (5 + (TMA ? 1 : kWgProdWarps));
   static constexpr int kAccCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   static constexpr uint32_t kTmemCols = 2 * kAccCols;  // two accumulators (power of 2, >= 64)
 };
@@ -204,10 +207,18 @@ struct WgProducer {
   }
 };
 
-template <int BN, bool SPLIT3>
-__global__ void __launch_bounds__(WgCfg<BN, SPLIT3>::kThreads, 1) wgrad_sm100(const __grid_constant__ WgradParams p) {
+// TMA path (recipe tma:1): X and dY relaid once per call into 32-channel blocks
+// ([N][C/32][H][W][32], wgrad_relayout_kernel; 3xTF32: + the lo halves), so one pixel's 32
+// channels are 128 contiguous bytes -- a TMA box with a 128-B inner dimension lands dense in the
+// SWIZZLE_128B_ATOM_32B layout, one box per tap (X) / per stage (dY), multicast-free, ~2x the
+// L2->SM rate of the cp.async gather.
+template <int BN, bool SPLIT3, bool TMA = false>
+__global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
+    wgrad_sm100(const __grid_constant__ WgradParams p, const __grid_constant__ CUtensorMap tm_x,
+                const __grid_constant__ CUtensorMap tm_xlo, const __grid_constant__ CUtensorMap tm_y,
+                const __grid_constant__ CUtensorMap tm_ylo) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using Cfg = WgCfg<BN, SPLIT3>;
+  using Cfg = WgCfg<BN, SPLIT3, TMA>;
   constexpr uint32_t kIdesc = ptx::idesc_tf32_mn<BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3>::kThreads, 1) wgrad_sm100(co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 32 * kWgProdWarps);
+      ptx::mbar_init(&full[s], TMA ? 1 : 32 * kWgProdWarps);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -256,7 +267,50 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3>::kThreads, 1) wgrad_sm100(co
   const int k8_stage = p.rows / 8;
   const int chunk_st = (SPLIT3 && p.chunk_k8 > 0) ? max(1, p.chunk_k8 / k8_stage) : (1 << 30);
 
-  if (warp >= 5) {
+  if (TMA && warp == 5) {
+    // ------------------------------------------------------------ producer (TMA)
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&tm_x);
+      ptx::prefetch_tmap(&tm_y);
+    }
+    ptx::griddep_wait();
+    __syncwarp();
+    const uint32_t tx = static_cast<uint32_t>(p.x_bytes + p.y_bytes) * (SPLIT3 ? 2u : 1u);
+    const uint32_t lo = static_cast<uint32_t>(p.x_bytes + p.y_bytes);
+    const uint32_t tap_bytes = static_cast<uint32_t>(p.cn) * p.rows * 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int split = u / p.tiles, tile = u - split * p.tiles;
+      const int ct = tile % p.tiles_c, tt = (tile / p.tiles_c) % p.tiles_t, kt = tile / (p.tiles_c * p.tiles_t);
+      const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
+      for (int g = g0; g < g1; ++g) {
+        int n, p0, q0;
+        wg_stage_coords(p, g, n, p0, q0);
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (ptx::elect_one()) {
+          uint8_t* sb = smem + stage * p.stage_bytes;
+          ptx::mbar_expect_tx(&full[stage], tx);
+          for (int t = 0; t < p.ntap; ++t) {
+            // taps past R*S (a partial last tap group) load the last tap again; the reduce
+            // kernel never reads those accumulator rows / columns
+            const int tap = min(tt * p.ntap + t, p.R * p.S - 1);
+            const int r = tap / p.S, sx = tap - r * p.S;
+            const int wq = q0 * p.sw + sx - p.pw, hp = p0 * p.sh + r - p.ph;
+            ptx::tma_load_5d(sb + t * tap_bytes, &tm_x, &full[stage], 0, wq, hp, ct * (p.cn / 32), n);
+            if (SPLIT3) ptx::tma_load_5d(sb + lo + t * tap_bytes, &tm_xlo, &full[stage], 0, wq, hp, ct * (p.cn / 32), n);
+          }
+          ptx::tma_load_5d(sb + p.x_bytes, &tm_y, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
+          if (SPLIT3) ptx::tma_load_5d(sb + lo + p.x_bytes, &tm_ylo, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (!TMA && warp >= 5) {
     // ------------------------------------------------------------ producers (cp.async)
     WgProducer<kWgProdWarps> pr;
     pr.init(threadIdx.x - 160);
@@ -443,6 +497,35 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3>::kThreads, 1) wgrad_sm100(co
     ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 #endif
+}
+
+// TMA path: NCHW16c (or NKPQ16k) -> [N][C/32][H][W][32] (an odd last block's partner is
+// zero); lo != nullptr also writes lo = x - trunc_tf32(x) in the same layout. One thread per
+// 16-B piece of the output.
+__global__ void wgrad_relayout_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ lo,
+                                      int Cb, int Cb2, int64_t HW, int64_t n_pieces) {
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_pieces; e += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(e & 7);  // 16-B piece of the 128-B pixel row
+    const int64_t t = e >> 3;  // (n, cb2, pixel)
+    const int64_t px = t % HW;
+    const int64_t nc = t / HW;
+    const int cb2 = int(nc % Cb2);
+    const int64_t n = nc / Cb2;
+    const int cb = 2 * cb2 + (j >> 2);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cb < Cb) v = __ldg(reinterpret_cast<const float4*>(in + ((n * Cb + cb) * HW + px) * 16) + (j & 3));
+    reinterpret_cast<float4*>(out)[e] = v;
+    if (lo) {
+      float4 l;
+      l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+      l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+      l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+      l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+      reinterpret_cast<float4*>(lo)[e] = l;
+    }
+  }
 }
 
 // dW (KCRS16c16k) = the split partials of every tile added in split order.
