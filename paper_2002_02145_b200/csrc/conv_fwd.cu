@@ -1404,8 +1404,25 @@ WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* re
   g.Cb2 = (Cb + 1) / 2;
   g.Kb2 = (Kb + 1) / 2;
   // TMA path: one relayout pass over X and dY buys dense TMA boxes (about twice the cp.async
-  // gather's L2->SM rate); the gather stays for boxes TMA cannot express (> 256 px per dim)
-  g.tma = want.tma >= 0 ? want.tma : 1;
+  // gather's L2->SM rate). Pick by modelled time: L2->SM bytes at the measured rates (TMA
+  // ~10.4 TB/s, gather ~4.5 TB/s: l3 3x3 TF32, tools/_wgt.py), the MMA time at the N floor, the
+  // compulsory HBM bytes, plus the relayout pass (read X + dY, write them once per copy) for TMA.
+  // HBM-heavy 1x1 layers keep the gather (l1 1x1 64->256 TF32: 272 vs 510 us).
+  const bool fits = g.Qb * g.sw <= 256 && g.Pb * g.sh <= 256;
+  if (want.tma >= 0) {
+    g.tma = want.tma;
+  } else {
+    const double xb = 4.0 * f.nImg * Cb * 16 * f.ifh * f.ifw, yb = 4.0 * f.nImg * Kb * 16 * P * Q;
+    const double l2 = double(g.units) * g.stage_per_split * (g.x_bytes + g.y_bytes);  // hi bytes
+    const double k8 = double(g.units) * g.stage_per_split * (g.rows / 8);
+    const double mma_cyc = std::max(g.bn / 2.0, g.bn <= 64 ? 45.0 : 0.0) * (split3 ? 3 : 1);
+    const double t_mma = k8 * mma_cyc / num_sms / 1.8e9;
+    const double hbm = (xb + yb) / 6.0e12;
+    // (3xTF32 gather: the producers also split every piece, ~2.2x slower per byte, measured)
+    const double t_cp = std::max({t_mma, l2 / (split3 ? 2.0e12 : 4.5e12), hbm});
+    const double t_tma = (xb + yb) * (split3 ? 3 : 2) / 6.0e12 + std::max({t_mma, l2 * mult / 10.4e12, hbm});
+    g.tma = (fits && t_tma < t_cp) ? 1 : 0;
+  }
   if (g.tma && (g.Qb * g.sw > 256 || g.Pb * g.sh > 256))
     throw ConfigError("backward weight: tma:1 needs Qb*stride_w and Pb*stride_h <= 256");
   return g;
