@@ -160,9 +160,14 @@ class WgradPlan:
     pixel-major wgrad kernel (MN-major tf32 operands straight from the activation layouts,
     split over pixel ranges, partials added in split order)."""
 
-    def __init__(self, preset: "ConvPreset", mode="3xtf32", device: int = 0, recipe: str | None = None):
+    def __init__(self, preset: "ConvPreset", mode="3xtf32", device: int = 0, recipe: str | None = None,
+                 c_logical: int = 0):
+        """c_logical < 16 on a one-block (nIfm = 16) layer whose padded input channels are zero
+        (the ResNet stem): the tap-folded path (recipe pp:C)."""
         if isinstance(mode, str):
             mode = _MODES[mode.lower()]
+        if c_logical and c_logical < 16 and preset.nIfm == 16 and not (recipe and "pp:" in recipe):
+            recipe = f"{recipe},pp:{c_logical}" if recipe and "gpu=" in recipe else f"gpu=pp:{c_logical}"
         self.preset = ConvPreset(**{f.name: getattr(preset, f.name) for f in fields(preset)}).validate()
         self.mode = mode
         self.device = device

@@ -1229,6 +1229,7 @@ namespace {
 // sp:SPLITS,st:STAGES,ch:K8" overrides any of the choices.
 struct WgPick {
   int swap = -1, kn = 0, cn = 0, ntap = 0, qb = 0, pb = 0, splits = 0, stages = 0, chunk = -1, tma = -1;
+  int pp = 0;  // tap fold for few-channel layers: the real channel count
 };
 WgPick parse_wgrad_recipe(const char* recipe) {
   WgPick w;
@@ -1258,6 +1259,7 @@ WgPick parse_wgrad_recipe(const char* recipe) {
     else if (k == "sp") w.splits = num(v);
     else if (k == "st") w.stages = num(v);
     else if (k == "ch") w.chunk = num(v);
+    else if (k == "pp") w.pp = num(v);
     else if (k == "tma") {
       w.tma = num(v);
       if (w.tma > 1) throw ConfigError("backward-weight recipe: tma:0|1");
@@ -1278,13 +1280,12 @@ std::string wgrad_recipe(const WgradParams& g) {
   return "gpu=sw:" + std::to_string(g.swap) + ",kn:" + std::to_string(g.kn) + ",cn:" + std::to_string(g.cn) +
          ",nt:" + std::to_string(g.ntap) + ",box:" + std::to_string(g.Qb) + "x" + std::to_string(g.Pb) +
          ",sp:" + std::to_string(g.splits) + ",st:" + std::to_string(g.stages) + ",ch:" + std::to_string(g.chunk_k8) +
-         ",tma:" + std::to_string(g.tma);
+         ",tma:" + std::to_string(g.tma) + (g.fc ? ",pp:" + std::to_string(g.fc) : std::string());
 }
 
 constexpr int kWgSmemBudget = 227 * 1024 - 6144;  // ring; the rest: alignment, barriers, row/tap tables
 
-WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* recipe) {
-  const WgPick want = parse_wgrad_recipe(recipe);
+WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgPick& want) {
   const bool split3 = mode == PSCONV_MODE_3XTF32;
   const int C = int(f.nIfm), K = int(f.nOfm), RS = int(f.kh * f.kw);
   const int Cb = C / 16, Kb = K / 16;
@@ -1423,8 +1424,42 @@ WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* re
     const double t_tma = (xb + yb) * (split3 ? 3 : 2) / 6.0e12 + std::max({t_mma, l2 * mult / 10.4e12, hbm});
     g.tma = (fits && t_tma < t_cp) ? 1 : 0;
   }
+  if (want.pp) g.tma = 1;  // the tap fold's relayout is the TMA input
   if (g.tma && (g.Qb * g.sw > 256 || g.Pb * g.sh > 256))
     throw ConfigError("backward weight: tma:1 needs Qb*stride_w and Pb*stride_h <= 256");
+  return g;
+}
+
+// Few-channel layers (recipe pp:C, C real channels in the first 16-channel block, e.g. the
+// ResNet stem's 3): the wgrad of the 1x1 conv over the folded input X' (per output pixel the
+// R*S*C window values, padded to a multiple of 32) -- R*S*C / 32 channel groups instead of R*S
+// taps x 32 channels of which C are real (the stem: 5 groups for 49 taps of 3 channels).
+WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* recipe) {
+  WgPick want = parse_wgrad_recipe(recipe);
+  if (!want.pp) return wgrad_geom_core(f, mode, num_sms, want);
+  const int fc = want.pp;
+  if (fc > 16 || f.nIfm != 16) throw ConfigError("backward-weight recipe: pp:C needs nIfm = 16 and C <= 16");
+  if (want.tma == 0) throw ConfigError("backward-weight recipe: pp:C runs on the TMA path");
+  if (want.ntap > 1) throw ConfigError("backward-weight recipe: pp:C folds the taps (no nt:)");
+  const int64_t T = f.kh * f.kw * fc;
+  conv_desc fd = f;
+  fd.nIfm = (T + 31) / 32 * 32;
+  fd.kh = fd.kw = 1;
+  fd.stride_h = fd.stride_w = 1;
+  fd.pad_h = fd.pad_w = 0;
+  fd.ifh = f.ofh;
+  fd.ifw = f.ofw;
+  WgradParams g = wgrad_geom_core(fd, mode, num_sms, want);
+  g.fc = fc;
+  g.oCb = int(f.nIfm / 16);
+  g.oR = int(f.kh);
+  g.oS = int(f.kw);
+  g.oH = int(f.ifh);
+  g.oW = int(f.ifw);
+  g.osh = int(f.stride_h);
+  g.osw = int(f.stride_w);
+  g.oph = int(f.pad_h);
+  g.opw = int(f.pad_w);
   return g;
 }
 
@@ -1484,7 +1519,28 @@ void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw
   std::memset(tm, 0, sizeof tm);
   if (g.tma) {
     const int64_t HW = int64_t(g.H) * g.W, PQ = int64_t(g.P) * g.Q;
-    launch_relayout(x, P->wg_x32, split3, g.Cb, g.Cb2, g.N, HW, st);
+    if (g.fc) {
+      const int64_t pieces = int64_t(g.N) * g.Cb2 * HW * 8, n_rows = int64_t(g.N) * g.P;
+      const int win = (kFoldQ - 1) * g.osw + g.oS;
+      const int fold_smem = g.oR * win * ((g.fc + 3) / 4) * 16 + g.Cb2 * 32 * 4 + kFoldQ * 36 * 4;
+      static SmemAttr fold_attr;
+      CUDA_OK(fold_attr.ensure(wgrad_fold_kernel, 160 * 1024, P->device));
+      if (fold_smem > 160 * 1024) throw RuntimeError("backward weight: tap-fold window larger than shared memory");
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(int(std::min<int64_t>(n_rows * ((g.Q + kFoldQ - 1) / kFoldQ), 148 * 16)));
+      cfg.blockDim = dim3(kFoldQ);
+      cfg.dynamicSmemBytes = fold_smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_fold_kernel, g, x, P->wg_x32, split3 ? P->wg_x32 + pieces * 4 : nullptr,
+                                 n_rows));
+    } else {
+      launch_relayout(x, P->wg_x32, split3, g.Cb, g.Cb2, g.N, HW, st);
+    }
     launch_relayout(dy, P->wg_y32, split3, g.Kb, g.Kb2, g.N, PQ, st);
     const cuuint32_t ex[5] = {1, cuuint32_t(g.sw), cuuint32_t(g.sh), 1, 1};
     const cuuint32_t e1[5] = {1, 1, 1, 1, 1};
@@ -1521,7 +1577,7 @@ void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw
     default: throw RuntimeError("internal: wgrad bn");
   }
 #undef PSCONV_WG
-  const int64_t n = int64_t(g.Kb) * 16 * g.Cb * 16 * g.R * g.S;
+  const int64_t n = g.fc ? int64_t(g.Kb) * 16 * g.oCb * 16 * g.oR * g.oS : int64_t(g.Kb) * 16 * g.Cb * 16 * g.R * g.S;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid_for(n));
   cfg.blockDim = dim3(256);
@@ -1700,9 +1756,9 @@ int conv_plan_create_bwd_weight(const conv_desc* d_in, int mode, int device, con
     cudaError_t e = cudaMalloc(&P->wg_ws, size_t(g.units) * 128 * g.bn * sizeof(float));
     if (e == cudaSuccess && g.tma) {
       const int copies = mode == PSCONV_MODE_3XTF32 ? 2 : 1;  // hi (raw) | lo
-      e = cudaMalloc(&P->wg_x32, size_t(copies) * f.nImg * g.Cb2 * 32 * f.ifh * f.ifw * sizeof(float));
+      e = cudaMalloc(&P->wg_x32, size_t(copies) * g.N * g.Cb2 * 32 * g.H * g.W * sizeof(float));
       if (e == cudaSuccess)
-        e = cudaMalloc(&P->wg_y32, size_t(copies) * f.nImg * g.Kb2 * 32 * f.ofh * f.ofw * sizeof(float));
+        e = cudaMalloc(&P->wg_y32, size_t(copies) * g.N * g.Kb2 * 32 * g.P * g.Q * sizeof(float));
     }
     if (e != cudaSuccess) {
       cudaFree(P->wg_ws);

@@ -765,6 +765,31 @@ def test_backward_weight_resnet_layer(mode):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log", [("conv:2,64,16,16,16,7,7,2,2,16,3,3,32,32", 3),   # stem-shaped
+                                        ("conv:3,32,16,9,9,3,3,1,1,16,1,1,9,9", 5),
+                                        ("conv:2,64,16,8,8,5,5,2,2,16,2,2,16,16", 16)])
+def test_backward_weight_tap_fold(conv, c_log, mode):
+    """Few-channel layers (pp:C): the 1x1 wgrad over the tap-folded input; the padded channels
+    of X are zero and their dW is zero."""
+    p = ps.ConvPreset.parse(conv)
+    rng = np.random.default_rng(28)
+    x = rng.uniform(-1, 1, p.input_elems()).astype(np.float32)
+    x.reshape(p.nImg, 1, p.ifh, p.ifw, 16)[..., c_log:] = 0.0
+    dy = rng.uniform(-1, 1, p.output_elems()).astype(np.float32)
+    ref = _wgrad_ref(p, x, dy)
+    dev = torch.device("cuda:0")
+    dw = torch.full((p.filter_elems(),), float("nan"), device=dev)
+    plan = ps.WgradPlan(p, mode=mode, device=0, recipe=f"gpu=pp:{c_log}")
+    assert "pp:" in plan.recipe
+    plan.forward(torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev), dw)
+    torch.cuda.synchronize()
+    got = dw.cpu().numpy()
+    err = oracle.rel_l2(got, ref)
+    assert err <= TOL[mode], f"relL2 {err:.3e} ({plan.recipe})"
+
+
 def test_backward_weight_rejects():
     with pytest.raises(ps.ConfigRejectedError):
         ps.WgradPlan(ps.ConvPreset.parse("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10"), mode="f16x2")

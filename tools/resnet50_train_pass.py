@@ -45,7 +45,7 @@ def main():
             bwd = ps.ConvPlan(p, mode=mode, bwd_data=True) if dx is not None else None
             if bwd is not None:
                 bwd.prepack(w)
-            wg = ps.WgradPlan(p, mode=mode)
+            wg = ps.WgradPlan(p, mode=mode, c_logical=c_log)  # (the stem: tap-folded, 3 channels)
             roof = measure.roofline(p, c_log, mode, hbm, bf16)
             layers.append(dict(name=name, p=p, x=x, w=w, y=y, dy=dy, dx=dx, dw=dw, fwd=fwd, bwd=bwd, wg=wg,
                                flops=p.flops(c_log), roof_ms=roof["t_roof_s"] * 1e3, c_log=c_log))

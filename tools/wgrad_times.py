@@ -35,7 +35,7 @@ def main():
         flops = measure.flops(p)
         nbytes = 4 * (p.input_elems() + p.output_elems() + p.filter_elems())
         for mode in modes:
-            plan = ps.WgradPlan(p, mode=mode)
+            plan = ps.WgradPlan(p, mode=mode, c_logical=c_log)
             for _ in range(2):
                 plan.forward(x, dy, dw)
             ts = []
