@@ -1230,6 +1230,7 @@ namespace {
 struct WgPick {
   int swap = -1, kn = 0, cn = 0, ntap = 0, qb = 0, pb = 0, splits = 0, stages = 0, chunk = -1, tma = -1;
   int pp = 0;  // tap fold for few-channel layers: the real channel count
+  int cl = 0;  // 1: single CTAs, 2: CTA pairs (default: pairs where eligible)
 };
 WgPick parse_wgrad_recipe(const char* recipe) {
   WgPick w;
@@ -1260,6 +1261,10 @@ WgPick parse_wgrad_recipe(const char* recipe) {
     else if (k == "st") w.stages = num(v);
     else if (k == "ch") w.chunk = num(v);
     else if (k == "pp") w.pp = num(v);
+    else if (k == "cl") {
+      w.cl = num(v);
+      if (w.cl < 1 || w.cl > 2) throw ConfigError("backward-weight recipe: cl:1|2");
+    }
     else if (k == "tma") {
       w.tma = num(v);
       if (w.tma > 1) throw ConfigError("backward-weight recipe: tma:0|1");
@@ -1280,7 +1285,8 @@ std::string wgrad_recipe(const WgradParams& g) {
   return "gpu=sw:" + std::to_string(g.swap) + ",kn:" + std::to_string(g.kn) + ",cn:" + std::to_string(g.cn) +
          ",nt:" + std::to_string(g.ntap) + ",box:" + std::to_string(g.Qb) + "x" + std::to_string(g.Pb) +
          ",sp:" + std::to_string(g.splits) + ",st:" + std::to_string(g.stages) + ",ch:" + std::to_string(g.chunk_k8) +
-         ",tma:" + std::to_string(g.tma) + (g.fc ? ",pp:" + std::to_string(g.fc) : std::string());
+         ",tma:" + std::to_string(g.tma) + (g.fc ? ",pp:" + std::to_string(g.fc) : std::string()) +
+         (g.pair ? ",cl:2" : "");
 }
 
 constexpr int kWgSmemBudget = 227 * 1024 - 6144;  // ring; the rest: alignment, barriers, row/tap tables
@@ -1425,6 +1431,20 @@ WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgP
     g.tma = (fits && t_tma < t_cp) ? 1 : 0;
   }
   if (want.pp) g.tma = 1;  // the tap fold's relayout is the TMA input
+  // CTA pairs (cta_group::2, M = 256): two 128-channel output tiles share the pixel range and
+  // each CTA stages half of the input channels -- per SM 8 KB of operands per K=8 step instead
+  // of 12 at bn = 256, the bytes the TMA path is bound by (L2 -> SM and shared memory)
+  const bool pair_ok = g.tma && g.swap == 0 && g.ntap == 1 && g.kn == 128 && K % 256 == 0 && g.cn >= 64 &&
+                       g.tiles % 2 == 0;
+  if (want.cl == 2 && !pair_ok)
+    throw ConfigError("backward-weight recipe: cl:2 needs tma:1, sw:0, nt:1, kn:128, K % 256 == 0, cn >= 64");
+  g.pair = (want.cl == 2 || (want.cl == 0 && pair_ok)) ? 1 : 0;
+  if (g.pair) {
+    g.x_bytes = g.cn / 2 * g.rows * 4;
+    g.stage_bytes = (g.x_bytes + g.y_bytes) * mult;
+    if (!want.stages) g.stages = std::min(kWgMaxStages, kWgSmemBudget / g.stage_bytes);
+    if (g.stages * g.stage_bytes > kWgSmemBudget) throw ConfigError("backward weight: the stage ring does not fit");
+  }
   if (g.tma && (g.Qb * g.sw > 256 || g.Pb * g.sh > 256))
     throw ConfigError("backward weight: tma:1 needs Qb*stride_w and Pb*stride_h <= 256");
   return g;
@@ -1463,27 +1483,44 @@ WgradParams wgrad_geom(const conv_desc& f, int mode, int num_sms, const char* re
   return g;
 }
 
-template <int BN, bool SPLIT3, bool TMA>
+template <int BN, bool SPLIT3, bool TMA, bool PAIR = false>
 void launch_wgrad_kernel(const conv_plan* P, const WgradParams& g, const CUtensorMap* tm, cudaStream_t st) {
-  using Cfg = WgCfg<BN, SPLIT3, TMA>;
+  using Cfg = WgCfg<BN, SPLIT3, TMA, PAIR>;
   const int smem = g.stages * g.stage_bytes + 6144;
   static SmemAttr attr_once;  // the largest ring any plan may use (set once per device)
-  CUDA_OK(attr_once.ensure(wgrad_sm100<BN, SPLIT3, TMA>, kWgSmemBudget + 6144, P->device));
+  CUDA_OK(attr_once.ensure(wgrad_sm100<BN, SPLIT3, TMA, PAIR>, kWgSmemBudget + 6144, P->device));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::min(g.units, P->num_sms));
+  int grid = std::min(g.units, P->num_sms);
+  if (PAIR) grid &= ~1;
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (!std::getenv("PSCONV_NO_PDL")) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (PAIR) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = std::getenv("PSCONV_NO_PDL") ? 0 : 1;
-  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_sm100<BN, SPLIT3, TMA>, g, tm[0], tm[1], tm[2], tm[3]));
+  cfg.numAttrs = na;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, wgrad_sm100<BN, SPLIT3, TMA, PAIR>, g, tm[0], tm[1], tm[2], tm[3]));
 }
 
 template <int BN, bool SPLIT3>
 void launch_wgrad_bn(const conv_plan* P, const WgradParams& g, const CUtensorMap* tm, cudaStream_t st) {
+  if (g.pair) {
+    if constexpr (BN >= 64) return launch_wgrad_kernel<BN, SPLIT3, true, true>(P, g, tm, st);
+    throw RuntimeError("internal: wgrad pair bn");
+  }
   if (g.tma)
     launch_wgrad_kernel<BN, SPLIT3, true>(P, g, tm, st);
   else
@@ -1547,7 +1584,8 @@ void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw
     {  // X32 [N][Cb2][H][W][32]: box {32, Qb*sw, Pb*sh, cn/32, 1}
       const cuuint64_t dims[5] = {32, cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.Cb2), cuuint64_t(g.N)};
       const cuuint64_t strides[4] = {128, cuuint64_t(g.W) * 128, cuuint64_t(HW) * 128, cuuint64_t(g.Cb2) * HW * 128};
-      const cuuint32_t box[5] = {32, cuuint32_t(g.Qb * g.sw), cuuint32_t(g.Pb * g.sh), cuuint32_t(g.cn / 32), 1};
+      const cuuint32_t box[5] = {32, cuuint32_t(g.Qb * g.sw), cuuint32_t(g.Pb * g.sh),
+                                 cuuint32_t(g.cn / (g.pair ? 64 : 32)), 1};  // (pair: this CTA's half)
       encode(&tm[0], P->wg_x32, 5, dims, strides, box, ex, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
              g.sw > 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
       tm[1] = tm[0];

@@ -63,6 +63,10 @@ struct WgradParams {
   int chunk_k8;                     // 3xTF32: K=8 steps per accumulation chunk (0: whole unit)
   int debug;                        // profiling (PSCONV_DEBUG): 1 skip copies, 2 skip MMAs
   int tma;                          // 1: TMA path over the relaid X / dY (else cp.async gather)
+  int pair;                         // TMA path, sw 0, one tap: CTA pairs (cta_group::2, M = 256): the
+                                    // two CTAs hold the output channels 2kp*128.. / (2kp+1)*128.. and
+                                    // one half each of the input channels (cn / 2); tile index
+                                    // ((kp * tiles_t + tt) * tiles_c + ct) * 2 + (kt & 1)
   // tap fold (recipe pp:C, few-channel layers such as the ResNet stem): the kernel runs the
   // 1x1 wgrad of X' = the layer's (tap, channel) window per output pixel (fc real channels per
   // tap, R*S*fc folded channels padded to 32) against dY; o* is the original layer
@@ -80,10 +84,10 @@ __device__ __forceinline__ uint64_t smem_desc_mn32(uint32_t saddr, uint32_t lbo,
   return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (1ull << 61);
 }
-template <int BN>
+template <int BN, int M = 128>
 __host__ __device__ constexpr uint32_t idesc_tf32_mn() {
   return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
-         (static_cast<uint32_t>(128 >> 4) << 24);
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 // 16-byte global -> shared copy; src_bytes = 0 zero-fills the destination
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
@@ -96,13 +100,28 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 }  // namespace ptx
 
-template <int BN, bool SPLIT3, bool TMA = false>
+template <int BN, bool SPLIT3, bool TMA = false, bool PAIR = false>
 struct WgCfg {
   // 4 epilogue + 1 MMA + producer warps (the TMA path: one producer warp)
   static constexpr int kThreads = 32 * (5 + (TMA ? 1 : kWgProdWarps));
   static constexpr int kAccCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   static constexpr uint32_t kTmemCols = 2 * kAccCols;  // two accumulators (power of 2, >= 64)
 };
+
+__device__ __forceinline__ void wg_tile_coords(const WgradParams& p, int tile, int& kt, int& tt, int& ct) {
+  int rest = tile, bit = 0;
+  if (p.pair) {
+    bit = tile & 1;
+    rest = tile >> 1;
+  }
+  ct = rest % p.tiles_c;
+  tt = (rest / p.tiles_c) % p.tiles_t;
+  kt = rest / (p.tiles_c * p.tiles_t);
+  if (p.pair) kt = 2 * kt + bit;
+}
+__host__ __device__ __forceinline__ int wg_tile_index(const WgradParams& p, int kt, int tt, int ct) {
+  return p.pair ? (((kt >> 1) * p.tiles_t + tt) * p.tiles_c + ct) * 2 + (kt & 1) : (kt * p.tiles_t + tt) * p.tiles_c + ct;
+}
 
 __device__ __forceinline__ void wg_stage_coords(const WgradParams& p, int g, int& n, int& p0, int& q0) {
   const int per_img = p.tiles_p * p.tiles_q;
@@ -216,14 +235,22 @@ struct WgProducer {
 // channels are 128 contiguous bytes -- a TMA box with a 128-B inner dimension lands dense in the
 // SWIZZLE_128B_ATOM_32B layout, one box per tap (X) / per stage (dY), multicast-free, ~2x the
 // L2->SM rate of the cp.async gather.
-template <int BN, bool SPLIT3, bool TMA = false>
-__global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
+template <int BN, bool SPLIT3, bool TMA = false, bool PAIR = false>
+__global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA, PAIR>::kThreads, 1)
     wgrad_sm100(const __grid_constant__ WgradParams p, const __grid_constant__ CUtensorMap tm_x,
                 const __grid_constant__ CUtensorMap tm_xlo, const __grid_constant__ CUtensorMap tm_y,
                 const __grid_constant__ CUtensorMap tm_ylo) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using Cfg = WgCfg<BN, SPLIT3, TMA>;
-  constexpr uint32_t kIdesc = ptx::idesc_tf32_mn<BN>();
+  using Cfg = WgCfg<BN, SPLIT3, TMA, PAIR>;
+  static_assert(!PAIR || TMA, "CTA pairs run on the TMA path");
+  constexpr uint32_t kIdesc = ptx::idesc_tf32_mn<BN, PAIR ? 256 : 128>();
+  constexpr int CS = PAIR ? 2 : 1;
+  const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
+  const bool leader = rank == 0;
+  // PAIR: the cluster takes CTA-level units 2 uc and 2 uc + 1 (the two output-channel halves
+  // of one pair tile, same pixel range)
+  const int ustart = PAIR ? static_cast<int>(blockIdx.x >> 1) * 2 + rank : static_cast<int>(blockIdx.x);
+  const int ustep = static_cast<int>(gridDim.x);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int kStages = p.stages;
@@ -254,13 +281,19 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
-      ptx::mbar_init(&acc_empty[a], 4);
+      ptx::mbar_init(&acc_empty[a], 4 * CS);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 4) {
+    if (PAIR)
+      ptx::tmem_alloc_pair(tmem_slot, Cfg::kTmemCols);
+    else
+      ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   ptx::griddep_launch_dependents();
@@ -279,33 +312,50 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
     }
     ptx::griddep_wait();
     __syncwarp();
-    const uint32_t tx = static_cast<uint32_t>(p.x_bytes + p.y_bytes) * (SPLIT3 ? 2u : 1u);
+    const uint32_t tx = static_cast<uint32_t>(p.x_bytes + p.y_bytes) * (SPLIT3 ? 2u : 1u) * CS;
     const uint32_t lo = static_cast<uint32_t>(p.x_bytes + p.y_bytes);
-    const uint32_t tap_bytes = static_cast<uint32_t>(p.cn) * p.rows * 4;
+    const uint32_t tap_bytes = static_cast<uint32_t>(p.cn / CS) * p.rows * 4;
+    // PAIR: both CTAs' boxes complete on the LEADER's full barrier (it expects both shares)
+    const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / p.tiles, tile = u - split * p.tiles;
-      const int ct = tile % p.tiles_c, tt = (tile / p.tiles_c) % p.tiles_t, kt = tile / (p.tiles_c * p.tiles_t);
+    for (int u = ustart; u < p.units; u += ustep) {
+      const int split = u / p.tiles;
+      int kt, tt, ct;
+      wg_tile_coords(p, u - split * p.tiles, kt, tt, ct);
       const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
+      const int xcb = ct * (p.cn / 32) + rank * (p.cn / 64);  // this CTA's input-channel groups
       for (int g = g0; g < g1; ++g) {
         int n, p0, q0;
         wg_stage_coords(p, g, n, p0, q0);
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        if (ptx::elect_one()) {
+        if (p.debug & 1) {  // profiling: no loads, the stage is "full" at once
+          if (leader && ptx::elect_one()) ptx::mbar_arrive(&full[stage]);
+        } else if (ptx::elect_one()) {
           uint8_t* sb = smem + stage * p.stage_bytes;
-          ptx::mbar_expect_tx(&full[stage], tx);
+          if (leader) ptx::mbar_expect_tx(&full[stage], tx);
+          const uint32_t fb = full_leader + 8u * stage;
           for (int t = 0; t < p.ntap; ++t) {
             // taps past R*S (a partial last tap group) load the last tap again; the reduce
             // kernel never reads those accumulator rows / columns
             const int tap = min(tt * p.ntap + t, p.R * p.S - 1);
             const int r = tap / p.S, sx = tap - r * p.S;
             const int wq = q0 * p.sw + sx - p.pw, hp = p0 * p.sh + r - p.ph;
-            ptx::tma_load_5d(sb + t * tap_bytes, &tm_x, &full[stage], 0, wq, hp, ct * (p.cn / 32), n);
-            if (SPLIT3) ptx::tma_load_5d(sb + lo + t * tap_bytes, &tm_xlo, &full[stage], 0, wq, hp, ct * (p.cn / 32), n);
+            if (PAIR) {
+              ptx::tma_load_5d_cb(sb + t * tap_bytes, &tm_x, fb, 0, wq, hp, xcb, n);
+              if (SPLIT3) ptx::tma_load_5d_cb(sb + lo + t * tap_bytes, &tm_xlo, fb, 0, wq, hp, xcb, n);
+            } else {
+              ptx::tma_load_5d(sb + t * tap_bytes, &tm_x, &full[stage], 0, wq, hp, xcb, n);
+              if (SPLIT3) ptx::tma_load_5d(sb + lo + t * tap_bytes, &tm_xlo, &full[stage], 0, wq, hp, xcb, n);
+            }
           }
-          ptx::tma_load_5d(sb + p.x_bytes, &tm_y, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
-          if (SPLIT3) ptx::tma_load_5d(sb + lo + p.x_bytes, &tm_ylo, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
+          if (PAIR) {
+            ptx::tma_load_5d_cb(sb + p.x_bytes, &tm_y, fb, 0, q0, p0, kt * (p.kn / 32), n);
+            if (SPLIT3) ptx::tma_load_5d_cb(sb + lo + p.x_bytes, &tm_ylo, fb, 0, q0, p0, kt * (p.kn / 32), n);
+          } else {
+            ptx::tma_load_5d(sb + p.x_bytes, &tm_y, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
+            if (SPLIT3) ptx::tma_load_5d(sb + lo + p.x_bytes, &tm_ylo, &full[stage], 0, q0, p0, kt * (p.kn / 32), n);
+          }
         }
         __syncwarp();
         if (++stage == kStages) {
@@ -331,9 +381,10 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
       ptx::mbar_arrive(&full[sig_stage]);
       if (++sig_stage == kStages) sig_stage = 0;
     };
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / p.tiles, tile = u - split * p.tiles;
-      const int ct = tile % p.tiles_c, tt = (tile / p.tiles_c) % p.tiles_t, kt = tile / (p.tiles_c * p.tiles_t);
+    for (int u = ustart; u < p.units; u += ustep) {
+      const int split = u / p.tiles;
+      int kt, tt, ct;
+      wg_tile_coords(p, u - split * p.tiles, kt, tt, ct);
       const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
       if (tt != tt_cur) {  // the unit's taps (double-buffered: the other warps may still read)
         tt_cur = tt;
@@ -377,8 +428,9 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
     }
     ptx::cp_async_wait<0>();
     while (pending-- > 0) signal_oldest();
-  } else if (warp == 4) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 4 && leader) {
+    // ------------------------------------------------------------ MMA issuer (PAIR: the leader
+    // issues M = 256 MMAs over both CTAs' A rows and B halves)
     const uint32_t lbo = static_cast<uint32_t>(p.rows) * 128u;
     const uint32_t s0 = ptx::smem_u32(smem);
     const uint32_t a_off = p.swap ? 0u : static_cast<uint32_t>(p.x_bytes);
@@ -386,13 +438,16 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
     const uint32_t lo_off = static_cast<uint32_t>(p.x_bytes + p.y_bytes);
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int u = ustart; u < p.units; u += ustep) {
       const int split = u / p.tiles;
       const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
       int in_chunk = 0;
       for (int g = g0; g < g1; ++g) {
-        if (in_chunk == 0) {  // a fresh accumulator (chunk) begins
-          ptx::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        if (in_chunk == 0) {  // a fresh accumulator (chunk) begins (PAIR: both CTAs drained it)
+          if (PAIR)
+            ptx::mbar_wait_cluster(&acc_empty[acc], acc_phase ^ 1);
+          else
+            ptx::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
           ptx::tc_fence_after();
         }
         ptx::mbar_wait(&full[stage], phase);
@@ -406,14 +461,27 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
           for (int j = 0; j < nk8; ++j) {
             const uint32_t a = base + a_off + j * 1024u, b = base + b_off + j * 1024u;
             const uint64_t ad = ptx::smem_desc_mn32(a, lbo, 512), bd = ptx::smem_desc_mn32(b, lbo, 512);
-            ptx::mma_tf32(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
-            if (SPLIT3) {
-              ptx::mma_tf32(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
-              ptx::mma_tf32(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+            if (PAIR) {
+              ptx::mma_tf32_pair(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
+              if (SPLIT3) {
+                ptx::mma_tf32_pair(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
+                ptx::mma_tf32_pair(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+              }
+            } else {
+              ptx::mma_tf32(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
+              if (SPLIT3) {
+                ptx::mma_tf32(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
+                ptx::mma_tf32(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+              }
             }
           }
-          ptx::mma_commit(&empty[stage]);
-          if (last) ptx::mma_commit(&acc_full[acc]);
+          if (PAIR) {
+            ptx::mma_commit_pair(&empty[stage]);
+            if (last) ptx::mma_commit_pair(&acc_full[acc]);
+          } else {
+            ptx::mma_commit(&empty[stage]);
+            if (last) ptx::mma_commit(&acc_full[acc]);
+          }
         }
         __syncwarp();
         if (last) {
@@ -429,13 +497,26 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 4) {
     // ------------------------------------------------------------ epilogue (warps 0-3)
     const int row = warp * 32 + (threadIdx.x & 31);
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    // accumulator drained: PAIR's second CTA arrives on the leader's barrier
+    const uint32_t acc_empty_leader = PAIR ? ptx::mapa(&acc_empty[0], 0) : 0u;
+    auto release = [&](int a) {
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (ptx::elect_one()) {  // one arrival per warp
+        if (PAIR && !leader)
+          ptx::mbar_arrive_remote(acc_empty_leader + 8u * a);
+        else
+          ptx::mbar_arrive(&acc_empty[a]);
+      }
+      __syncwarp();
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int u = ustart; u < p.units; u += ustep) {
       const int split = u / p.tiles;
       const int g0 = split * per_split, g1 = min(p.nstage, g0 + per_split);
       float* dst = p.ws + (static_cast<int64_t>(u) * 128 + row) * p.bn;
@@ -456,10 +537,7 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) sum[c0 + i] += __uint_as_float(v[i]);
           }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (ptx::elect_one()) ptx::mbar_arrive(&acc_empty[acc]);  // one arrival per warp
-          __syncwarp();
+          release(acc);
           if (++acc == 2) {
             acc = 0;
             acc_phase ^= 1;
@@ -483,10 +561,7 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
                 make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
                             __uint_as_float(v[i + 3]));
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (ptx::elect_one()) ptx::mbar_arrive(&acc_empty[acc]);
-        __syncwarp();
+        release(acc);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -496,9 +571,13 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA>::kThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync_all();  // no CTA leaves while the pair still uses it
   if (warp == 4) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    if (PAIR)
+      ptx::tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+    else
+      ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 #endif
 }
@@ -645,7 +724,7 @@ __global__ void wgrad_reduce_kernel(const __grid_constant__ WgradParams p, float
     }
     const int tt = tap / p.ntap, tl = tap - tt * p.ntap, ct = c / p.cn, cl = c - ct * p.cn;
     const int kt = k / p.kn, kl = k - kt * p.kn;
-    const int tile = (kt * p.tiles_t + tt) * p.tiles_c + ct;
+    const int tile = wg_tile_index(p, kt, tt, ct);
     const int xi = tl * p.cn + cl;  // X-side index within the tile (taps x channels)
     const int64_t off = p.swap ? int64_t(xi) * p.bn + kl : int64_t(kl) * p.bn + xi;
     const float* src = p.ws + int64_t(tile) * tile_elems + off;

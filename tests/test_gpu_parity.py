@@ -714,6 +714,10 @@ WGRAD = [
     ("conv:8,128,64,10,10,3,3,1,1,16,1,1,10,10", "gpu=sw:0,kn:128,cn:64,nt:2,box:10x4,sp:5"),
     ("conv:8,64,64,10,10,3,3,1,1,16,1,1,10,10", "gpu=sw:1,kn:64,cn:64,nt:2,box:8x1,sp:3,st:3,ch:8"),
     ("conv:8,256,128,8,8,3,3,1,1,16,1,1,8,8", "gpu=sw:0,kn:128,cn:128,nt:1,box:8x2"),
+    # CTA pairs (cta_group::2): two 128-channel output tiles, each CTA half of the input channels
+    ("conv:6,512,256,7,7,3,3,1,1,16,1,1,7,7", "gpu=cl:2,sp:3"),
+    ("conv:5,256,96,9,9,1,1,1,1,16,0,0,9,9", "gpu=cl:2,sw:0,kn:128,cn:64,tma:1"),   # C = 96: partial last pair
+    ("conv:4,256,128,7,7,3,3,2,2,16,1,1,14,14", "gpu=cl:1,tma:1"),
 ]
 
 
