@@ -1615,9 +1615,9 @@ void launch_wgrad(const conv_plan* P, const float* x, const float* dy, float* dw
     default: throw RuntimeError("internal: wgrad bn");
   }
 #undef PSCONV_WG
-  const int64_t n = g.fc ? int64_t(g.Kb) * 16 * g.oCb * 16 * g.oR * g.oS : int64_t(g.Kb) * 16 * g.Cb * 16 * g.R * g.S;
+  const int64_t nblk = g.fc ? int64_t(g.Kb) * g.oCb * g.oR * g.oS : int64_t(g.Kb) * g.Cb * g.R * g.S;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid_for(n));
+  cfg.gridDim = dim3(int(std::min<int64_t>(nblk, 148 * 16)));
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

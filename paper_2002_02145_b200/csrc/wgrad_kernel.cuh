@@ -695,42 +695,57 @@ __global__ void __launch_bounds__(kFoldQ) wgrad_fold_kernel(const __grid_constan
   }
 }
 
-// dW (KCRS16c16k) = the split partials of every tile added in split order.
-__global__ void wgrad_reduce_kernel(const __grid_constant__ WgradParams p, float* __restrict__ dw) {
+// dW (KCRS16c16k) = the split partials of every tile added in split order. One 256-thread
+// block per 16 x 16 (k, c) block of one tap: it reads the partials along their contiguous
+// dimension (64-B segments) and writes the block's 1 KB of dW contiguously (through a shared
+// transpose when the partial rows are output channels).
+__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const __grid_constant__ WgradParams p, float* __restrict__ dw) {
+  __shared__ float tr[16][17];
   ptx::griddep_wait();
   // (tap fold: dW of the original layer; its channel c of tap t is folded channel t * fc + c)
   const int oCb = p.fc ? p.oCb : p.Cb, RS = p.fc ? p.oR * p.oS : p.R * p.S;
-  const int64_t n_el = int64_t(p.Kb) * 16 * oCb * 16 * RS;
+  const int64_t nblk = int64_t(p.Kb) * oCb * RS;
   const int64_t tile_elems = int64_t(128) * p.bn;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_el; e += int64_t(gridDim.x) * blockDim.x) {
-    int64_t t = e;
-    const int k16 = int(t & 15);
-    t >>= 4;
-    const int c16 = int(t & 15);
-    t >>= 4;
-    int tap = int(t % RS);
-    t /= RS;
-    const int cb = int(t % oCb);
-    const int kb = int(t / oCb);
+  const int t = threadIdx.x;
+  // read roles: swap 0 -> rows are k (contiguous c): (k16, c16) = (t / 16, t % 16);
+  //             swap 1 -> rows are c (contiguous k): (c16, k16) = (t / 16, t % 16)
+  const int k16 = p.swap ? (t & 15) : (t >> 4), c16 = p.swap ? (t >> 4) : (t & 15);
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    int64_t r = b;
+    const int tap0 = int(r % RS);
+    r /= RS;
+    const int cb = int(r % oCb);
+    const int kb = int(r / oCb);
     const int k = kb * 16 + k16;
-    int c = cb * 16 + c16;
+    int c = cb * 16 + c16, tap = tap0;
+    float s = 0.f;
+    bool zero = false;
     if (p.fc) {
       if (c >= p.fc) {  // padded channels of the few-channel layer
-        dw[e] = 0.f;
-        continue;
+        zero = true;
+      } else {
+        c = tap * p.fc + c;
+        tap = 0;
       }
-      c = tap * p.fc + c;
-      tap = 0;
     }
-    const int tt = tap / p.ntap, tl = tap - tt * p.ntap, ct = c / p.cn, cl = c - ct * p.cn;
-    const int kt = k / p.kn, kl = k - kt * p.kn;
-    const int tile = wg_tile_index(p, kt, tt, ct);
-    const int xi = tl * p.cn + cl;  // X-side index within the tile (taps x channels)
-    const int64_t off = p.swap ? int64_t(xi) * p.bn + kl : int64_t(kl) * p.bn + xi;
-    const float* src = p.ws + int64_t(tile) * tile_elems + off;
-    float s = 0.f;
-    for (int sp = 0; sp < p.splits; ++sp) s += src[int64_t(sp) * p.tiles * tile_elems];
-    dw[e] = s;
+    if (!zero) {
+      const int tt = tap / p.ntap, tl = tap - tt * p.ntap, ct = c / p.cn, cl = c - ct * p.cn;
+      const int kt = k / p.kn, kl = k - kt * p.kn;
+      const int tile = wg_tile_index(p, kt, tt, ct);
+      const int xi = tl * p.cn + cl;  // X-side index within the tile (taps x channels)
+      const int64_t off = p.swap ? int64_t(xi) * p.bn + kl : int64_t(kl) * p.bn + xi;
+      const float* src = p.ws + int64_t(tile) * tile_elems + off;
+      for (int sp = 0; sp < p.splits; ++sp) s += src[int64_t(sp) * p.tiles * tile_elems];
+    }
+    float* blk = dw + b * 256;  // [16c][16k] of (kb, cb, tap0)
+    if (p.swap) {
+      blk[t] = s;  // t = c16 * 16 + k16: the block's own order
+    } else {
+      __syncthreads();
+      tr[k16][c16] = s;
+      __syncthreads();
+      blk[t] = tr[t & 15][t >> 4];  // (c16, k16) = (t / 16, t % 16)
+    }
   }
 }
 
