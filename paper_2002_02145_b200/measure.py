@@ -195,11 +195,10 @@ class LayerBench:
         """Per-step (repack + conv) and conv-only event times in ms (lists); L2 flushed before
         every step. With prepack_in_step=False the step is the conv alone (prepacked filter).
 
-        Two passes of `steps` each: the step pass records events only around the whole step
-        (an event between the repack and the conv launch would serialise them: the conv's
+        Per timed step two L2-flushed measurements: the step with events only around the whole
+        step (an event between the repack and the conv launch would serialise them: the conv's
         prologue overlaps the repack through PDL, so a middle event adds ~6 us to a step of a
-        small layer, tools/step_overhead.py), then the kernel pass times the conv alone on the
-        prepacked filter."""
+        small layer, tools/step_overhead.py), then the conv alone on the prepacked filter."""
         torch, st = self.torch, self.stream
 
         def one():
@@ -212,22 +211,20 @@ class LayerBench:
         for _ in range(warmup):
             one()
         torch.cuda.synchronize()
-        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(steps)]
-        for e0, e1 in ev:
+        # the two timings alternate step by step, so that both see the same clocks (power-capped
+        # parts slow down over a run: separate passes made the later one look slower)
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(steps)]
+        for e0, e1, e2, e3 in ev:
             flush()
             e0.record(st)
             one()
             e1.record(st)
-        torch.cuda.synchronize()
-        step = [a.elapsed_time(b) for a, b in ev]
-        plan.prepack(self.w, st)
-        for e0, e1 in ev:
             flush()
-            e0.record(st)
+            e2.record(st)
             plan.forward(self.x, None, self.y, self.b0, self.n, st, prepacked=True)
-            e1.record(st)
+            e3.record(st)
         torch.cuda.synchronize()
-        return step, [a.elapsed_time(b) for a, b in ev]
+        return [a.elapsed_time(b) for a, b, _, _ in ev], [c.elapsed_time(d) for _, _, c, d in ev]
 
     # -- steady state: rotating sets, back-to-back launches -------------------------------
     def _rotating_sets(self):
