@@ -1309,7 +1309,9 @@ WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgP
         const int rows = q * pp;
         if (rows % 8 || rows > rows_max || rows > 256) continue;
         const double waste = double(cdiv(Q, q) * q * cdiv(P, pp) * pp) / (double(P) * Q);
-        const double score = waste * (1.0 + 2.0 / rows);  // per-stage fixed cost ~ 2 rows
+        // per-stage fixed cost (barrier round trip, box issue) ~ 24 rows of N = 256 MMA time:
+        // l3 3x3 TF32 dW 165 -> 142 us going from 32- to 56-row stages, 16-row stages 263 us
+        const double score = waste * (1.0 + 24.0 / rows);
         if (score < best - 1e-12) {
           best = score;
           qb = q;
@@ -1376,35 +1378,49 @@ WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgP
   g.tiles_c = int(cdiv(C, g.cn));
   g.tiles_t = int(cdiv(RS, g.ntap));
   g.tiles = g.tiles_k * g.tiles_c * g.tiles_t;
-  const int row_bytes = (g.ntap * g.cn + g.kn) * 4 * mult;
-  if (want.qb) {
-    g.Qb = want.qb;
-    g.Pb = want.pb;
-    if ((g.Qb * g.Pb) % 8 || g.Qb * g.Pb > 256 || g.Qb < 1 || g.Pb < 1)
-      throw ConfigError("backward-weight recipe: box rows (QxP) must be a multiple of 8, at most 256");
-  } else {
-    pick_box(row_bytes, split3 ? 3 : 4, g.Qb, g.Pb);
-  }
-  g.rows = g.Qb * g.Pb;
-  g.tiles_q = int(cdiv(Q, g.Qb));
-  g.tiles_p = int(cdiv(P, g.Pb));
-  const int64_t nstage = int64_t(g.N) * g.tiles_p * g.tiles_q;
-  if (nstage >= (int64_t(1) << 31)) throw ConfigError("backward weight: too many pixel stages");
-  g.nstage = int(nstage);
-  g.x_bytes = g.ntap * g.cn * g.rows * 4;
-  g.y_bytes = g.kn * g.rows * 4;
-  g.stage_bytes = (g.x_bytes + g.y_bytes) * mult;
-  g.stages = want.stages ? want.stages : std::min(kWgMaxStages, kWgSmemBudget / g.stage_bytes);
-  if (g.stages < 2 || g.stages > kWgMaxStages || g.stages * g.stage_bytes > kWgSmemBudget)
-    throw ConfigError("backward weight: the stage ring does not fit shared memory");
-  // one unit per SM: split the pixel stages so that splits x tiles ~ the SM count (at least
-  // 2 stages per unit); more units than SMs only when the tiles alone exceed them
-  int splits = want.splits;
-  if (!splits) splits = int(std::max<int64_t>(1, std::min<int64_t>(num_sms / g.tiles, nstage / 2)));
-  splits = int(std::min<int64_t>(splits, nstage));
-  g.stage_per_split = int(cdiv(nstage, splits));
-  g.splits = int(cdiv(nstage, g.stage_per_split));
-  g.units = g.splits * g.tiles;
+  // CTA pairs (cta_group::2, M = 256): two 128-channel output tiles share the pixel range and
+  // each CTA stages half of the input channels -- per SM 8 KB of operands per K=8 step instead
+  // of 12 at bn = 256. TMA path only; chosen unless the recipe says cl:1 or tma:0.
+  // A refinement of the TMA path, decided after it (below); the box is picked for the
+  // single-CTA stage and the pair then gets a deeper ring.
+  const bool pair_cand = g.swap == 0 && g.ntap == 1 && g.kn == 128 && K % 256 == 0 && g.cn >= 64 && !want.pp;
+  if (want.cl == 2 && (!pair_cand || want.tma == 0))
+    throw ConfigError("backward-weight recipe: cl:2 needs tma:1, sw:0, nt:1, kn:128, K % 256 == 0, cn >= 64");
+  // The pixel box / ring are sized for the CTA's staging footprint: a pair candidate is sized
+  // for the pair (half the input channels per CTA: deeper stages, fewer barrier round trips --
+  // l4 3x3 TF32 dW 177 -> 130 us at 56 instead of 32 rows); if the gather wins instead, the box
+  // is re-picked for the single-CTA footprint.
+  const bool pair_try = pair_cand && want.tma != 0 && want.cl != 1;
+  auto layout = [&](int xch) {
+    const int row_bytes = (xch + g.kn) * 4 * mult;
+    if (want.qb) {
+      g.Qb = want.qb;
+      g.Pb = want.pb;
+      if ((g.Qb * g.Pb) % 8 || g.Qb * g.Pb > 256 || g.Qb < 1 || g.Pb < 1)
+        throw ConfigError("backward-weight recipe: box rows (QxP) must be a multiple of 8, at most 256");
+    } else {
+      pick_box(row_bytes, 3, g.Qb, g.Pb);
+    }
+    g.rows = g.Qb * g.Pb;
+    g.tiles_q = int(cdiv(Q, g.Qb));
+    g.tiles_p = int(cdiv(P, g.Pb));
+    const int64_t nstage = int64_t(g.N) * g.tiles_p * g.tiles_q;
+    if (nstage >= (int64_t(1) << 31)) throw ConfigError("backward weight: too many pixel stages");
+    g.nstage = int(nstage);
+    g.x_bytes = xch * g.rows * 4;
+    g.y_bytes = g.kn * g.rows * 4;
+    g.stage_bytes = (g.x_bytes + g.y_bytes) * mult;
+    g.stages = want.stages ? want.stages : std::min(kWgMaxStages, kWgSmemBudget / g.stage_bytes);
+    // one unit per SM: split the pixel stages so that splits x tiles ~ the SM count (at least
+    // 2 stages per unit); more units than SMs only when the tiles alone exceed them
+    int splits = want.splits;
+    if (!splits) splits = int(std::max<int64_t>(1, std::min<int64_t>(num_sms / g.tiles, nstage / 2)));
+    splits = int(std::min<int64_t>(splits, nstage));
+    g.stage_per_split = int(cdiv(nstage, splits));
+    g.splits = int(cdiv(nstage, g.stage_per_split));
+    g.units = g.splits * g.tiles;
+  };
+  layout(pair_try ? g.cn / 2 : g.ntap * g.cn);
   // 3xTF32 accumulation chunks (~32 K=8 steps: error ~6e-8 per step)
   g.chunk_k8 = split3 ? (want.chunk >= 0 ? want.chunk : 32) : 0;
   if (split3 && g.chunk_k8 > 0 && g.chunk_k8 < g.rows / 8) g.chunk_k8 = g.rows / 8;
@@ -1418,9 +1434,11 @@ WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgP
   const bool fits = g.Qb * g.sw <= 256 && g.Pb * g.sh <= 256;
   if (want.tma >= 0) {
     g.tma = want.tma;
+  } else if (want.cl == 2) {
+    g.tma = 1;
   } else {
     const double xb = 4.0 * f.nImg * Cb * 16 * f.ifh * f.ifw, yb = 4.0 * f.nImg * Kb * 16 * P * Q;
-    const double l2 = double(g.units) * g.stage_per_split * (g.x_bytes + g.y_bytes);  // hi bytes
+    const double l2 = double(g.units) * g.stage_per_split * (g.ntap * g.cn + g.kn) * g.rows * 4.0;  // hi bytes
     const double k8 = double(g.units) * g.stage_per_split * (g.rows / 8);
     const double mma_cyc = std::max(g.bn / 2.0, g.bn <= 64 ? 45.0 : 0.0) * (split3 ? 3 : 1);
     const double t_mma = k8 * mma_cyc / num_sms / 1.8e9;
@@ -1431,20 +1449,10 @@ WgradParams wgrad_geom_core(const conv_desc& f, int mode, int num_sms, const WgP
     g.tma = (fits && t_tma < t_cp) ? 1 : 0;
   }
   if (want.pp) g.tma = 1;  // the tap fold's relayout is the TMA input
-  // CTA pairs (cta_group::2, M = 256): two 128-channel output tiles share the pixel range and
-  // each CTA stages half of the input channels -- per SM 8 KB of operands per K=8 step instead
-  // of 12 at bn = 256, the bytes the TMA path is bound by (L2 -> SM and shared memory)
-  const bool pair_ok = g.tma && g.swap == 0 && g.ntap == 1 && g.kn == 128 && K % 256 == 0 && g.cn >= 64 &&
-                       g.tiles % 2 == 0;
-  if (want.cl == 2 && !pair_ok)
-    throw ConfigError("backward-weight recipe: cl:2 needs tma:1, sw:0, nt:1, kn:128, K % 256 == 0, cn >= 64");
-  g.pair = (want.cl == 2 || (want.cl == 0 && pair_ok)) ? 1 : 0;
-  if (g.pair) {
-    g.x_bytes = g.cn / 2 * g.rows * 4;
-    g.stage_bytes = (g.x_bytes + g.y_bytes) * mult;
-    if (!want.stages) g.stages = std::min(kWgMaxStages, kWgSmemBudget / g.stage_bytes);
-    if (g.stages * g.stage_bytes > kWgSmemBudget) throw ConfigError("backward weight: the stage ring does not fit");
-  }
+  g.pair = (pair_try && g.tma) ? 1 : 0;
+  if (pair_try && !g.pair) layout(g.ntap * g.cn);  // the gather won: single-CTA footprint
+  if (g.stages < 2 || g.stages > kWgMaxStages || g.stages * g.stage_bytes > kWgSmemBudget)
+    throw ConfigError("backward weight: the stage ring does not fit shared memory");
   if (g.tma && (g.Qb * g.sw > 256 || g.Pb * g.sh > 256))
     throw ConfigError("backward weight: tma:1 needs Qb*stride_w and Pb*stride_h <= 256");
   return g;
