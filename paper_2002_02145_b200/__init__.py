@@ -210,6 +210,36 @@ class WgradPlan:
             pass
 
 
+def _cached_bwd_data_recipe(preset: "ConvPreset", mode: int) -> str | None:
+    """Backward data of a stride-1 layer is the forward conv of its transposed descriptor
+    (channels swapped, padding k - 1 - pad), which is often another layer's forward shape (the
+    ResNet 3x3s, the 1x1 pairs 64->256 / 256->64 ...): reuse that shape's measured recipe from
+    the committed plan cache. Strided layers run per-phase child plans (selector choice)."""
+    if preset.stride_h != 1 or preset.stride_w != 1:
+        return None
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "plans_b200.json")
+    try:
+        with open(path) as fh:
+            cache = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    p = preset
+    t = ConvPreset(nImg=p.nImg, nOfm=p.nIfm, nIfm=p.nOfm, ofh=p.ifh, ofw=p.ifw, kh=p.kh, kw=p.kw, stride_h=1,
+                   stride_w=1, gemm_block=p.gemm_block, pad_h=p.kh - 1 - p.pad_h, pad_w=p.kw - 1 - p.pad_w,
+                   ifh=p.ofh, ifw=p.ofw)
+    try:
+        t.validate()
+    except Error:
+        return None
+    name = {v: k for k, v in _MODES.items()}.get(mode, mode)
+    e = cache.get(f"{t}|{name}")
+    if not e or "pp:" in e["recipe"] or "fold:" in e["recipe"]:
+        return None
+    return e["recipe"]
+
+
 class ConvPlan:
     """One conv layer bound to a device, a mode and a schedule (recipe)."""
 
@@ -224,6 +254,8 @@ class ConvPlan:
         self.mode = mode
         self.device = device
         self.bwd_data = bwd_data
+        if bwd_data and recipe is None:
+            recipe = _cached_bwd_data_recipe(self.preset, mode)
         self._d = self.preset.to_c()
         h = ctypes.c_void_p()
         create = lib.conv_plan_create_bwd_data if bwd_data else lib.conv_plan_create

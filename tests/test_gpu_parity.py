@@ -399,6 +399,31 @@ def test_backward_data_strided_paths():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_backward_data_cached_recipe(mode):
+    """A stride-1 ResNet layer's backward data reuses the plan cache's recipe of its transposed
+    (forward) shape; checked on an image range of the full N = 256 plan."""
+    conv = R50["r50_l3_3x3_256_256"][0]
+    p = ps.ConvPreset.parse(conv)
+    plan = ps.ConvPlan(p, mode=mode, device=0, bwd_data=True)
+    def items(r):
+        perm, gpu = r.split(";gpu=")
+        return perm, set(gpu.split(","))
+    assert items(plan.recipe) == items(ps._cached_bwd_data_recipe(p, ps._MODES[mode]))
+    rng = np.random.default_rng(7)
+    sub = ps.ConvPreset.parse(conv.replace("conv:256,", "conv:2,", 1))
+    dy = rng.uniform(-1, 1, sub.output_elems()).astype(np.float32)
+    w = rng.uniform(-1, 1, sub.filter_elems()).astype(np.float32)
+    dyd = torch.zeros(p.output_elems(), device="cuda:0")
+    dyd[:dy.size] = torch.from_numpy(dy).cuda()
+    dx = torch.full((p.input_elems(),), float("nan"), device="cuda:0")
+    plan.forward(dyd, torch.from_numpy(w).cuda(), dx, img_begin=0, img_count=2)
+    torch.cuda.synchronize()
+    err = oracle.rel_l2(dx[:sub.input_elems()].cpu().numpy(), _bwd_data_ref(sub, dy, w))
+    assert err <= TOL[mode], f"relL2 {err:.3e} ({plan.recipe})"
+
+
+@pytest.mark.gpu
 def test_backward_data_rejects_negative_phase_pad():
     # 2x2 / stride 2 / pad 1: phase 1's taps start one row past its first output row
     with pytest.raises(ps.ConfigRejectedError):
