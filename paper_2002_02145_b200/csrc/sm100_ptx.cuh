@@ -458,7 +458,9 @@ __host__ __device__ constexpr uint32_t idesc_f16_m128() {
 
 // Instruction descriptor: kind::tf32, D=f32, A and B K-major, M=128.
 // (Measured on B200: kind::tf32 with an MN-major SWIZZLE_64B B operand
-// silently yields zeros -- tools/probe2.cu -- so B is prepacked K-major.)
+// silently yields zeros -- tools/probe2.cu -- so B is prepacked K-major. MN-major
+// tf32 exists only in the SWIZZLE_128B_BASE32B layout (tools/probe_mn.cu), whose
+// 128-B rows are 32 channels: the backward-weight kernel's layout, wgrad_kernel.cuh.)
 template <int BN, int M = 128>
 __host__ __device__ constexpr uint32_t idesc_tf32_m128() {
   return (1u << 4)                                  // D format f32
