@@ -458,22 +458,26 @@ __global__ void __launch_bounds__(WgCfg<BN, SPLIT3, TMA, PAIR>::kThreads, 1)
           const uint32_t base = s0 + static_cast<uint32_t>(stage * p.stage_bytes);
           const uint32_t d = tmem_base + static_cast<uint32_t>(acc * Cfg::kAccCols);
           const int nk8 = (p.debug & 2) ? 0 : k8_stage;
-          for (int j = 0; j < nk8; ++j) {
-            const uint32_t a = base + a_off + j * 1024u, b = base + b_off + j * 1024u;
-            const uint64_t ad = ptx::smem_desc_mn32(a, lbo, 512), bd = ptx::smem_desc_mn32(b, lbo, 512);
+          // descriptors built once per stage; a K=8 step is +1024 B = +64 in the 16-B address
+          // field (no carry out of it: smem offsets < 256 KB)
+          uint64_t ad = ptx::smem_desc_mn32(base + a_off, lbo, 512), bd = ptx::smem_desc_mn32(base + b_off, lbo, 512);
+          const uint64_t lo16 = lo_off >> 4;
+          uint32_t accum = first ? 0u : 1u;
+          for (int j = 0; j < nk8; ++j, ad += 64, bd += 64) {
             if (PAIR) {
-              ptx::mma_tf32_pair(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
+              ptx::mma_tf32_pair(d, ad, bd, kIdesc, accum);
               if (SPLIT3) {
-                ptx::mma_tf32_pair(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
-                ptx::mma_tf32_pair(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+                ptx::mma_tf32_pair(d, ad + lo16, bd, kIdesc, 1u);
+                ptx::mma_tf32_pair(d, ad, bd + lo16, kIdesc, 1u);
               }
             } else {
-              ptx::mma_tf32(d, ad, bd, kIdesc, (first && j == 0) ? 0u : 1u);
+              ptx::mma_tf32(d, ad, bd, kIdesc, accum);
               if (SPLIT3) {
-                ptx::mma_tf32(d, ptx::smem_desc_mn32(a + lo_off, lbo, 512), bd, kIdesc, 1u);
-                ptx::mma_tf32(d, ad, ptx::smem_desc_mn32(b + lo_off, lbo, 512), kIdesc, 1u);
+                ptx::mma_tf32(d, ad + lo16, bd, kIdesc, 1u);
+                ptx::mma_tf32(d, ad, bd + lo16, kIdesc, 1u);
               }
             }
+            accum = 1u;
           }
           if (PAIR) {
             ptx::mma_commit_pair(&empty[stage]);
