@@ -195,10 +195,11 @@ class LayerBench:
         """Per-step (repack + conv) and conv-only event times in ms (lists); L2 flushed before
         every step. With prepack_in_step=False the step is the conv alone (prepacked filter).
 
-        Per timed step two L2-flushed measurements: the step with events only around the whole
-        step (an event between the repack and the conv launch would serialise them: the conv's
-        prologue overlaps the repack through PDL, so a middle event adds ~6 us to a step of a
-        small layer, tools/step_overhead.py), then the conv alone on the prepacked filter."""
+        Two passes of `steps` L2-flushed launches each: the step pass records events only around
+        the whole step (an event between the repack and the conv launch would serialise them:
+        the conv's prologue overlaps the repack through PDL, so a middle event adds ~6 us to a
+        step of a small layer, tools/step_overhead.py); after a short idle, the kernel pass
+        times the conv alone on the prepacked filter."""
         torch, st = self.torch, self.stream
 
         def one():
@@ -211,20 +212,25 @@ class LayerBench:
         for _ in range(warmup):
             one()
         torch.cuda.synchronize()
-        # the two timings alternate step by step, so that both see the same clocks (power-capped
-        # parts slow down over a run: separate passes made the later one look slower)
-        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(steps)]
-        for e0, e1, e2, e3 in ev:
+        # two passes, each started from the same idle power state (the sw power cap lowers the
+        # clocks under sustained load: a pass run right after the other, or alternating with it,
+        # measured up to 5% slower on cfg5)
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(steps)]
+        for e0, e1 in ev:
             flush()
             e0.record(st)
             one()
             e1.record(st)
-            flush()
-            e2.record(st)
-            plan.forward(self.x, None, self.y, self.b0, self.n, st, prepacked=True)
-            e3.record(st)
         torch.cuda.synchronize()
-        return [a.elapsed_time(b) for a, b, _, _ in ev], [c.elapsed_time(d) for _, _, c, d in ev]
+        step = [a.elapsed_time(b) for a, b in ev]
+        time.sleep(0.3)
+        for e0, e1 in ev:
+            flush()
+            e0.record(st)
+            plan.forward(self.x, None, self.y, self.b0, self.n, st, prepacked=True)
+            e1.record(st)
+        torch.cuda.synchronize()
+        return step, [a.elapsed_time(b) for a, b in ev]
 
     # -- steady state: rotating sets, back-to-back launches -------------------------------
     def _rotating_sets(self):
