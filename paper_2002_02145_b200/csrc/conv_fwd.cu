@@ -658,7 +658,7 @@ void launch_conv(const conv_plan* P, const ConvParams& prm, const CUtensorMap& a
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CS);
     cfg.blockDim = dim3(Cfg::kThreads);
-    cfg.dynamicSmemBytes = Cfg::smem_bytes(prm.ring_bytes);
+    cfg.dynamicSmemBytes = Cfg::smem_bytes(prm.ring_bytes, prm.ostages);
     cfg.stream = st;
     // programmatic stream serialization (PDL): the prologue overlaps the
     // preceding kernel; the producer's griddepcontrol.wait orders the operands
@@ -990,6 +990,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
     prm.b_lo_off = prm.b_off + s.kps * brows * 64;
     prm.tmem_a = s.tmem_a;
     prm.egroups = s.egroups;
+    prm.ostages = s.ostages;
     prm.absmax_a = amax_a;
     prm.absmax_b = P->absmax;
     prm.ncat = P->ncat ? 1 : 0;
@@ -1025,7 +1026,7 @@ void launch_range(const conv_plan* P, const float* in, const float* flt, float* 
       if (prm.stages > kHaloB || prm.hb_stages < (s.b_res ? 1 : 2) || prm.hb_stages > kMaxStages - kHaloB)
         throw RuntimeError("internal: bad halo stage plan");
     }
-    if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget)
+    if (prm.stages < 2 || prm.stages > kMaxStages || prm.ring_bytes > kStageBudget - (prm.ostages - kOutStages) * kOutStageBytes)
       throw RuntimeError("internal: bad pipeline stage plan");
   }
   const int chunk = s.chunk > 0 ? s.chunk : prm.ksteps;

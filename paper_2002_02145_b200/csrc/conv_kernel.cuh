@@ -117,6 +117,10 @@ struct ConvParams {
   int tap_dw;                     // input columns between consecutive ki taps (1; G for the
                                   // (c,s)-folded input, conv_fwd.cu fold)
   int egroups;                    // host dispatch: epilogue warp groups (kernel template EG)
+  int ostages;                    // output staging blocks of 8 KB after the ring: kOutStages, or
+                                  // kMaxOutStages (recipe os:8, output-heavy layers: the store warp
+                                  // then hands a slot back only when half the slots' stores are
+                                  // still reading, so TMA store latency overlaps the next rounds)
   int ncat;                       // 3xTF32, BN <= 64, not halo: filter rows [B_hi;B_lo] per
                                   // N tile; per K half one N = 2 BN MMA A_hi x [B_hi;B_lo]
                                   // (-> D1 | D2) + one N = BN MMA A_lo x B_hi (-> D1);
@@ -127,7 +131,7 @@ struct ConvParams {
   int accumulate;                 // out += conv
   const float* bias;              // fused epilogue: + bias[k] (nullptr: none)
   int relu;                       // fused epilogue: max(., 0) (not with accumulate)
-  int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores
+  int debug;                      // profiling only (PSCONV_DEBUG): 1 skip A loads, 2 skip MMA, 4 skip stores, 32 skip B loads
   float* out;                     // output at image img_begin
   long long out_img_stride;       // Kb*P*Q*16 floats
   unsigned long long* trace;      // profiling only (PSCONV_DEBUG & 8): CTA 0 stage timestamps
@@ -158,6 +162,8 @@ constexpr int kHaloB = 8;
 // k-step; grouping amortises it over kps k-steps.
 constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
 constexpr int kOutStages = 4;             // staging blocks: two rounds of 32 channels in flight
+constexpr int kMaxOutStages = 8;          // recipe os:8 (ConvParams::ostages): four rounds, the store
+                                          // warp keeps two TMA stores reading smem at a time
 constexpr int kStageBudget = 227 * 1024 - kOutStages * kOutStageBytes - 2048 - 1024;
 constexpr int kMaxStages = 16;
 
@@ -193,15 +199,15 @@ struct KernelCfg {
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes =
       kStageBudget + kOutStages * kOutStageBytes + kBarBytes + 1024;  // upper bound (+align slack)
-  static constexpr int smem_bytes(int ring_bytes) {
-    return ring_bytes + kOutStages * kOutStageBytes + kBarBytes + 1024;
+  static constexpr int smem_bytes(int ring_bytes, int ostages = kOutStages) {
+    return ring_bytes + ostages * kOutStageBytes + kBarBytes + 1024;
   }
   static constexpr int kDrainW = BN < 32 ? BN : 32;  // epilogue TMEM load width (columns)
   static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
   static_assert(kBRows >= 8, "B rows per CTA must be whole 8-row swizzle atoms");
   static_assert(2 * (kABytes + kBBytes) * (SPLIT3 ? 2 : 1) <= kStageBudget, "two stages of one k-step");
   static_assert(kSmemBytes <= 227 * 1024, "smem");
-  static_assert(4 * kMaxStages * 8 + 4 * 8 + 8 + 2 * kOutStages * 8 + kOutStages * 4 <= kBarBytes,
+  static_assert(4 * kMaxStages * 8 + 4 * 8 + 8 + 2 * kMaxOutStages * 8 + kMaxOutStages * 4 <= kBarBytes,
                 "barriers");  // full/split/empty/aslot + acc + tmem slot/ticket + staging slots
   static_assert(kColsNeeded <= 512, "TMEM");
   // 3xTF32's splitter needs a CTA-local "A landed" signal; pairing it would need
@@ -733,8 +739,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   auto stage_base = [&](int s) { return smem + s * p.stage_bytes; };
 
-  uint8_t* out_stage = smem + p.ring_bytes;  // kOutStages x 8 KB (1024-B aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.ring_bytes + kOutStages * Cfg::kOutStageBytes);
+  uint8_t* out_stage = smem + p.ring_bytes;  // p.ostages x 8 KB (1024-B aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.ring_bytes + p.ostages * Cfg::kOutStageBytes);
   uint64_t* full = bars;                         // own TMA landed (1 arrive + tx)
   uint64_t* split_full = bars + kMaxStages;      // own splitter done (count 128)
   uint64_t* empty = bars + 2 * kMaxStages;       // MMA consumed the stage (commit, pair: both CTAs)
@@ -744,8 +750,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aslot_empty + kMaxStages);
   volatile int* split_word = reinterpret_cast<volatile int*>(tmem_slot + 1);  // split-K ticket broadcast
   uint64_t* out_full = aslot_empty + kMaxStages + 1;  // staging slot filled (128 epilogue threads)
-  uint64_t* out_free = out_full + kOutStages;         // staging slot read by its TMA store (store warp)
-  volatile int* out_skip = reinterpret_cast<volatile int*>(out_free + kOutStages);  // slot holds no tile
+  uint64_t* out_free = out_full + kMaxOutStages;      // staging slot read by its TMA store (store warp)
+  volatile int* out_skip = reinterpret_cast<volatile int*>(out_free + kMaxOutStages);  // slot holds no tile
 
   const int warp = threadIdx.x >> 5;
   const int rank = PAIR ? static_cast<int>(blockIdx.x & 1) : 0;
@@ -769,7 +775,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
       ptx::mbar_init(&acc_empty[a], 4 * EG * CS);
     }
     for (int a = 0; a < (p.tmem_a ? p.a_slots : 0); ++a) ptx::mbar_init(&aslot_empty[a], 1);
-    for (int o = 0; o < kOutStages; ++o) {
+    for (int o = 0; o < kMaxOutStages; ++o) {
       ptx::mbar_init(&out_full[o], 128);
       ptx::mbar_init(&out_free[o], 1);
     }
@@ -821,8 +827,9 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // PAIR: both CTAs' loads complete on the LEADER's full barrier (the leader
     // expects both shares); the second CTA never arrives on its own.
     const bool skip_a = (p.debug & 1) != 0;
+    const bool skip_b = (p.debug & 32) != 0;  // profiling: what a resident filter would save
     const uint32_t tx1 =
-        ((skip_a ? 0u : a_step_bytes) + Cfg::kBBytes * (SPLIT3 && !F16 ? 2 : 1)) * CS;  // per k-step
+        ((skip_a ? 0u : a_step_bytes) + (skip_b ? 0u : Cfg::kBBytes * (SPLIT3 && !F16 ? 2 : 1))) * CS;  // per k-step
     const uint32_t full_leader = PAIR ? ptx::mapa(&full[0], 0) : 0u;
     // cb_group: one coordinate step per stage, boxes span kps channel blocks;
     // otherwise kps coordinate steps per stage (the last stage may be partial)
@@ -872,8 +879,8 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d(sa + i * p.a_pitch, &tmap_in, &full[stage], 0, wq + tw, hp + r, n0, cb + i);
               // (ncat: one box of [B_hi;B_lo] rows of the N tile)
-              ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, ncat ? 2 * k0 : k0, rs, cb >> p.b128);
-              if (SPLIT3 && !F16 && !ncat)
+              if (!skip_b) ptx::tma_load_4d(sbb, &tmap_flt, &full[stage], 0, ncat ? 2 * k0 : k0, rs, cb >> p.b128);
+              if (SPLIT3 && !F16 && !ncat && !skip_b)
                 ptx::tma_load_4d(sbb - p.b_off + p.b_lo_off, &tmap_flt_lo, &full[stage], 0, k0, rs,
                                  cb >> p.b128);
             } else {
@@ -881,7 +888,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
               if (!skip_a)
                 for (int i = 0; i < p.a_boxes; ++i)
                   ptx::tma_load_5d_cb(sa + i * p.a_pitch, &tmap_in, fb, 0, wq + tw, hp + r, n0, cb + i);
-              ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
+              if (!skip_b) ptx::tma_load_4d_cb(sbb, &tmap_flt, fb, 0, k0, rs, cb >> p.b128);
             }
           }
           if (++v2 == e2) {
@@ -1099,7 +1106,13 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // back. Slots of split-K writer units carry no tile (out_skip).
     constexpr int DW = Cfg::kDrainW;
     constexpr int kBlk = DW / 16;
-    constexpr int kRounds = kOutStages / EG / kBlk;  // staging slots per epilogue group
+    const int kRounds = p.ostages / EG / kBlk;  // staging slots per epilogue group
+    // os:8 -- deferred hand-back: up to `depth` (half the slots) bulk groups keep reading smem
+    // while the epilogue fills the other half; a slot returns once `depth` younger groups are
+    // committed (cp.async.bulk.wait_group.read depth). Default staging: one group at a time.
+    const int depth = p.ostages > kOutStages ? (kRounds * EG) / 2 : 0;
+    uint32_t fifo = 0u;  // committed slots, oldest in the low nibble
+    int pending = 0;
     if (ptx::elect_one()) {
       ptx::prefetch_tmap(&tmap_out);
       int ost[2] = {0, 0};
@@ -1126,9 +1139,31 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
                 ptx::tma_store_5d(&tmap_out, st + blk * Cfg::kOutStageBytes, 0, q0, p0, kb, n0);
             }
             ptx::bulk_commit();
-            ptx::bulk_wait_read<0>();  // the slot's bytes are in flight to global memory
+            if (depth == 0) {
+              ptx::bulk_wait_read<0>();  // the slot's bytes are in flight to global memory
+              ptx::mbar_arrive(&out_free[slot]);
+            } else {
+              fifo |= static_cast<uint32_t>(slot) << (4 * pending);
+              if (++pending > depth) {
+                if (depth == 1) ptx::bulk_wait_read<1>();
+                else if (depth == 2) ptx::bulk_wait_read<2>();
+                else ptx::bulk_wait_read<4>();
+                while (pending > depth) {
+                  ptx::mbar_arrive(&out_free[fifo & 15u]);
+                  fifo >>= 4;
+                  --pending;
+                }
+              }
+            }
+          } else {
+            // a slot without a store (split-K writer unit): no younger group will push the
+            // pending ones out, so drain them here (else the epilogue could wait on them forever)
+            if (pending > 0) {
+              ptx::bulk_wait_read<0>();
+              for (; pending > 0; --pending, fifo >>= 4) ptx::mbar_arrive(&out_free[fifo & 15u]);
+            }
+            ptx::mbar_arrive(&out_free[slot]);
           }
-          ptx::mbar_arrive(&out_free[slot]);
           if (++ost[g] == kRounds) {
             ost[g] = 0;
             oph[g] ^= 1u;
@@ -1332,7 +1367,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
             // barrier pair and one bulk group per round, kOutStages/(DW/16)
             // rounds in flight
             constexpr int kBlk = DW / 16;
-            constexpr int kRounds = kOutStages / kGroups / kBlk;  // per group
+            const int kRounds = p.ostages / kGroups / kBlk;  // per group
             const int slot = egrp * kRounds + ostage;
             uint8_t* st = out_stage + slot * (kBlk * Cfg::kOutStageBytes);
             ptx::mbar_wait(&out_free[slot], oph ^ 1u);  // the slot's previous store has read it

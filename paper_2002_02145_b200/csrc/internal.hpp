@@ -62,6 +62,7 @@ struct Recipe {
   int br = -1;                                                // halo: resident filter, -1 auto
   int chunk = 0;                                              // 0 = default (3x: 16 k-steps)
   int eg = 0;                                                 // epilogue warp groups, 0 = auto (1)
+  int os = 0;                                                 // output staging blocks (4 or 8), 0 = default (4)
   int pp = 0;                                                 // parity-plane tap pairs: C real channels (<= 4)
   int tc = 0;                                                 // halo: the kw taps of a row concatenated on N
   int cs = 0;                                                 // cluster size, 0 = default
@@ -91,6 +92,8 @@ struct Schedule {
   int split_all = 0;   // split every tile (zeroed output, all partials reduce-added)
                        // instead of only the last partial wave's (flag-ordered)
   int egroups = 1;     // epilogue warp groups draining alternate 32-channel rounds (1 or 2)
+  int ostages = 4;     // output staging blocks of 8 KB (recipe os:8 -- 32 KB less ring, deferred
+                       // staging-slot hand-back in the store warp; not halo)
   int pp = 0;          // few-channel kernel (conv_pp.cuh): C <= 4 real channels, tap pairs per MMA
   int tc = 0;          // halo tap concat (TF32, 3x3, bn == nOfm <= 64): one N = 3 bn MMA per filter row
                        // (the three ki taps share the A rows; the epilogue adds D_ki shifted by ki rows)

@@ -132,6 +132,9 @@ Recipe Recipe::parse(const std::string& text) {
         } else if (key == "eg") {
           r.eg = static_cast<int>(parse_int(val, "gpu epilogue groups"));
           if (r.eg != 1 && r.eg != 2) throw ConfigError("gpu eg must be 1 or 2");
+        } else if (key == "os") {
+          r.os = static_cast<int>(parse_int(val, "gpu output staging blocks"));
+          if (r.os != 4 && r.os != 8) throw ConfigError("gpu os must be 4 or 8");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -169,6 +172,7 @@ std::string Recipe::id() const {
     if (br >= 0) s += ",br:" + std::to_string(br);
     if (kg) s += ",kg:" + std::to_string(kg);
     if (eg) s += ",eg:" + std::to_string(eg);
+    if (os) s += ",os:" + std::to_string(os);
     if (pp) s += ",pp:" + std::to_string(pp);
     if (chunk) s += ",ch:" + std::to_string(chunk);
   }
@@ -378,6 +382,9 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   s.ta = r.ta;
   s.br = r.br;
   canon.br = r.br;
+  if (r.os == 8 && s.halo) throw ConfigError("GPU tile: os:8 (deep output staging) is not available in halo mode");
+  if (r.os == 8 && r.pp) throw ConfigError("GPU tile: os:8 is not an option of the few-channel kernel (pp)");
+  s.ostages = r.os == 8 ? 8 : 4;
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
@@ -463,6 +470,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.kg = r.kg ? s.kps : 0;
   s.egroups = r.eg ? r.eg : 1;
   canon.eg = s.egroups == 2 ? 2 : 0;
+  canon.os = s.ostages == 8 ? 8 : 0;
   s.recipe_id = canon.id();
   return s;
 }
@@ -564,7 +572,7 @@ void plan_stages(const conv_desc& d, Schedule& s, int mode, int kg) {
   auto ring = [&](int k) {
     Schedule t = s;
     t.kps = k;
-    return std::min(kSmemMaxStages, kSmemStageBudget / stage_bytes(t, mode));
+    return std::min(kSmemMaxStages, (kSmemStageBudget - (s.ostages - 4) * 8192) / stage_bytes(t, mode));
   };
   int kps = 1;
   if (kg) {

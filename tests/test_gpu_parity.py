@@ -448,6 +448,39 @@ def test_split_k(conv, c_log, recipe, mode):
         _check("ks-pair", conv, c_log, 16, mode, n, recipe + ",cl:2")
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("conv,c_log,recipe", [
+    # output-heavy 1x1 shapes: many tiles per CTA so the staging ring wraps many times
+    ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:256,box:4x4x8,cl:1,os:8"),
+    ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:256,box:4x4x8,cl:1,eg:2,os:8"),
+    ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:128,box:2x4x16,cl:1,os:8"),
+    ("conv:40,128,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:64,box:4x4x8,cl:1,os:8"),
+    ("conv:40,128,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:16,box:4x4x8,cl:1,os:8"),
+    ("conv:12,128,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:128,box:2x2x32,cl:1,ks:3,os:8"),
+])
+def test_deep_output_staging(conv, c_log, recipe, mode):
+    """os:8: eight staging blocks; the store warp hands a slot back only once half the slots'
+    TMA stores are still reading shared memory (deferred, in order)."""
+    n = ps.ConvPreset.parse(conv).nImg
+    _check("os8", conv, c_log, 21, mode, n, recipe)
+    if mode == "tf32" and "bn:16" not in recipe:
+        _check("os8-pair", conv, c_log, 21, mode, n, recipe.replace("cl:1", "cl:2"))
+
+
+@pytest.mark.gpu
+def test_deep_output_staging_accumulate():
+    """os:8 with `+=` (TMA reduce-add stores) on a pre-filled output."""
+    conv = "conv:24,256,64,14,14,1,1,1,1,16,0,0,14,14"
+    p = ps.ConvPreset.parse(conv)
+    sx, sw = seeds(22)
+    init = np.random.default_rng(5).uniform(-1, 1, p.output_elems()).astype(np.float32)
+    _, _, yg, rec = _run_gpu(p, 64, sx, sw, "3xtf32", "gpu=bn:256,box:2x2x32,cl:1,os:8",
+                             accumulate=True, out_init=init)
+    ref = oracle.conv(p, oracle.fill_input(p, sx, 64), oracle.fill_filter(p, sw, 64)).ravel() + init
+    assert oracle.rel_l2(yg, ref) <= 1e-5, rec
+
+
 TAIL = "conv:8,64,64,56,56,3,3,1,1,16,1,1,56,56"  # 196 tiles of 8x8x2 px: 1 wave + 48
 
 
