@@ -162,8 +162,8 @@ constexpr int kHaloB = 8;
 // k-step; grouping amortises it over kps k-steps.
 constexpr int kOutStageBytes = 128 * 64;  // one 128-pixel x 16-channel output block
 constexpr int kOutStages = 4;             // staging blocks: two rounds of 32 channels in flight
-constexpr int kMaxOutStages = 8;          // recipe os:8 (ConvParams::ostages): four rounds, the store
-                                          // warp keeps two TMA stores reading smem at a time
+constexpr int kMaxOutStages = 16;         // recipe os:8 / 12 / 16 (ConvParams::ostages): more rounds, the
+                                          // store warp keeps half of them reading smem at a time
 constexpr int kStageBudget = 227 * 1024 - kOutStages * kOutStageBytes - 2048 - 1024;
 constexpr int kMaxStages = 16;
 
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
     // while the epilogue fills the other half; a slot returns once `depth` younger groups are
     // committed (cp.async.bulk.wait_group.read depth). Default staging: one group at a time.
     const int depth = p.ostages > kOutStages ? (kRounds * EG) / 2 : 0;
-    uint32_t fifo = 0u;  // committed slots, oldest in the low nibble
+    uint64_t fifo = 0u;  // committed slots, oldest in the low nibble
     int pending = 0;
     if (ptx::elect_one()) {
       ptx::prefetch_tmap(&tmap_out);
@@ -1143,11 +1143,16 @@ __global__ void __launch_bounds__(KernelCfg<BN, SPLIT3, PAIR, EG>::kThreads, 1)
               ptx::bulk_wait_read<0>();  // the slot's bytes are in flight to global memory
               ptx::mbar_arrive(&out_free[slot]);
             } else {
-              fifo |= static_cast<uint32_t>(slot) << (4 * pending);
+              fifo |= static_cast<uint64_t>(slot) << (4 * pending);
               if (++pending > depth) {
-                if (depth == 1) ptx::bulk_wait_read<1>();
-                else if (depth == 2) ptx::bulk_wait_read<2>();
-                else ptx::bulk_wait_read<4>();
+                switch (depth) {  // (an immediate operand)
+                  case 1: ptx::bulk_wait_read<1>(); break;
+                  case 2: ptx::bulk_wait_read<2>(); break;
+                  case 3: ptx::bulk_wait_read<3>(); break;
+                  case 4: ptx::bulk_wait_read<4>(); break;
+                  case 6: ptx::bulk_wait_read<6>(); break;
+                  default: ptx::bulk_wait_read<8>(); break;
+                }
                 while (pending > depth) {
                   ptx::mbar_arrive(&out_free[fifo & 15u]);
                   fifo >>= 4;

@@ -134,7 +134,7 @@ Recipe Recipe::parse(const std::string& text) {
           if (r.eg != 1 && r.eg != 2) throw ConfigError("gpu eg must be 1 or 2");
         } else if (key == "os") {
           r.os = static_cast<int>(parse_int(val, "gpu output staging blocks"));
-          if (r.os != 4 && r.os != 8) throw ConfigError("gpu os must be 4 or 8");
+          if (r.os != 4 && r.os != 8 && r.os != 12 && r.os != 16) throw ConfigError("gpu os must be 4, 8, 12 or 16");
         } else if (key == "ch") {
           r.chunk = static_cast<int>(parse_int(val, "gpu chunk"));
           if (r.chunk < 1) throw ConfigError("gpu chunk must be positive");
@@ -382,9 +382,11 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   s.ta = r.ta;
   s.br = r.br;
   canon.br = r.br;
-  if (r.os == 8 && s.halo) throw ConfigError("GPU tile: os:8 (deep output staging) is not available in halo mode");
-  if (r.os == 8 && r.pp) throw ConfigError("GPU tile: os:8 is not an option of the few-channel kernel (pp)");
-  s.ostages = r.os == 8 ? 8 : 4;
+  if (r.os > 4 && s.halo) throw ConfigError("GPU tile: os (deep output staging) is not available in halo mode");
+  if (r.os > 4 && r.pp) throw ConfigError("GPU tile: os is not an option of the few-channel kernel (pp)");
+  s.ostages = r.os > 4 ? r.os : 4;
+  if (s.ostages == 12 && (r.eg == 2 || s.bn < 32))  // whole rounds per epilogue group
+    throw ConfigError("GPU tile: os:12 needs one epilogue group and bn >= 32");
   // cluster size sharing the filter block: largest of {4, 2, 1} keeping >= 8-row pieces
   // cl:2 = CTA pair (tcgen05.mma.cta_group::2, M=256, each SM stages half of B);
   // TF32 only (see conv_kernel.cuh)
@@ -470,7 +472,7 @@ Schedule resolve_schedule(const conv_desc& d, const Recipe& r, int mode, bool gp
   canon.kg = r.kg ? s.kps : 0;
   s.egroups = r.eg ? r.eg : 1;
   canon.eg = s.egroups == 2 ? 2 : 0;
-  canon.os = s.ostages == 8 ? 8 : 0;
+  canon.os = s.ostages > 4 ? s.ostages : 0;
   s.recipe_id = canon.id();
   return s;
 }

@@ -49,6 +49,14 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
     # epilogue-heavy layers, slower on others
     if int(kv["bn"]) >= 64:
         alts.append({**kv, "eg": "2"})
+    # deep output staging (os:8: 32 KB of the ring become four more staging blocks and the
+    # store warp keeps two TMA stores in flight): output-heavy layers, mostly TF32
+    if not any(key in kv for key in ("halo", "tc", "pp")):
+        alts.append({**kv, "os": "8"})
+        if "eg" not in kv:
+            alts.append({**kv, "os": "12"})
+        if bn >= 64 and "eg" not in kv:
+            alts.append({**kv, "eg": "2", "os": "8"})
     if mode in ("3xtf32", "f16x2") and bn == 128:  # TMEM-resident A is opt-in at bn 128
         alts.append({**kv, "ta": "1"})
     widest = max(c for c in (16, 32, 64, 128, 256) if preset.nOfm % c == 0)

@@ -131,14 +131,15 @@ def test_epilogue_groups_recipe_key():
 
 
 def test_output_staging_recipe_key():
-    """os:8 (eight 8 KB output staging blocks, deferred hand-back in the store warp) is a
+    """os:8 / 12 / 16 (8 KB output staging blocks, deferred hand-back in the store warp) is a
     non-halo option of the main kernel: 4 is the default and not shown, other values and
     halo / pp combinations are rejected."""
     p = ConvPreset.parse("conv:8,128,64,8,8,3,3,1,1,16,1,1,8,8")
     assert "os:" not in ps.select_topk(p, "tf32", 1)[0][0]
     assert ps.model_us(p, "gpu=bn:128,os:8", "tf32") > 0
     assert ps.model_us(p, "gpu=bn:128,os:4", "3xtf32") > 0
-    for bad in ("gpu=bn:64,os:2", "gpu=bn:64,os:16", "gpu=bn:64,halo:1,os:8"):
+    assert ps.model_us(p, "gpu=bn:128,os:16", "tf32") > 0
+    for bad in ("gpu=bn:64,os:2", "gpu=bn:64,os:32", "gpu=bn:64,halo:1,os:8", "gpu=bn:64,eg:2,os:12"):
         with pytest.raises(ConfigRejectedError):
             ps.model_us(p, bad, "tf32")
 

@@ -457,11 +457,14 @@ def test_split_k(conv, c_log, recipe, mode):
     ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:128,box:2x4x16,cl:1,os:8"),
     ("conv:40,128,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:64,box:4x4x8,cl:1,os:8"),
     ("conv:40,128,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:16,box:4x4x8,cl:1,os:8"),
+    ("conv:40,128,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:16,box:4x4x8,cl:1,os:16"),
+    ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:256,box:4x4x8,cl:1,os:12"),
+    ("conv:40,256,64,28,28,1,1,1,1,16,0,0,28,28", 64, "gpu=bn:256,box:4x4x8,cl:1,eg:2,os:16"),
     ("conv:12,128,128,14,14,3,3,1,1,16,1,1,14,14", 128, "gpu=bn:128,box:2x2x32,cl:1,ks:3,os:8"),
 ])
 def test_deep_output_staging(conv, c_log, recipe, mode):
-    """os:8: eight staging blocks; the store warp hands a slot back only once half the slots'
-    TMA stores are still reading shared memory (deferred, in order)."""
+    """os:8 / 12 / 16 staging blocks; the store warp hands a slot back only once half the
+    slots' TMA stores are still reading shared memory (deferred, in order)."""
     n = ps.ConvPreset.parse(conv).nImg
     _check("os8", conv, c_log, 21, mode, n, recipe)
     if mode == "tf32" and "bn:16" not in recipe:

@@ -1,0 +1,119 @@
+"""Refine the committed plan cache with recipe options added after it was tuned.
+
+For every cached (descriptor, mode) whose best recipe runs the main kernel without the halo, time
+the cached recipe against the same recipe with os:8 (deep output staging; with and without the
+second epilogue group; os:12 for entries already at os:8), interleaved on the same box (prepacked filter, L2 flushed, median), and
+keep a variant only if it wins by more than `--margin`. Rewrites plans_b200.json in place.
+
+  python tools/refine_plans.py [--margin 0.03] [--reps 9] [--only tf32]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2002_02145_b200 as ps  # noqa: E402
+from paper_2002_02145_b200 import tune, workloads  # noqa: E402
+from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
+
+
+def workload_of(conv: str):
+    """(c_logical, seeds) of the named workload with these fields (any image count)."""
+    tail = conv.split(",", 1)[1]
+    for _, (c, c_log, cid) in workloads.ALL.items():
+        if c.split(",", 1)[1] == tail:
+            return c_log, workloads.seeds(cid)
+    return 0, (1, 2)
+
+
+def variants(recipe: str):
+    head, gpu = recipe.split(";gpu=")
+    kv = dict(item.split(":") for item in gpu.split(","))
+    if any(k in kv for k in ("halo", "tc", "pp")):
+        return []
+    if "os" in kv:  # already refined: try the next depth only
+        return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in {**kv, "os": "12"}.items())] \
+            if kv["os"] == "8" and "eg" not in kv else []
+    out = [{**kv, "os": "8"}]
+    if int(kv["bn"]) >= 64:
+        if "eg" in kv:
+            out.append({**{k: v for k, v in kv.items() if k != "eg"}, "os": "8"})
+        else:
+            out.append({**kv, "eg": "2", "os": "8"})
+    return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in a.items()) for a in out]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--margin", type=float, default=0.03)
+    ap.add_argument("--reps", type=int, default=9)
+    ap.add_argument("--only", default=None, help="mode filter")
+    ap.add_argument("--out", default=tune.PLANS_PATH)
+    args = ap.parse_args()
+    with open(tune.PLANS_PATH) as fh:
+        cache = json.load(fh)
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream(dev)
+    flush = L2Flush(dev)
+    changed = 0
+    for key in sorted(cache):
+        conv, mode = key.split("|")
+        if args.only and mode != args.only:
+            continue
+        base = cache[key]["recipe"]
+        alts = variants(base)
+        if not alts:
+            continue
+        p = ps.ConvPreset.parse(conv)
+        c_log, seeds = workload_of(conv)
+        x = torch.empty(p.input_elems(), dtype=torch.float32, device=dev)
+        w = torch.empty(p.filter_elems(), dtype=torch.float32, device=dev)
+        y = torch.empty(p.output_elems(), dtype=torch.float32, device=dev)
+        ps.fill_input(p, seeds[0], x, c_logical=c_log)
+        ps.fill_filter(p, seeds[1], w, c_logical=c_log)
+        plans = []
+        for rid in [base] + alts:
+            try:
+                pl = ps.ConvPlan(p, mode=mode, device=0, recipe=rid)
+            except ps.ConfigRejectedError:
+                continue
+            pl.prepack(w, st)
+            plans.append((pl.recipe, pl, []))
+        for pl in plans:  # warm-up
+            for _ in range(2):
+                pl[1].forward(x, None, y, stream=st, prepacked=True)
+        for _ in range(args.reps):  # interleaved: same clocks for every candidate
+            for _, pl, ts in plans:
+                flush()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                pl.forward(x, None, y, stream=st, prepacked=True)
+                e1.record(st)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        rows = [(rid, statistics.median(ts)) for rid, _, ts in plans]
+        for _, pl, _ in plans:
+            pl.close()
+        b_us = rows[0][1]
+        best = min(rows[1:], key=lambda r: r[1], default=None)
+        line = f"{key}: base {b_us:.1f} us; " + "; ".join(f"{r.split('gpu=')[1]} {u:.1f}" for r, u in rows[1:])
+        if best and best[1] < (1.0 - args.margin) * b_us:
+            cache[key]["recipe"] = best[0]
+            cache[key]["ranked"] = [[best[0], 0.0, best[1]]] + cache[key].get("ranked", [])
+            cache[key]["refined"] = f"os:8 pass: {b_us:.1f} -> {best[1]:.1f} us (tools/refine_plans.py)"
+            changed += 1
+            line += "  => " + best[0].split("gpu=")[1]
+        print(line, flush=True)
+        del x, w, y
+    with open(args.out, "w") as fh:
+        json.dump(cache, fh, indent=1, sort_keys=True)
+    print(f"refined {changed} of {len(cache)} entries -> {args.out}")
+
+
+if __name__ == "__main__":
+    main()
