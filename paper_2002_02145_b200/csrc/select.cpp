@@ -240,7 +240,12 @@ ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode) {
   // sum); double-buffered, so a tile costs max(mainloop, epilogue). The CTA pair couples
   // both CTAs' epilogues on one accumulator release (~1.3x when it binds).
   const double rounds = std::max(1.0, s.bn / 32.0);
-  const double epi_tile = (EPI_FIX + rounds * ((s.tc ? EPI_TC : EPI_ROUND) + (nchunks - 1.0) * 250.0)) /
+  // deep output staging (os:8 / 12): the TMA stores' shared-memory reads overlap the next
+  // rounds; A/B on the epilogue-bound TF32 1x1 layers (tools/refine_plans.py, r02): a tile's
+  // rounds cost ~0.82x (os:8), ~0.78x (os:12+). Its price -- 32+ KB less ring, so fewer
+  // k-steps per stage -- is already in s.kps / s.stages.
+  const double os_f = s.ostages >= 12 ? 0.78 : (s.ostages >= 8 ? 0.82 : 1.0);
+  const double epi_tile = (EPI_FIX + rounds * ((s.tc ? EPI_TC : EPI_ROUND) * os_f + (nchunks - 1.0) * 250.0)) /
                           (s.egroups == 2 ? EPI_EG : 1.0) * (cs == 2 ? EPI_PAIR : 1.0);
   const double main_tile = double(ksteps) * kstep_cyc;
   const double tile_cyc = std::max(main_tile, epi_tile) + (drain_exposed ? nchunks * drain_cyc : drain_cyc);
@@ -317,6 +322,14 @@ std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
         r.box_n = n;
         Schedule s = resolve_schedule(d, r, mode);
         if (seen.insert(s.recipe_id).second) out.push_back(s);
+        // the same tile with deep output staging (epilogue-bound layers)
+        r.os = 8;
+        try {
+          Schedule s8 = resolve_schedule(d, r, mode);
+          if (seen.insert(s8.recipe_id).second) out.push_back(s8);
+        } catch (const ConfigError&) {
+          // the smaller ring does not hold two stages at this bn
+        }
       }
   // halo mode (stride-1 R x S > 1): its own tile shape (whole padded rows)
   if (halo_eligible(d))
