@@ -67,6 +67,8 @@ def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list
             if mode in ("3xtf32", "f16x2"):
                 alt["ch"] = "32" if nb == 256 else "16"
             alts.append(alt)
+            if mode in ("3xtf32", "f16x2") and nb == 128:  # (l2 1x1 128->512: 183 -> 160 us)
+                alts.append({**alt, "ta": "1"})
     # tail split-K: the model's split decision both ways
     # (kt:1 splits every tile instead of the tail wave: faster on some 3xTF32 layers)
     if "ks" in kv:

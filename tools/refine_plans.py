@@ -31,9 +31,22 @@ def workload_of(conv: str):
     return 0, (1, 2)
 
 
-def variants(recipe: str):
+def variants(recipe: str, what: str = "os", mode: str = "tf32", n_ofm: int = 0):
     head, gpu = recipe.split(";gpu=")
     kv = dict(item.split(":") for item in gpu.split(","))
+    if what == "ta":
+        # 3xTF32 plans at bn 256 / 128 without TMEM-resident A: the bn 128 + ta:1 tile (the
+        # tuner only tried ta:1 when the model's own top-1 was at bn 128)
+        if mode != "3xtf32" or any(k in kv for k in ("halo", "tc", "pp", "ta")) or n_ofm % 128:
+            return []
+        if kv["bn"] not in ("256", "128"):
+            return []
+        base = {k: v for k, v in kv.items() if k not in ("os", "eg", "ch")}
+        base.update({"bn": "128", "ta": "1"})
+        if "ch" in kv:
+            base["ch"] = str(min(int(kv["ch"]), 16))
+        out = [base, {**base, "eg": "2"}, {**base, "os": "8"}]
+        return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in a.items()) for a in out]
     if any(k in kv for k in ("halo", "tc", "pp")):
         return []
     if "os" in kv:  # already refined: try the next depth only
@@ -53,6 +66,7 @@ def main():
     ap.add_argument("--margin", type=float, default=0.03)
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--only", default=None, help="mode filter")
+    ap.add_argument("--what", default="os", choices=["os", "ta"], help="which option to try")
     ap.add_argument("--out", default=tune.PLANS_PATH)
     args = ap.parse_args()
     with open(tune.PLANS_PATH) as fh:
@@ -66,10 +80,10 @@ def main():
         if args.only and mode != args.only:
             continue
         base = cache[key]["recipe"]
-        alts = variants(base)
+        p = ps.ConvPreset.parse(conv)
+        alts = variants(base, args.what, mode, p.nOfm)
         if not alts:
             continue
-        p = ps.ConvPreset.parse(conv)
         c_log, seeds = workload_of(conv)
         x = torch.empty(p.input_elems(), dtype=torch.float32, device=dev)
         w = torch.empty(p.filter_elems(), dtype=torch.float32, device=dev)
@@ -105,7 +119,7 @@ def main():
         if best and best[1] < (1.0 - args.margin) * b_us:
             cache[key]["recipe"] = best[0]
             cache[key]["ranked"] = [[best[0], 0.0, best[1]]] + cache[key].get("ranked", [])
-            cache[key]["refined"] = f"os:8 pass: {b_us:.1f} -> {best[1]:.1f} us (tools/refine_plans.py)"
+            cache[key]["refined"] = f"{args.what} pass: {b_us:.1f} -> {best[1]:.1f} us (tools/refine_plans.py)"
             changed += 1
             line += "  => " + best[0].split("gpu=")[1]
         print(line, flush=True)
