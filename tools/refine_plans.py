@@ -34,6 +34,15 @@ def workload_of(conv: str):
 def variants(recipe: str, what: str = "os", mode: str = "tf32", n_ofm: int = 0):
     head, gpu = recipe.split(";gpu=")
     kv = dict(item.split(":") for item in gpu.split(","))
+    if what == "kg":
+        # k-steps per stage: the default takes the largest of {4, 2} leaving >= 3 stages; HBM-fed
+        # long reductions want more, smaller stages in flight (CTA-0 trace of l4 1x1 2048->512 TF32:
+        # a 3-stage ring of 4 k-steps turns a slot around in ~3000 cycles = MMA 1024 + issue 500 +
+        # load latency 1500, i.e. ~1000 cycles per stage with the tensor pipe waiting on `full`)
+        if any(k in kv for k in ("halo", "tc", "pp", "kg")):
+            return []
+        out = [{**kv, "kg": g} for g in ("1", "2", "4")]
+        return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in a.items()) for a in out]
     if what == "ta":
         # 3xTF32 plans at bn 256 / 128 without TMEM-resident A: the bn 128 + ta:1 tile (the
         # tuner only tried ta:1 when the model's own top-1 was at bn 128)
@@ -66,7 +75,7 @@ def main():
     ap.add_argument("--margin", type=float, default=0.03)
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--only", default=None, help="mode filter")
-    ap.add_argument("--what", default="os", choices=["os", "ta"], help="which option to try")
+    ap.add_argument("--what", default="os", choices=["os", "ta", "kg"], help="which option to try")
     ap.add_argument("--out", default=tune.PLANS_PATH)
     args = ap.parse_args()
     with open(tune.PLANS_PATH) as fh:
