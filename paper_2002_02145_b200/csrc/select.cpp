@@ -322,14 +322,27 @@ std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
         r.box_n = n;
         Schedule s = resolve_schedule(d, r, mode);
         if (seen.insert(s.recipe_id).second) out.push_back(s);
-        // the same tile with deep output staging (epilogue-bound layers)
-        r.os = 8;
-        try {
-          Schedule s8 = resolve_schedule(d, r, mode);
-          if (seen.insert(s8.recipe_id).second) out.push_back(s8);
-        } catch (const ConfigError&) {
-          // the smaller ring does not hold two stages at this bn
-        }
+        // the same tile over the kernel's structural options, so that the model -- not a
+        // hand-written list in the tuner -- ranks them: deep output staging (os:8, epilogue-
+        // bound layers), the single CTA instead of the pair (TF32; HBM-bound K <= 64 layers),
+        // TMEM-resident A at bn 128 (3xTF32)
+        for (int os : {0, 8})
+          for (int alt = 0; alt < 2; ++alt) {
+            if (os == 0 && alt == 0) continue;  // the default above
+            Recipe v = r;
+            v.os = os;
+            if (alt == 1) {
+              if (mode == PSCONV_MODE_TF32) v.cs = 1;
+              else if (split_mode(mode) && bn == 128) v.ta = 1;
+              else continue;
+            }
+            try {
+              Schedule sv = resolve_schedule(d, v, mode);
+              if (seen.insert(sv.recipe_id).second) out.push_back(sv);
+            } catch (const ConfigError&) {
+              // (the smaller ring does not hold two stages at this bn)
+            }
+          }
       }
   // halo mode (stride-1 R x S > 1): its own tile shape (whole padded rows)
   if (halo_eligible(d))
