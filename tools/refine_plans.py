@@ -43,6 +43,16 @@ def variants(recipe: str, what: str = "os", mode: str = "tf32", n_ofm: int = 0):
             return []
         out = [{**kv, "kg": g} for g in ("1", "2", "4")]
         return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in a.items()) for a in out]
+    if what == "cl":
+        # TF32: the other cluster size with the same options (the tuner toggled cl only on the
+        # model's top-1, before os existed)
+        if mode != "tf32" or any(k in kv for k in ("halo", "tc", "pp")) or "cl" not in kv:
+            return []
+        o = {**kv, "cl": "1" if kv["cl"] == "2" else "2"}
+        out = [o]
+        if "os" not in kv:
+            out.append({**o, "os": "8"})
+        return [head + ";gpu=" + ",".join(f"{k}:{v}" for k, v in a.items()) for a in out]
     if what == "ta":
         # 3xTF32 plans at bn 256 / 128 without TMEM-resident A: the bn 128 + ta:1 tile (the
         # tuner only tried ta:1 when the model's own top-1 was at bn 128)
@@ -75,7 +85,7 @@ def main():
     ap.add_argument("--margin", type=float, default=0.03)
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--only", default=None, help="mode filter")
-    ap.add_argument("--what", default="os", choices=["os", "ta", "kg"], help="which option to try")
+    ap.add_argument("--what", default="os", choices=["os", "ta", "kg", "cl"], help="which option to try")
     ap.add_argument("--out", default=tune.PLANS_PATH)
     args = ap.parse_args()
     with open(tune.PLANS_PATH) as fh:
