@@ -13,7 +13,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
-import bench  # noqa: E402
 import paper_2002_02145_b200 as ps  # noqa: E402
 from paper_2002_02145_b200.timing import L2Flush  # noqa: E402
 from paper_2002_02145_b200.workloads import R50, seeds  # noqa: E402
@@ -35,11 +34,16 @@ assert sum(COUNT.values()) == 53 and set(COUNT) == set(R50)
 def main():
     sweep = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01_sweep.jsonl")
     modes = sys.argv[2:] or ["tf32", "3xtf32", "faithful"]
-    recs = {(r["layer"], r["mode"]): r for r in map(json.loads, open(sweep))}
+    recs = {}
+    for r in map(json.loads, open(sweep)):
+        if "modes" in r:  # r02 sweep rows: one per layer with a "modes" map
+            for m, v in r["modes"].items():
+                recs[(r["layer"], m)] = {**v, "mode": m}
+        else:             # r01 rows: one per (layer, mode)
+            recs[(r["layer"], r["mode"])] = r
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream()
     flush = L2Flush(dev)
-    hbm, bf16, _ = bench.peaks()
     for mode in modes:
         plans, bufs, flops, roof = [], [], 0.0, 0.0
         for name, (conv, c_log, cid) in R50.items():
