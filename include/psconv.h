@@ -127,7 +127,8 @@ int brgemm_f32(const conv_desc* d, float* out, const float* const* flt_blocks,
  * GPU layer entry (sm_100a). A plan binds a descriptor, a mode and a schedule.
  * The schedule is chosen by the selector from the reference's recipe space
  * (variants.hpp:16-65: "perm=...;tile=oj:T") extended with an optional GPU
- * clause ";gpu=bn:B,box:QxPxN,st:S". recipe == NULL lets the selector choose.
+ * clause ";gpu=bn:B,box:QxPxN,cl:1|2,kg:K,ks:S,eg:1|2,os:4|8|12|16,..." (the full key list and
+ * meanings: INTEGRATION.md "Recipe grammar"). recipe == NULL lets the selector choose.
  */
 typedef struct conv_plan conv_plan;
 
