@@ -170,6 +170,41 @@ def test_image_range_and_accumulate():
 
 
 @pytest.mark.gpu
+def test_deep_output_staging_other_entries():
+    """os:8 through the other entry points: an image sub-range, the host-buffer path (chunked,
+    three device slots) and CUDA-graph replay give the plain device result bit for bit."""
+    p = ps.ConvPreset.parse("conv:96,128,64,28,28,1,1,1,1,16,0,0,28,28")
+    sx, sw = seeds(23)
+    dev = torch.device("cuda:0")
+    x = torch.empty(p.input_elems(), device=dev)
+    w = torch.empty(p.filter_elems(), device=dev)
+    ps.fill_input(p, sx, x, c_logical=64)
+    ps.fill_filter(p, sw, w, c_logical=64)
+    ref_plan = ps.ConvPlan(p, mode="3xtf32", device=0, recipe="gpu=bn:128,box:4x4x8,cl:1")
+    plan = ps.ConvPlan(p, mode="3xtf32", device=0, recipe="gpu=bn:128,box:4x4x8,cl:1,os:8")
+    assert "os:8" in plan.recipe
+    y0 = torch.zeros(p.output_elems(), device=dev)
+    y1 = torch.zeros(p.output_elems(), device=dev)
+    ref_plan.forward(x, w, y0, img_begin=7, img_count=80)
+    plan.forward(x, w, y1, img_begin=7, img_count=80)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1), "os:8 changes the result of an image sub-range"
+    hy = torch.zeros(p.output_elems()).pin_memory()
+    plan.forward_host(x.cpu().pin_memory(), w.cpu().pin_memory(), hy, img_begin=7, img_count=80)
+    torch.cuda.synchronize()
+    assert torch.equal(hy, y0.cpu()), "os:8 host path differs from the device path"
+    y2 = torch.zeros(p.output_elems(), device=dev)
+    plan.prepack(w)
+    g = plan.graph(x, None, y2)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    plan.forward(x, w, y0)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y0), "os:8 graph replay differs from the eager call"
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_forward_host(accumulate):
     """conv_fwd_host: host buffers streamed through the device in double-buffered chunks
@@ -205,7 +240,7 @@ def test_forward_host(accumulate):
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
 @pytest.mark.parametrize("relu", [False, True])
-@pytest.mark.parametrize("recipe", [None, "gpu=bn:64,halo:1"])
+@pytest.mark.parametrize("recipe", [None, "gpu=bn:64,halo:1", "gpu=bn:64,box:4x4x8,os:8"])
 def test_fused_bias_relu(mode, relu, recipe):
     """fused epilogue out = max(conv + bias, 0) against the oracle conv
     with the same bias / ReLU applied on the host (3xTF32 uses several accumulation chunks)."""
