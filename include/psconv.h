@@ -230,6 +230,11 @@ int64_t conv_emit_driver(const conv_desc* d, const char* recipe, char* buf, size
  * NULL). Returns the number written, or -2 / -1 on config / runtime error.
  */
 int conv_select_topk(const conv_desc* d, int mode, int k, char* buf, size_t len, double* us_out);
+/* The same with the caller's assertion that only the first c_logical of the nIfm input channels
+ * are non-zero (0 = all; the descriptor cannot carry it): with c_logical <= 4 and nIfm = 16 the
+ * few-channel kernel's recipes (gpu=...,pp:C -- the ResNet stem) join the ranking. */
+int conv_select_topk_ex(const conv_desc* d, int mode, int c_logical, int k, char* buf, size_t len,
+                        double* us_out);
 
 /* ---------------------------------------------------------------------------
  * Pairwise DNN ranker (PolyScientist-DNN; reference

@@ -404,7 +404,7 @@ def emit_driver(preset: ConvPreset, recipe: str | None = None) -> str:
 
 
 def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5, ranker: str = "cost",
-                weights: str | None = None):
+                weights: str | None = None, c_logical: int = 0):
     """Ranked recipes, best first: [(recipe, modelled_us), ...]. ranker="cost" sorts by the
     closed-form model (costrank.hpp:31-40 analogue); ranker="dnn" runs the pairwise-net
     tournament with `weights` (pairnet text; default: the shipped B200 weights)."""
@@ -422,7 +422,9 @@ def select_topk(preset: ConvPreset, mode="3xtf32", k: int = 5, ranker: str = "co
         mname = {v: k for k, v in _MODES.items()}[mode]
         return [(r, model_us(preset, r, mname)) for r in ids]
     us = (ctypes.c_double * k)()
-    n = lib.conv_select_topk(ctypes.byref(d), mode, k, buf, len(buf), us)
+    # (c_logical: the caller's assertion that only that many input channels are non-zero --
+    # lets the model rank the few-channel kernel, recipe pp:C)
+    n = lib.conv_select_topk_ex(ctypes.byref(d), mode, int(c_logical), k, buf, len(buf), us)
     if n < 0:
         _check(-n)
     ids = buf.value.decode().split("\n") if n else []

@@ -77,6 +77,8 @@ _sigs = {
     "conv_select_topk": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                         ctypes.c_size_t, _P(ctypes.c_double)]),
     "conv_model_us": (ctypes.c_double, [_P(conv_desc), ctypes.c_int, ctypes.c_char_p]),
+    "conv_select_topk_ex": (ctypes.c_int, [_P(conv_desc), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_char_p, ctypes.c_size_t, _P(ctypes.c_double)]),
     "conv_select_set_machine": (ctypes.c_int, [ctypes.c_char_p]),
     "conv_fill_input": (ctypes.c_int, [_P(conv_desc), ctypes.c_uint64, c_i64, c_vp, c_i64, c_i64,
                                        c_vp]),

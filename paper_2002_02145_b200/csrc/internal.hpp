@@ -150,7 +150,7 @@ struct ModelBreakdown {
   int64_t m_tiles, tiles;
 };
 ModelBreakdown model_schedule(const conv_desc& d, const Schedule& s, int mode);
-std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode);
+std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode, int c_logical = 0);
 // The four per-variant statistics of the pairwise ranker (mirrors VariantStats,
 // dnnrank.hpp:17-24, with B200 resources instead of cache levels).
 void model_stats(const conv_desc& d, const Schedule& s, int mode, double out[4]);

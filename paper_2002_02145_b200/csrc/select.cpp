@@ -304,7 +304,7 @@ void model_stats(const conv_desc& d, const Schedule& s, int mode, double out[4])
   out[3] = b.us_hbm;
 }
 
-std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
+std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode, int c_logical) {
   std::vector<Schedule> out;
   std::set<std::string> seen;
   std::vector<int> bns;
@@ -378,6 +378,21 @@ std::vector<Schedule> candidate_schedules(const conv_desc& d, int mode) {
           } catch (const ConfigError&) {
           }
         }
+  // few-channel kernel (conv_pp.cuh): only when the caller asserts <= 4 real input channels
+  if (c_logical > 0 && c_logical <= 4 && d.nIfm == 16)
+    for (int bn : {64, 128}) {
+      if (d.nOfm % bn) continue;
+      Recipe r = Recipe::parse(std::string("perm=") + kPerms[1]);
+      r.has_gpu = true;
+      r.bn = bn;
+      r.pp = c_logical;
+      try {
+        Schedule s = resolve_schedule(d, r, mode);
+        if (seen.insert(s.recipe_id).second) out.push_back(s);
+      } catch (const ConfigError&) {
+        // (strides, taps or the resident filter rule it out)
+      }
+    }
   return out;
 }
 
@@ -388,12 +403,16 @@ using namespace psconv;
 extern "C" {
 
 int conv_select_topk(const conv_desc* d_in, int mode, int k, char* buf, size_t len, double* us) {
+  return conv_select_topk_ex(d_in, mode, 0, k, buf, len, us);
+}
+
+int conv_select_topk_ex(const conv_desc* d_in, int mode, int c_logical, int k, char* buf, size_t len, double* us) {
   int written = 0;
   const int rc = guarded([&] {
-    if (!d_in || !buf || k < 1) throw ConfigError("bad argument");
+    if (!d_in || !buf || k < 1 || c_logical < 0) throw ConfigError("bad argument");
     conv_desc d = *d_in;
     validate_desc(d);
-    auto cands = candidate_schedules(d, mode);
+    auto cands = candidate_schedules(d, mode, c_logical);
     if (cands.empty()) throw ConfigError("no GPU schedule for this descriptor");
     std::vector<std::pair<double, std::string>> scored;
     for (const auto& s : cands) scored.emplace_back(model_schedule(d, s, mode).us_total, s.recipe_id);

@@ -36,7 +36,7 @@ def lookup(preset: ConvPreset, mode: str, path: str | None = None) -> str | None
 
 
 def _variants(preset: ConvPreset, mode: str, k: int, c_logical: int = 0) -> list[str]:
-    ranked = [r for r, _ in select_topk(preset, mode, k)]
+    ranked = [r for r, _ in select_topk(preset, mode, k, c_logical=c_logical if 0 < c_logical < preset.nIfm else 0)]
     out = list(ranked)
     base = ranked[0]
     head, gpu = base.split(";gpu=")

@@ -144,6 +144,20 @@ def test_output_staging_recipe_key():
             ps.model_us(p, bad, "tf32")
 
 
+def test_select_topk_with_real_channel_count():
+    """conv_select_topk_ex: with the caller's assertion that only 3 of the 16 input channels are
+    real, the few-channel kernel's recipe joins the ranking (and wins on the ResNet stem);
+    without it the descriptor alone never yields pp:."""
+    stem = ConvPreset.parse("conv:256,64,16,112,112,7,7,2,2,16,3,3,224,224")
+    for mode in ("3xtf32", "tf32"):
+        assert all("pp:" not in r for r, _ in ps.select_topk(stem, mode, 8))
+        top, us = ps.select_topk(stem, mode, 2, c_logical=3)[0]
+        assert "pp:3" in top and us > 0
+    # a 64-channel layer ignores the hint
+    p = ConvPreset.parse("conv:8,64,64,8,8,3,3,1,1,16,1,1,8,8")
+    assert ps.select_topk(p, "tf32", 3, c_logical=3) == ps.select_topk(p, "tf32", 3)
+
+
 def test_parity_plane_recipe_key():
     """pp:C (few-channel kernel): accepted for C <= 4 real channels of one 16-channel block,
     stride 1 or 2, 2..64 taps; canonical id pins the 8x16 pixel tile; modelled far below the

@@ -1,5 +1,6 @@
 """Selector quality: the closed-form model's own top-1 recipe (select_topk, no tuning) timed against
-the plan cache's measured best on every bench workload and mode, interleaved on one box
+the plan cache's measured best on every bench workload and mode (the stem with the caller's
+assertion of 3 real input channels, select_topk(c_logical=3)), interleaved on one box
 (prepacked filter, L2 flushed, median of 7).  python tools/selector_top1.py > profiles/r02_selector_top1.md"""
 import math
 import os
@@ -32,7 +33,7 @@ def main():
         ps.fill_input(p, sx, x, c_logical=c_log)
         ps.fill_filter(p, sw, w, c_logical=c_log)
         for mode in ("3xtf32", "tf32"):
-            top = ps.select_topk(p, mode, 1)[0][0]
+            top = ps.select_topk(p, mode, 1, c_logical=c_log if c_log < p.nIfm else 0)[0][0]
             best = tune.lookup(p, mode) or top
             plans = []
             for rid in (top, best):
